@@ -1,0 +1,360 @@
+"""Op table, shape inference and eager f64 semantics (ORACLE — test infrastructure only).
+
+Type layer: "defines the different supported operations as a variant type.
+An operation can be parametrised by arguments (for instance, Conv2d of
+padding * int array)".  Shape layer: "infer the shape of the
+output value of each operation, given the shape of its inputs".
+Evaluation: "evaluation functions for all the operators defined in the Type
+functor".
+
+Numerics: inputs are fp32; every node computes in float64
+and rounds once to fp32 (round-to-nearest).  SUM/MAX, DOT and CONV accumulate
+in f64 over the whole reduction and round once.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class CGError(Exception):
+    """Mirror of the C-ABI error codes (include/cg.h)."""
+
+    def __init__(self, code: str, msg: str):
+        super().__init__(f"{code}: {msg}")
+        self.code = code
+
+
+UNARY = ("NEG", "ABS", "SQRT", "EXP", "LOG", "SIN", "COS", "TANH", "RELU")
+BINARY = ("ADD", "SUB", "MUL", "DIV", "POW", "MAX2", "MIN2", "RELU_GRAD")
+TERNARY = ("FMA",)
+EW = frozenset(UNARY + BINARY + TERNARY)
+RED = frozenset(("SUM", "MAX"))
+COMMUTATIVE = frozenset(("ADD", "MUL", "MAX2", "MIN2"))
+LEAF = frozenset(("VAR", "CONST"))
+
+# arity: fixed per tag; CONCAT is variadic (>= 1).
+ARITY = {"VAR": 0, "CONST": 0, "SUM": 1, "MAX": 1, "DOT": 2, "CONV2D": 2,
+         "CONV2D_BWD_INPUT": 2, "CONV2D_BWD_KERNEL": 2, "MAXPOOL2D": 1, "MAXPOOL2D_BWD": 2,
+         "AVGPOOL2D": 1, "RESHAPE": 1, "ALLREDUCE_SUM": 1, "CONCAT": -1}
+for _o in UNARY:
+    ARITY[_o] = 1
+for _o in BINARY:
+    ARITY[_o] = 2
+ARITY["FMA"] = 3
+OPS = tuple(ARITY)
+
+# integer attributes each op carries (canonical keys; the structural JSON dump lists exactly these)
+ATTR_KEYS = {"SUM": ("a0", "a1"), "MAX": ("a0", "a1"), "DOT": ("ta", "tb"),
+             "CONV2D": ("pad", "sh", "sw"), "CONV2D_BWD_INPUT": ("h", "pad", "sh", "sw", "w"),
+             "CONV2D_BWD_KERNEL": ("kh", "kw", "pad", "sh", "sw"),
+             "MAXPOOL2D": ("kh", "kw", "pad", "sh", "sw"), "MAXPOOL2D_BWD": ("kh", "kw", "pad", "sh", "sw"),
+             "AVGPOOL2D": ("kh", "kw", "pad", "sh", "sw"), "CONCAT": ("axis",), "RESHAPE": ("dims",)}
+
+
+def numel(shape) -> int:
+    n = 1
+    for d in shape:
+        n *= int(d)
+    return n
+
+
+def broadcast_shape(*shapes):
+    """numpy trailing-dimension broadcasting."""
+    rank = max(len(s) for s in shapes)
+    out = []
+    for k in range(rank):
+        ext = 1
+        for s in shapes:
+            j = k - (rank - len(s))
+            if j < 0:
+                continue
+            d = int(s[j])
+            if d == 1:
+                continue
+            if ext == 1:
+                ext = d
+            elif ext != d:
+                raise CGError("CG_E_SHAPE", f"cannot broadcast {list(map(list, shapes))}")
+        out.append(ext)
+    return tuple(out)
+
+
+def conv_out(h, k, s, pad):
+    """TF/Owl padding (SURVEY §8(c) "Padding convention"): returns (out, pad_before)."""
+    if pad == 1:  # SAME
+        o = -(-h // s)
+        tot = max((o - 1) * s + k - h, 0)
+        return o, tot // 2
+    if h < k:
+        raise CGError("CG_E_SHAPE", f"VALID window {k} larger than input {h}")
+    return (h - k) // s + 1, 0
+
+
+def infer_shape(op: str, in_shapes, attrs) -> tuple:
+    """Output shape of ``op``.  Raises CGError("CG_E_SHAPE") on mismatch."""
+    a = attrs
+    if op in EW:
+        return broadcast_shape(*in_shapes)
+    if op in RED:
+        (x,) = in_shapes
+        a0, a1 = int(a["a0"]), int(a["a1"])
+        if not (0 <= a0 < a1 <= len(x)):
+            raise CGError("CG_E_SHAPE", f"reduction axes [{a0},{a1}) invalid for rank {len(x)}")
+        return tuple(1 if a0 <= k < a1 else int(d) for k, d in enumerate(x))
+    if op == "DOT":
+        A, B = in_shapes
+        if len(A) != 2 or len(B) != 2:
+            raise CGError("CG_E_SHAPE", "DOT needs rank-2 operands")
+        m, k = (A[1], A[0]) if a["ta"] else (A[0], A[1])
+        k2, n = (B[1], B[0]) if a["tb"] else (B[0], B[1])
+        if k != k2:
+            raise CGError("CG_E_SHAPE", f"DOT inner dims {k} != {k2}")
+        return (int(m), int(n))
+    if op == "CONV2D":
+        x, w = in_shapes
+        if len(x) != 4 or len(w) != 4 or x[3] != w[2]:
+            raise CGError("CG_E_SHAPE", f"CONV2D x{list(x)} w{list(w)}")
+        ho, _ = conv_out(x[1], w[0], a["sh"], a["pad"])
+        wo, _ = conv_out(x[2], w[1], a["sw"], a["pad"])
+        return (int(x[0]), ho, wo, int(w[3]))
+    if op == "CONV2D_BWD_INPUT":
+        dy, w = in_shapes
+        if len(dy) != 4 or len(w) != 4 or dy[3] != w[3]:
+            raise CGError("CG_E_SHAPE", f"CONV2D_BWD_INPUT dy{list(dy)} w{list(w)}")
+        ho, _ = conv_out(a["h"], w[0], a["sh"], a["pad"])
+        wo, _ = conv_out(a["w"], w[1], a["sw"], a["pad"])
+        if (ho, wo) != (dy[1], dy[2]):
+            raise CGError("CG_E_SHAPE", "CONV2D_BWD_INPUT spatial mismatch")
+        return (int(dy[0]), int(a["h"]), int(a["w"]), int(w[2]))
+    if op == "CONV2D_BWD_KERNEL":
+        x, dy = in_shapes
+        if len(x) != 4 or len(dy) != 4 or x[0] != dy[0]:
+            raise CGError("CG_E_SHAPE", f"CONV2D_BWD_KERNEL x{list(x)} dy{list(dy)}")
+        ho, _ = conv_out(x[1], a["kh"], a["sh"], a["pad"])
+        wo, _ = conv_out(x[2], a["kw"], a["sw"], a["pad"])
+        if (ho, wo) != (dy[1], dy[2]):
+            raise CGError("CG_E_SHAPE", "CONV2D_BWD_KERNEL spatial mismatch")
+        return (int(a["kh"]), int(a["kw"]), int(x[3]), int(dy[3]))
+    if op in ("MAXPOOL2D", "AVGPOOL2D"):
+        (x,) = in_shapes
+        if len(x) != 4:
+            raise CGError("CG_E_SHAPE", "pool needs NHWC")
+        ho, _ = conv_out(x[1], a["kh"], a["sh"], a["pad"])
+        wo, _ = conv_out(x[2], a["kw"], a["sw"], a["pad"])
+        return (int(x[0]), ho, wo, int(x[3]))
+    if op == "MAXPOOL2D_BWD":
+        x, dy = in_shapes
+        exp = infer_shape("MAXPOOL2D", [x], a)
+        if tuple(dy) != exp:
+            raise CGError("CG_E_SHAPE", "MAXPOOL2D_BWD dy shape mismatch")
+        return tuple(int(d) for d in x)
+    if op == "CONCAT":
+        ax = int(a["axis"])
+        r = len(in_shapes[0])
+        if not 0 <= ax < r:
+            raise CGError("CG_E_SHAPE", "CONCAT axis")
+        tot = 0
+        for s in in_shapes:
+            if len(s) != r or any(int(s[k]) != int(in_shapes[0][k]) for k in range(r) if k != ax):
+                raise CGError("CG_E_SHAPE", "CONCAT shapes")
+            tot += int(s[ax])
+        return tuple(tot if k == ax else int(in_shapes[0][k]) for k in range(r))
+    if op == "RESHAPE":
+        (x,) = in_shapes
+        dims = tuple(int(d) for d in a["dims"])
+        if any(d < 1 for d in dims) or numel(dims) != numel(x):
+            raise CGError("CG_E_SHAPE", f"RESHAPE {list(x)} -> {list(dims)} changes element count")
+        return dims
+    if op == "ALLREDUCE_SUM":
+        return tuple(in_shapes[0])
+    raise CGError("CG_E_ARITY", f"unknown op {op}")
+
+
+# ---------------------------------------------------------------------------
+# eager semantics, f64 compute, one rounding to fp32
+# ---------------------------------------------------------------------------
+
+def _f64(x):
+    return np.asarray(x, dtype=np.float64)
+
+
+def _pad_nhwc(x, pt, pb, pl, pr, fill):
+    n, h, w, c = x.shape
+    out = np.full((n, h + pt + pb, w + pl + pr, c), fill, dtype=x.dtype)
+    out[:, pt:pt + h, pl:pl + w, :] = x
+    return out
+
+
+def _pads(h, w, kh, kw, sh, sw, pad):
+    ho, pt = conv_out(h, kh, sh, pad)
+    wo, pl = conv_out(w, kw, sw, pad)
+    pb = max((ho - 1) * sh + kh - h - pt, 0)
+    pr = max((wo - 1) * sw + kw - w - pl, 0)
+    return ho, wo, pt, pb, pl, pr
+
+
+def conv2d_f64(x, w, sh, sw, pad):
+    """y[n,ho,wo,co] = sum_{kh,kw,ci} x[n, ho*sh+kh-pt, wo*sw+kw-pl, ci] * w[kh,kw,ci,co], zero outside."""
+    n, h, wd, ci = x.shape
+    KH, KW, _, co = w.shape
+    ho, wo, pt, pb, pl, pr = _pads(h, wd, KH, KW, sh, sw, pad)
+    xp = _pad_nhwc(x, pt, pb, pl, pr, 0.0)
+    y = np.zeros((n, ho, wo, co), dtype=np.float64)
+    for kh in range(KH):
+        for kw in range(KW):
+            patch = xp[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :]
+            y += (patch.reshape(-1, ci) @ w[kh, kw]).reshape(n, ho, wo, co)
+    return y
+
+
+def conv2d_bwd_input_f64(dy, w, h, wd, sh, sw, pad):
+    """dx[n,h,w,ci] = sum dy[n,ho,wo,co] * w[kh,kw,ci,co] over h = ho*sh+kh-pt, w = wo*sw+kw-pl."""
+    n, ho, wo, co = dy.shape
+    KH, KW, ci, _ = w.shape
+    _, _, pt, pb, pl, pr = _pads(h, wd, KH, KW, sh, sw, pad)
+    dxp = np.zeros((n, h + pt + pb, wd + pl + pr, ci), dtype=np.float64)
+    for kh in range(KH):
+        for kw in range(KW):
+            contrib = (dy.reshape(-1, co) @ w[kh, kw].T).reshape(n, ho, wo, ci)
+            dxp[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :] += contrib
+    return dxp[:, pt:pt + h, pl:pl + wd, :]
+
+
+def conv2d_bwd_kernel_f64(x, dy, KH, KW, sh, sw, pad):
+    """dw[kh,kw,ci,co] = sum_{n,ho,wo} x[n, ho*sh+kh-pt, wo*sw+kw-pl, ci] * dy[n,ho,wo,co]."""
+    n, h, wd, ci = x.shape
+    _, ho, wo, co = dy.shape
+    _, _, pt, pb, pl, pr = _pads(h, wd, KH, KW, sh, sw, pad)
+    xp = _pad_nhwc(x, pt, pb, pl, pr, 0.0)
+    dw = np.zeros((KH, KW, ci, co), dtype=np.float64)
+    d2 = dy.reshape(-1, co)
+    for kh in range(KH):
+        for kw in range(KW):
+            patch = xp[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :]
+            dw[kh, kw] = patch.reshape(-1, ci).T @ d2
+    return dw
+
+
+def maxpool_f64(x, KH, KW, sh, sw, pad):
+    """Window max; SAME pads with -inf."""
+    n, h, wd, c = x.shape
+    ho, wo, pt, pb, pl, pr = _pads(h, wd, KH, KW, sh, sw, pad)
+    xp = _pad_nhwc(x, pt, pb, pl, pr, -np.inf)
+    y = np.full((n, ho, wo, c), -np.inf)
+    for kh in range(KH):
+        for kw in range(KW):
+            y = np.maximum(y, xp[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :])
+    return y
+
+
+def maxpool_bwd_f64(x, dy, KH, KW, sh, sw, pad):
+    """Each window's dy goes to the FIRST maximal element in row-major window order
+    (kh outer, kw inner); overlapping windows accumulate."""
+    n, h, wd, c = x.shape
+    ho, wo, pt, pb, pl, pr = _pads(h, wd, KH, KW, sh, sw, pad)
+    xp = _pad_nhwc(x, pt, pb, pl, pr, -np.inf)
+    m = maxpool_f64(x, KH, KW, sh, sw, pad)
+    taken = np.zeros((n, ho, wo, c), dtype=bool)
+    dxp = np.zeros(xp.shape, dtype=np.float64)
+    for kh in range(KH):
+        for kw in range(KW):
+            win = xp[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :]
+            hit = (win == m) & ~taken
+            taken |= hit
+            dxp[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :] += np.where(hit, dy, 0.0)
+    return dxp[:, pt:pt + h, pl:pl + wd, :]
+
+
+def avgpool_f64(x, KH, KW, sh, sw, pad):
+    """Mean over in-bounds elements only (SAME excludes padding from the divisor)."""
+    n, h, wd, c = x.shape
+    ho, wo, pt, pb, pl, pr = _pads(h, wd, KH, KW, sh, sw, pad)
+    xp = _pad_nhwc(x, pt, pb, pl, pr, 0.0)
+    ones = _pad_nhwc(np.ones((1, h, wd, 1)), pt, pb, pl, pr, 0.0)
+    s = np.zeros((n, ho, wo, c))
+    cnt = np.zeros((1, ho, wo, 1))
+    for kh in range(KH):
+        for kw in range(KW):
+            s += xp[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :]
+            cnt += ones[:, kh:kh + (ho - 1) * sh + 1:sh, kw:kw + (wo - 1) * sw + 1:sw, :]
+    return s / cnt
+
+
+def eval_op(op: str, ins, attrs, out_shape, dtype=np.float32):
+    """Evaluate one node: fp32 inputs -> f64 compute -> one rounding to fp32 (c1).
+
+    ``dtype=np.float64`` keeps full f64 storage (used only by the finite-difference
+    pins of the hand-written backward graphs)."""
+    a = attrs
+    x = [_f64(v) for v in ins]
+    if op == "ADD":
+        r = x[0] + x[1]
+    elif op == "SUB":
+        r = x[0] - x[1]
+    elif op == "MUL":
+        r = x[0] * x[1]
+    elif op == "DIV":
+        with np.errstate(divide="ignore", invalid="ignore"):
+            r = x[0] / x[1]
+    elif op == "POW":
+        with np.errstate(divide="ignore", invalid="ignore", over="ignore"):
+            r = np.power(x[0], x[1])
+    elif op == "MAX2":
+        r = np.maximum(x[0], x[1])
+    elif op == "MIN2":
+        r = np.minimum(x[0], x[1])
+    elif op == "RELU_GRAD":
+        r = np.where(x[0] > 0, x[1], 0.0)
+    elif op == "FMA":
+        r = x[0] * x[1] + x[2]
+    elif op == "NEG":
+        r = -x[0]
+    elif op == "ABS":
+        r = np.abs(x[0])
+    elif op == "SQRT":
+        with np.errstate(invalid="ignore"):
+            r = np.sqrt(x[0])
+    elif op == "EXP":
+        with np.errstate(over="ignore"):
+            r = np.exp(x[0])
+    elif op == "LOG":
+        with np.errstate(divide="ignore", invalid="ignore"):
+            r = np.log(x[0])
+    elif op == "SIN":
+        r = np.sin(x[0])
+    elif op == "COS":
+        r = np.cos(x[0])
+    elif op == "TANH":
+        r = np.tanh(x[0])
+    elif op == "RELU":
+        r = np.where(x[0] > 0, x[0], 0.0)
+    elif op == "SUM":
+        r = np.sum(x[0], axis=tuple(range(a["a0"], a["a1"])), keepdims=True)
+    elif op == "MAX":
+        r = np.max(x[0], axis=tuple(range(a["a0"], a["a1"])), keepdims=True)
+    elif op == "DOT":
+        A = x[0].T if a["ta"] else x[0]
+        B = x[1].T if a["tb"] else x[1]
+        r = A @ B
+    elif op == "CONV2D":
+        r = conv2d_f64(x[0], x[1], a["sh"], a["sw"], a["pad"])
+    elif op == "CONV2D_BWD_INPUT":
+        r = conv2d_bwd_input_f64(x[0], x[1], a["h"], a["w"], a["sh"], a["sw"], a["pad"])
+    elif op == "CONV2D_BWD_KERNEL":
+        r = conv2d_bwd_kernel_f64(x[0], x[1], a["kh"], a["kw"], a["sh"], a["sw"], a["pad"])
+    elif op == "MAXPOOL2D":
+        r = maxpool_f64(x[0], a["kh"], a["kw"], a["sh"], a["sw"], a["pad"])
+    elif op == "MAXPOOL2D_BWD":
+        r = maxpool_bwd_f64(x[0], x[1], a["kh"], a["kw"], a["sh"], a["sw"], a["pad"])
+    elif op == "AVGPOOL2D":
+        r = avgpool_f64(x[0], a["kh"], a["kw"], a["sh"], a["sw"], a["pad"])
+    elif op == "CONCAT":
+        r = np.concatenate(x, axis=a["axis"])
+    elif op == "RESHAPE":
+        r = x[0].reshape(tuple(a["dims"]))
+    elif op == "ALLREDUCE_SUM":
+        r = x[0]  # world == 1: sum over one rank
+    else:
+        raise CGError("CG_E_ARITY", f"no evaluation function for {op}")
+    r = np.broadcast_to(r, out_shape) if r.shape != tuple(out_shape) else r
+    return np.array(r, dtype=dtype, order="C")
