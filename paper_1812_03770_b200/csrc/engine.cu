@@ -1,0 +1,879 @@
+// Executor and C ABI (include/cg.h).
+//
+// Device-dependent half of the paper's design [Engine + Device layers,
+// P:286-367]: memory initialisation with Algorithm 1 lives in host.cpp; this
+// file allocates the pool (one device allocation, every value a view at offset
+// 0 of its block), compiles one kernel per fused group with NVRTC
+// for sm_100a, evaluates groups in Gamma order [P:366-367], applies the update
+// edges in one pass [update_iopair, P:283], and re-evaluates incrementally
+// [P:25, P:42] with the validity / clobber fix-point of DESIGN.md ("c9").
+// Full evaluations replay a captured CUDA graph.
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/cg.h"
+#include "codegen.h"
+#include "host.h"
+#include "kernels.h"
+
+using namespace cg;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+// ---------------------------------------------------------------- NCCL (dlopen: no link-time dependency)
+struct Nccl {
+  void* h = nullptr;
+  int (*GetUniqueId)(void*) = nullptr;
+  int (*CommInitRank)(void**, int, char[128], int) = nullptr;  // (comm*, nranks, uniqueId by value, rank)
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool load(std::string* err) {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { *err = "cannot dlopen libnccl.so.2"; return false; }
+    GetUniqueId = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (int (*)(void**, int, char[128], int))dlsym(h, "ncclCommInitRank");
+    AllReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
+    CommDestroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy) { *err = "libnccl lacks symbols"; return false; }
+    return true;
+  }
+};
+Nccl g_nccl;
+struct NcclUid { char b[128]; };
+// ncclCommInitRank takes ncclUniqueId BY VALUE (a 128-byte struct)
+typedef int (*CommInitRankFn)(void**, int, NcclUid, int);
+
+// ---------------------------------------------------------------- NVRTC + module cache (process-wide)
+struct KCache {
+  std::mutex mu;
+  std::map<std::string, cudaKernel_t> by_name;  // name = hash of the body
+  std::vector<cudaLibrary_t> libs;
+};
+KCache g_kcache;
+
+int compile_kernel(const KernelSpec& ks, cudaKernel_t* out, std::string* err, bool* fresh) {
+  {
+    std::lock_guard<std::mutex> lk(g_kcache.mu);
+    auto it = g_kcache.by_name.find(ks.name);
+    if (it != g_kcache.by_name.end()) { *out = it->second; *fresh = false; return 0; }
+  }
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, ks.source.c_str(), (ks.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    *err = "nvrtcCreateProgram failed";
+    return CG_E_NVRTC;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-default-device", "--std=c++17", "-lineinfo"};
+  nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    *err = "NVRTC failed for " + ks.name + ": " + log;
+    return CG_E_NVRTC;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  std::vector<char> cubin(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  cudaLibrary_t lib;
+  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e != cudaSuccess) { *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e); return CG_E_CUDA; }
+  cudaKernel_t k;
+  e = cudaLibraryGetKernel(&k, lib, ks.name.c_str());
+  if (e != cudaSuccess) { *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e); return CG_E_CUDA; }
+  std::lock_guard<std::mutex> lk(g_kcache.mu);
+  g_kcache.by_name[ks.name] = k;
+  g_kcache.libs.push_back(lib);
+  *out = k;
+  *fresh = true;
+  return 0;
+}
+
+struct Launch {
+  std::function<cudaError_t(cudaStream_t)> fn;
+  int kernels = 1;  // device kernels this step launches
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------- the graph object
+struct cg_graph {
+  HostGraph hg;
+  int device = -1;
+  bool host_only = true;
+  cudaStream_t user_stream = nullptr;  // caller's stream (may be the legacy default)
+  cudaStream_t stream = nullptr;       // internal work stream (capturable)
+  cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  int state = 0;  // 0 BUILD, 1 OPTIMISED, 2 PLANNED
+  std::string err;
+  int rank = 0, world = 1;
+  void* comm = nullptr;
+  int num_sms = 148;
+  // memory
+  char* pool = nullptr;
+  char* arena = nullptr;
+  float* ws = nullptr;
+  size_t ws_floats = 0;
+  std::vector<float*> ptr;  // node -> device storage
+  // launches
+  std::vector<std::vector<Launch>> glaunch;
+  CopyDesc* upd_dev = nullptr;
+  int n_upd = 0;
+  long long upd_max = 0;
+  CopyDesc* stage_dev = nullptr;
+  int n_stage = 0;
+  long long stage_max = 0;
+  float* stage_buf = nullptr;
+  // incremental state
+  std::vector<char> dirty;
+  std::vector<int> owner;  // block -> node currently stored there (-1 none)
+  std::vector<int64_t> count;
+  // CUDA graph of a full evaluation
+  cudaGraphExec_t exec_full = nullptr;
+  bool graph_failed = false;
+  int full_kernels = 0;
+  int64_t launches = 0;
+  int n_kernels = 0;
+  cg_plan_info info{};
+
+  int fail(int code, const std::string& m) {
+    err = m;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* where) {
+    err = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? CG_E_OOM : CG_E_CUDA;
+  }
+  void join_in() {  // work stream waits for everything the caller enqueued so far
+    cudaEventRecord(ev_in, user_stream);
+    cudaStreamWaitEvent(stream, ev_in, 0);
+  }
+  void join_out() {  // caller's stream waits for our work
+    cudaEventRecord(ev_out, stream);
+    cudaStreamWaitEvent(user_stream, ev_out, 0);
+  }
+};
+
+#define CUDA_TRY(g, expr, where)                    \
+  do {                                              \
+    cudaError_t e_ = (expr);                        \
+    if (e_ != cudaSuccess) return (g)->cuda_fail(e_, where); \
+  } while (0)
+
+static cg_attr to_cattr(const Node& nd) {
+  cg_attr a{};
+  a.a0 = nd.attr.a0; a.a1 = nd.attr.a1; a.ta = nd.attr.ta; a.tb = nd.attr.tb;
+  a.sh = nd.attr.sh; a.sw = nd.attr.sw; a.pad = nd.attr.pad; a.kh = nd.attr.kh; a.kw = nd.attr.kw;
+  a.h = nd.attr.h; a.w = nd.attr.w; a.axis = nd.attr.axis;
+  if (nd.op == CG_RESHAPE) {
+    a.ndim = (int)nd.attr.dims.size();
+    for (int k = 0; k < a.ndim; ++k) a.dims[k] = nd.attr.dims[k];
+  } else if (nd.op == CG_CONST || nd.op == CG_VAR) {
+    a.ndim = (int)nd.shape.size();
+    for (int k = 0; k < a.ndim; ++k) a.dims[k] = nd.shape[k];
+    a.host_data = nd.host.empty() ? nullptr : nd.host.data();
+  }
+  return a;
+}
+
+static ConvGeom geom(const Node& nd, const Shape& x, const Shape& y, int kh, int kw) {
+  ConvGeom g{};
+  g.n = (int)x[0]; g.h = (int)x[1]; g.w = (int)x[2]; g.ci = (int)x[3];
+  g.kh = kh; g.kw = kw;
+  g.ho = (int)y[1]; g.wo = (int)y[2]; g.co = (int)y[3];
+  g.sh = nd.attr.sh; g.sw = nd.attr.sw;
+  int th = std::max((g.ho - 1) * g.sh + kh - g.h, 0), tw = std::max((g.wo - 1) * g.sw + kw - g.w, 0);
+  g.pt = nd.attr.pad ? th / 2 : 0;
+  g.pl = nd.attr.pad ? tw / 2 : 0;
+  return g;
+}
+
+// ---------------------------------------------------------------- plan: allocate + build launches
+static int build_launches(cg_graph* g) {
+  HostGraph& hg = g->hg;
+  const int n = (int)hg.nodes.size();
+  g->glaunch.assign(hg.groups.size(), {});
+  size_t ws_need = 0;
+  std::vector<KernelSpec> specs(hg.groups.size());
+  // 1) specs + workspace sizes
+  for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
+    const Group& G = hg.groups[gi];
+    if (G.kind == G_EW || G.kind == G_RED) {
+      specs[gi] = gen_group(hg, G, g->num_sms);
+      ws_need = std::max<size_t>(ws_need, specs[gi].ws_floats);
+    } else if (hg.nodes[G.sink].op == CG_CONV2D_BWD_KERNEL) {
+      const Node& nd = hg.nodes[G.sink];
+      ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
+      ws_need = std::max(ws_need, conv2d_bwd_kernel_ws(cgm, g->num_sms));
+    }
+  }
+  if (ws_need) {
+    CUDA_TRY(g, cudaMalloc(&g->ws, ws_need * sizeof(float)), "cudaMalloc(workspace)");
+    g->ws_floats = ws_need;
+  }
+  // 2) compile + closures
+  std::vector<std::string> seen;
+  for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
+    const Group& G = hg.groups[gi];
+    auto& L = g->glaunch[gi];
+    const Node& nd = hg.nodes[G.sink];
+    if (G.kind == G_EW || G.kind == G_RED) {
+      KernelSpec& ks = specs[gi];
+      cudaKernel_t k;
+      bool fresh = false;
+      int rc = compile_kernel(ks, &k, &g->err, &fresh);
+      if (rc) return rc;
+      if (std::find(seen.begin(), seen.end(), ks.name) == seen.end()) {
+        seen.push_back(ks.name);
+        g->n_kernels++;
+      }
+      std::vector<void*> argv;
+      for (int p : ks.in_ids) argv.push_back(g->ptr[p]);
+      for (int m : ks.out_ids) argv.push_back(g->ptr[m]);
+      if (ks.uses_ws) argv.push_back(g->ws);
+      dim3 grid(ks.grid[0], ks.grid[1], ks.grid[2]);
+      unsigned block = ks.block;
+      auto st = std::make_shared<std::vector<void*>>(argv);
+      L.push_back({[k, grid, block, st](cudaStream_t s) {
+                     std::vector<void*> ap(st->size());
+                     for (size_t i = 0; i < st->size(); ++i) ap[i] = &(*st)[i];
+                     return cudaLaunchKernel((const void*)k, grid, dim3(block), ap.data(), 0, s);
+                   },
+                   1});
+      if (ks.uses_ws) {
+        float* ws = g->ws;
+        float* out = g->ptr[ks.red_out];
+        long long oi = ks.oi, S = ks.splits;
+        int op = ks.red_op == CG_SUM ? 0 : 1;
+        L.push_back({[ws, out, oi, S, op](cudaStream_t s) { return launch_reduce_finalize(ws, out, oi, S, op, s); }, 1});
+      }
+      continue;
+    }
+    float* out = g->ptr[G.sink];
+    std::vector<const float*> in;
+    for (int p : nd.preds) in.push_back(g->ptr[p]);
+    const Shape& ys = nd.shape;
+    switch (nd.op) {
+      case CG_RESHAPE:
+      case CG_ALLREDUCE_SUM: {
+        const float* src = in[0];
+        long long cnt = numel(ys);
+        if (nd.op == CG_ALLREDUCE_SUM && g->world > 1) {
+          void* comm = g->comm;
+          L.push_back({[src, out, cnt, comm](cudaStream_t s) {
+                         int r = g_nccl.AllReduce(src, out, (size_t)cnt, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm, s);
+                         return r == 0 ? cudaSuccess : cudaErrorUnknown;
+                       },
+                       1});
+        } else if (src != out) {  // slid in place -> no work at all
+          L.push_back({[src, out, cnt](cudaStream_t s) { return launch_copy(src, out, cnt, s); }, 1});
+        }
+        break;
+      }
+      case CG_DOT: {
+        const Shape &as = hg.nodes[nd.preds[0]].shape;
+        int M = (int)ys[0], N = (int)ys[1], K = (int)(nd.attr.ta ? as[0] : as[1]);
+        int ta = nd.attr.ta, tb = nd.attr.tb;
+        const float *A = in[0], *B = in[1];
+        L.push_back({[A, B, out, M, N, K, ta, tb](cudaStream_t s) { return launch_dot_simt(A, B, out, M, N, K, ta, tb, s); }, 1});
+        break;
+      }
+      case CG_CONV2D: {
+        ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, ys, (int)hg.nodes[nd.preds[1]].shape[0],
+                            (int)hg.nodes[nd.preds[1]].shape[1]);
+        const float *x = in[0], *w = in[1];
+        L.push_back({[x, w, out, cgm](cudaStream_t s) { return launch_conv2d_fwd(x, w, out, cgm, s); }, 1});
+        break;
+      }
+      case CG_CONV2D_BWD_INPUT: {
+        const Shape& ws = hg.nodes[nd.preds[1]].shape;
+        ConvGeom cgm = geom(nd, ys, hg.nodes[nd.preds[0]].shape, (int)ws[0], (int)ws[1]);
+        const float *dy = in[0], *w = in[1];
+        L.push_back({[dy, w, out, cgm](cudaStream_t s) { return launch_conv2d_bwd_input(dy, w, out, cgm, s); }, 1});
+        break;
+      }
+      case CG_CONV2D_BWD_KERNEL: {
+        ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
+        const float *x = in[0], *dy = in[1];
+        float* ws = g->ws;
+        int sms = g->num_sms;
+        L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv2d_bwd_kernel(x, dy, out, ws, cgm, sms, s); },
+                     2});
+        break;
+      }
+      case CG_MAXPOOL2D:
+      case CG_AVGPOOL2D: {
+        ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, ys, nd.attr.kh, nd.attr.kw);
+        const float* x = in[0];
+        bool mx = nd.op == CG_MAXPOOL2D;
+        L.push_back({[x, out, cgm, mx](cudaStream_t s) { return mx ? launch_maxpool(x, out, cgm, s) : launch_avgpool(x, out, cgm, s); },
+                     1});
+        break;
+      }
+      case CG_MAXPOOL2D_BWD: {
+        ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
+        const float *x = in[0], *dy = in[1];
+        L.push_back({[x, dy, out, cgm](cudaStream_t s) { return launch_maxpool_bwd(x, dy, out, cgm, s); }, 1});
+        break;
+      }
+      case CG_CONCAT: {
+        if ((int)in.size() > kMaxConcat) return g->fail(CG_E_ARG, "CONCAT supports at most 16 inputs");
+        ConcatArgs a{};
+        int ax = nd.attr.axis;
+        long long outer = 1, dst_inner = 1;
+        for (int k = 0; k < ax; ++k) outer *= ys[k];
+        for (size_t k = ax; k < ys.size(); ++k) dst_inner *= ys[k];
+        long long off = 0;
+        for (size_t i = 0; i < in.size(); ++i) {
+          const Shape& s = hg.nodes[nd.preds[i]].shape;
+          long long inner = 1;
+          for (size_t k = ax; k < s.size(); ++k) inner *= s[k];
+          a.src[i] = in[i];
+          a.inner[i] = inner;
+          a.offset[i] = off;
+          off += inner;
+        }
+        a.n = (int)in.size();
+        L.push_back({[a, out, outer, dst_inner](cudaStream_t s) { return launch_concat(a, out, outer, dst_inner, s); }, 1});
+        break;
+      }
+      default:
+        return g->fail(CG_E_ARG, std::string("no kernel for op ") + op_info(nd.op).name);
+    }
+  }
+  (void)n;
+  return 0;
+}
+
+static int setup_updates(cg_graph* g) {
+  HostGraph& hg = g->hg;
+  std::vector<CopyDesc> stage, main;
+  std::vector<char> is_target(hg.nodes.size(), 0);
+  for (auto& e : hg.updates) is_target[e.second] = 1;
+  long long stage_floats = 0;
+  for (auto& e : hg.updates)
+    if (is_target[e.first]) stage_floats += numel(hg.nodes[e.first].shape);
+  if (stage_floats) CUDA_TRY(g, cudaMalloc(&g->stage_buf, stage_floats * sizeof(float)), "cudaMalloc(stage)");
+  long long soff = 0;
+  for (auto& e : hg.updates) {
+    long long cnt = numel(hg.nodes[e.first].shape);
+    const float* src = g->ptr[e.first];
+    if (is_target[e.first]) {  // parallel assignment: stage sources that are themselves targets
+      float* st = g->stage_buf + soff;
+      soff += (cnt + 63) / 64 * 64;
+      stage.push_back({src, st, cnt});
+      src = st;
+      g->stage_max = std::max(g->stage_max, cnt);
+    }
+    if (src == g->ptr[e.second]) continue;
+    main.push_back({src, g->ptr[e.second], cnt});
+    g->upd_max = std::max(g->upd_max, cnt);
+  }
+  if (!stage.empty()) {
+    CUDA_TRY(g, cudaMalloc(&g->stage_dev, stage.size() * sizeof(CopyDesc)), "cudaMalloc");
+    CUDA_TRY(g, cudaMemcpy(g->stage_dev, stage.data(), stage.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice), "cudaMemcpy");
+    g->n_stage = (int)stage.size();
+  }
+  if (!main.empty()) {
+    CUDA_TRY(g, cudaMalloc(&g->upd_dev, main.size() * sizeof(CopyDesc)), "cudaMalloc");
+    CUDA_TRY(g, cudaMemcpy(g->upd_dev, main.data(), main.size() * sizeof(CopyDesc), cudaMemcpyHostToDevice), "cudaMemcpy");
+    g->n_upd = (int)main.size();
+  }
+  return 0;
+}
+
+static int allocate(cg_graph* g) {
+  HostGraph& hg = g->hg;
+  const int n = (int)hg.nodes.size();
+  g->ptr.assign(n, nullptr);
+  // externals: every live Var (assignable even if unused) + Consts reachable from the roots
+  uint64_t ext = 0;
+  std::vector<uint64_t> eoff(n, 0);
+  std::vector<char> has(n, 0);
+  for (int v = 0; v < n; ++v) {
+    const Node& nd = hg.nodes[v];
+    bool live = hg.dead.empty() || !hg.dead[v];
+    if (!live) continue;
+    if (nd.op == CG_VAR || (nd.op == CG_CONST && hg.rank[v] >= 0)) {
+      has[v] = 1;
+      eoff[v] = ext;
+      ext += (4 * (uint64_t)numel(nd.shape) + 255) / 256 * 256;
+    }
+  }
+  if (ext) CUDA_TRY(g, cudaMalloc(&g->arena, ext), "cudaMalloc(externals)");
+  if (hg.pl.pool_bytes) CUDA_TRY(g, cudaMalloc(&g->pool, hg.pl.pool_bytes), "cudaMalloc(pool)");
+  for (int v = 0; v < n; ++v) {
+    const Node& nd = hg.nodes[v];
+    size_t nb = 4 * (size_t)numel(nd.shape);
+    if (has[v]) {
+      g->ptr[v] = reinterpret_cast<float*>(g->arena + eoff[v]);
+      if (!nd.host.empty()) CUDA_TRY(g, cudaMemcpy(g->ptr[v], nd.host.data(), nb, cudaMemcpyHostToDevice), "cudaMemcpy(const)");
+      else CUDA_TRY(g, cudaMemset(g->ptr[v], 0, nb), "cudaMemset(var)");
+    } else if (hg.pl.block_of[v] >= 0) {
+      g->ptr[v] = reinterpret_cast<float*>(g->pool + hg.pl.offset[hg.pl.block_of[v]]);
+    }
+  }
+  g->info.external_bytes = ext;
+  return 0;
+}
+
+// ---------------------------------------------------------------- evaluation
+static bool valid(cg_graph* g, int p) {
+  HostGraph& hg = g->hg;
+  if (hg.is_external(p)) return true;
+  return !g->dirty[p] && g->owner[hg.pl.block_of[p]] == p;
+}
+
+static void mark_dirty_from_var(cg_graph* g, int var) {
+  for (int n : g->hg.desc_of_var[var]) g->dirty[n] = 1;
+}
+
+static int run_launches(cg_graph* g, const std::vector<char>& R, bool full) {
+  HostGraph& hg = g->hg;
+  if (full && !g->graph_failed) {
+    if (!g->exec_full) {  // capture once: Gamma order, static addresses
+      cudaGraph_t graph;
+      bool ok = cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      int kcount = 0;
+      for (size_t gi = 0; ok && gi < hg.groups.size(); ++gi)
+        for (auto& L : g->glaunch[gi]) {
+          if (L.fn(g->stream) != cudaSuccess) ok = false;
+          kcount += L.kernels;
+        }
+      cudaError_t e = cudaStreamEndCapture(g->stream, &graph);
+      ok = ok && e == cudaSuccess;
+      if (ok) {
+        ok = cudaGraphInstantiate(&g->exec_full, graph, 0) == cudaSuccess;
+        cudaGraphDestroy(graph);
+      }
+      cudaGetLastError();
+      if (!ok) {
+        g->exec_full = nullptr;
+        g->graph_failed = true;
+      } else {
+        g->full_kernels = kcount;
+      }
+    }
+    if (g->exec_full) {
+      CUDA_TRY(g, cudaGraphLaunch(g->exec_full, g->stream), "cudaGraphLaunch");
+      g->launches += g->full_kernels;
+      return 0;
+    }
+  }
+  for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
+    if (!R[gi]) continue;
+    for (auto& L : g->glaunch[gi]) {
+      cudaError_t e = L.fn(g->stream);
+      if (e != cudaSuccess) return g->cuda_fail(e, "group launch");
+      g->launches += L.kernels;
+    }
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------- C ABI
+extern "C" {
+
+cg_graph* cg_create(int device, void* cuda_stream, const cg_dist* dist) {
+  auto g = std::make_unique<cg_graph>();
+  if (device >= 0) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev) {
+      g_create_error = "cg_create: no CUDA device " + std::to_string(device);
+      cudaGetLastError();
+      return nullptr;
+    }
+    cudaSetDevice(device);
+    g->device = device;
+    g->host_only = false;
+    g->user_stream = (cudaStream_t)cuda_stream;
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+      g_create_error = "cg_create: cannot create stream/events";
+      return nullptr;
+    }
+    cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (dist && dist->world > 1) {
+      std::string e;
+      if (!g_nccl.load(&e)) { g_create_error = "cg_create: " + e; return nullptr; }
+      if (!dist->nccl_unique_id) { g_create_error = "cg_create: world > 1 needs nccl_unique_id"; return nullptr; }
+      NcclUid uid;
+      memcpy(uid.b, dist->nccl_unique_id, 128);
+      int r = ((CommInitRankFn)g_nccl.CommInitRank)(&g->comm, dist->world, uid, dist->rank);
+      if (r != 0) {
+        g_create_error = std::string("ncclCommInitRank failed: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "");
+        return nullptr;
+      }
+      g->rank = dist->rank;
+      g->world = dist->world;
+    }
+  } else if (dist && dist->world > 1) {
+    g->rank = dist->rank;
+    g->world = dist->world;
+  }
+  return g.release();
+}
+
+cg_node cg_add_node(cg_graph* g, cg_op op, const cg_node* inputs, int32_t n_inputs, const cg_attr* attr) {
+  if (!g) return CG_E_ARG;
+  if (g->state != 0) return g->fail(CG_E_STATE, "cg_add_node after cg_optimise/cg_plan_memory (the graph is static, P:249)");
+  if (n_inputs > 0 && !inputs) return g->fail(CG_E_ARG, "inputs is NULL");
+  Error e{0, ""};
+  int r = g->hg.add_node((int)op, inputs, n_inputs, attr, &e);
+  if (r < 0) g->err = e.msg;
+  return r;
+}
+
+int cg_add_update(cg_graph* g, cg_node u, cg_node var) {
+  if (!g) return CG_E_ARG;
+  if (g->state != 0) return g->fail(CG_E_STATE, "cg_add_update after cg_optimise/cg_plan_memory");
+  Error e{0, ""};
+  int r = g->hg.add_update(u, var, &e);
+  if (r < 0) g->err = e.msg;
+  return r;
+}
+
+int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint32_t flags, cg_plan_info* info);
+int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float** out_dev_ptrs, uint32_t flags);
+int cg_read(cg_graph* g, cg_node node, void* host_dst, size_t nbytes);
+
+int cg_optimise(cg_graph* g, const cg_node* outputs, int32_t n_outputs, cg_report* report) {
+  if (!g) return CG_E_ARG;
+  if (g->state != 0) return g->fail(CG_E_STATE, "cg_optimise called twice or after planning");
+  if (n_outputs <= 0 || !outputs) return g->fail(CG_E_ARG, "cg_optimise needs outputs");
+  std::vector<int> outs(outputs, outputs + n_outputs);
+  std::vector<int> frontier;
+  Error e{0, ""};
+  int r = g->hg.optimise(outs, report, &frontier, &e);
+  if (r < 0) return g->fail(r, e.msg);
+  std::vector<std::vector<float>> values(frontier.size());
+  if (!g->host_only && !frontier.empty()) {
+    // constant folding: evaluate the const cone ONCE, on the device, with the same kernels [P:267]
+    HostGraph& hg = g->hg;
+    std::vector<char> cone(hg.nodes.size(), 0);
+    std::vector<int> st(frontier.begin(), frontier.end());
+    while (!st.empty()) {
+      int v = st.back();
+      st.pop_back();
+      if (cone[v]) continue;
+      cone[v] = 1;
+      for (int p : hg.nodes[v].preds) st.push_back(p);
+    }
+    cg_graph* sub = cg_create(g->device, g->user_stream, nullptr);
+    if (!sub) return g->fail(CG_E_CUDA, g_create_error);
+    std::vector<int> map(hg.nodes.size(), -1);
+    int rc = 0;
+    for (size_t v = 0; v < hg.nodes.size() && rc >= 0; ++v) {
+      if (!cone[v]) continue;
+      const Node& nd = hg.nodes[v];
+      cg_attr a = to_cattr(nd);
+      std::vector<int> in;
+      for (int p : nd.preds) in.push_back(map[p]);
+      rc = cg_add_node(sub, (cg_op)nd.op, in.data(), (int)in.size(), &a);
+      map[v] = rc;
+    }
+    std::vector<int> fo;
+    for (int v : frontier) fo.push_back(map[v]);
+    if (rc >= 0) rc = cg_plan_memory(sub, fo.data(), (int)fo.size(), 0, nullptr);
+    if (rc >= 0) rc = cg_eval(sub, fo.data(), (int)fo.size(), nullptr, 0);
+    for (size_t i = 0; rc >= 0 && i < frontier.size(); ++i) {
+      values[i].resize(numel(hg.nodes[frontier[i]].shape));
+      rc = cg_read(sub, fo[i], values[i].data(), values[i].size() * sizeof(float));
+    }
+    std::string serr = sub->err;
+    cg_destroy(sub);
+    if (rc < 0) return g->fail(rc, "constant folding on device: " + serr);
+  }
+  g->hg.apply_folds(values);
+  g->state = 1;
+  return 0;
+}
+
+int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint32_t flags, cg_plan_info* info) {
+  if (!g) return CG_E_ARG;
+  if (g->state > 1) return g->fail(CG_E_STATE, "cg_plan_memory called twice");
+  if (n_outputs <= 0 || !outputs) return g->fail(CG_E_ARG, "cg_plan_memory needs outputs");
+  if (flags & ~3u) return g->fail(CG_E_ARG, "unknown plan flag");
+  std::vector<int> outs(outputs, outputs + n_outputs);
+  Error e{0, ""};
+  int r = g->hg.plan(outs, flags, &e);
+  if (r < 0) return g->fail(r, e.msg);
+  HostGraph& hg = g->hg;
+  g->info = cg_plan_info{};
+  if (!g->host_only) {
+    if ((r = allocate(g)) < 0) return r;
+    if ((r = build_launches(g)) < 0) return r;
+    if ((r = setup_updates(g)) < 0) return r;
+  }
+  g->dirty.assign(hg.nodes.size(), 1);
+  g->owner.assign(hg.pl.size.size(), -1);
+  g->count.assign(hg.nodes.size(), 0);
+  g->info.n_groups = (int)hg.groups.size();
+  g->info.n_blocks = (int)hg.pl.size.size();
+  g->info.n_kernels = g->n_kernels;
+  g->info.pool_bytes = hg.pl.pool_bytes;
+  g->info.plan_bytes = hg.pl.plan_bytes;
+  g->info.workspace_bytes = g->ws_floats * sizeof(float);
+  g->info.unshared_bytes = hg.unshared_bytes;
+  if (g->host_only) {
+    uint64_t ext = 0;
+    for (int v : hg.gamma)
+      if (hg.is_external(v)) ext += (4 * (uint64_t)numel(hg.nodes[v].shape) + 255) / 256 * 256;
+    g->info.external_bytes = ext;
+  }
+  if (info) *info = g->info;
+  g->state = 2;
+  return 0;
+}
+
+int cg_assign(cg_graph* g, cg_node var, const void* src, size_t nbytes, int src_on_device) {
+  if (!g) return CG_E_ARG;
+  if (g->state != 2) return g->fail(CG_E_STATE, "cg_assign before cg_plan_memory");
+  if (g->host_only) return g->fail(CG_E_NO_DEVICE, "host-only graph");
+  HostGraph& hg = g->hg;
+  if (var < 0 || var >= (int)hg.nodes.size()) return g->fail(CG_E_BAD_NODE, "unknown node");
+  if (hg.nodes[var].op != CG_VAR) return g->fail(CG_E_NOT_VAR, "assign target " + std::to_string(var) + " is not a Var");
+  if (nbytes != 4 * (size_t)numel(hg.nodes[var].shape)) return g->fail(CG_E_SIZE, "byte count != numel*4");
+  if (!src) return g->fail(CG_E_ARG, "src is NULL");
+  g->join_in();
+  CUDA_TRY(g, cudaMemcpyAsync(g->ptr[var], src, nbytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                              g->stream),
+           "cudaMemcpyAsync(assign)");
+  g->join_out();
+  mark_dirty_from_var(g, var);
+  return 0;
+}
+
+int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float** out_dev_ptrs, uint32_t flags) {
+  if (!g) return CG_E_ARG;
+  if (g->state != 2) return g->fail(CG_E_STATE, "cg_eval before cg_plan_memory");
+  if (g->host_only) return g->fail(CG_E_NO_DEVICE, "host-only graph: no evaluation");
+  if (n_outputs < 0 || (n_outputs > 0 && !outputs)) return g->fail(CG_E_ARG, "bad outputs");
+  HostGraph& hg = g->hg;
+  std::vector<int> outs;
+  for (int i = 0; i < n_outputs; ++i) {
+    if (outputs[i] < 0 || outputs[i] >= (int)hg.nodes.size()) return g->fail(CG_E_BAD_NODE, "unknown output");
+    int o = hg.resolve(outputs[i]);
+    if (std::find(hg.outputs.begin(), hg.outputs.end(), o) == hg.outputs.end())
+      return g->fail(CG_E_NOT_PLANNED, "node " + std::to_string(outputs[i]) + " is not a planned output");
+    outs.push_back(o);
+  }
+  const bool no_update = flags & CG_EVAL_NO_UPDATE;
+  std::vector<int> roots = outs;
+  if (!no_update)
+    for (auto& e : hg.updates) roots.push_back(e.first);
+  const size_t NG = hg.groups.size();
+  std::vector<char> R(NG, 0);
+  // demand-driven recompute set
+  std::function<void(int, bool)> demand = [&](int v, bool force) {
+    if (hg.is_external(v)) return;
+    int gi = hg.group_of[v];
+    if (R[gi]) return;
+    if (!force && !(flags & CG_EVAL_FULL) && valid(g, v)) return;
+    R[gi] = 1;
+    for (int p : hg.groups[gi].inputs) demand(p, false);
+  };
+  for (int r : roots) demand(r, false);
+  for (;;) {  // clobber fix-point: a group may not read a block another launched group overwrote
+    std::vector<int> sim = g->owner;
+    int bad = -1;
+    for (size_t gi = 0; gi < NG && bad < 0; ++gi) {
+      if (!R[gi]) continue;
+      for (int p : hg.groups[gi].inputs)
+        if (!hg.is_external(p) && sim[hg.pl.block_of[p]] != p) { bad = p; break; }
+      if (bad >= 0) break;
+      for (int m : hg.groups[gi].materialised) sim[hg.pl.block_of[m]] = m;
+    }
+    if (bad < 0)
+      for (int r : roots)
+        if (!hg.is_external(r) && sim[hg.pl.block_of[r]] != r) { bad = r; break; }
+    if (bad < 0) break;
+    demand(bad, true);
+  }
+  size_t nR = 0;
+  for (char c : R) nR += c;
+  g->join_in();
+  int rc = run_launches(g, R, nR == NG && NG > 0);
+  if (rc < 0) return rc;
+  for (size_t gi = 0; gi < NG; ++gi) {
+    if (!R[gi]) continue;
+    for (int m : hg.groups[gi].materialised) g->owner[hg.pl.block_of[m]] = m;
+    for (int m : hg.groups[gi].members) {
+      g->dirty[m] = 0;
+      g->count[m]++;
+    }
+  }
+  if (!no_update && !hg.updates.empty()) {
+    if (g->n_stage) {
+      CUDA_TRY(g, launch_update_copy(g->stage_dev, g->n_stage, g->stage_max, g->stream), "update stage");
+      g->launches++;
+    }
+    if (g->n_upd) {
+      CUDA_TRY(g, launch_update_copy(g->upd_dev, g->n_upd, g->upd_max, g->stream), "update copy");
+      g->launches++;
+    }
+    for (auto& e : hg.updates) mark_dirty_from_var(g, e.second);
+  }
+  g->join_out();
+  if (out_dev_ptrs)
+    for (size_t i = 0; i < outs.size(); ++i) out_dev_ptrs[i] = g->ptr[outs[i]];
+  if (flags & CG_EVAL_SYNC) CUDA_TRY(g, cudaStreamSynchronize(g->stream), "cudaStreamSynchronize");
+  return 0;
+}
+
+int cg_read(cg_graph* g, cg_node node, void* host_dst, size_t nbytes) {
+  if (!g) return CG_E_ARG;
+  if (g->state != 2) return g->fail(CG_E_STATE, "cg_read before cg_plan_memory");
+  if (g->host_only) return g->fail(CG_E_NO_DEVICE, "host-only graph");
+  HostGraph& hg = g->hg;
+  if (node < 0 || node >= (int)hg.nodes.size()) return g->fail(CG_E_BAD_NODE, "unknown node");
+  int v = hg.resolve(node);
+  if (nbytes != 4 * (size_t)numel(hg.nodes[v].shape)) return g->fail(CG_E_SIZE, "byte count != numel*4");
+  if (!g->ptr[v] || (!hg.is_external(v) && !valid(g, v)))
+    return g->fail(CG_E_NOT_PLANNED, "node " + std::to_string(node) + " holds no current value");
+  g->join_in();
+  CUDA_TRY(g, cudaMemcpyAsync(host_dst, g->ptr[v], nbytes, cudaMemcpyDeviceToHost, g->stream), "cudaMemcpyAsync(read)");
+  CUDA_TRY(g, cudaStreamSynchronize(g->stream), "cudaStreamSynchronize");
+  return 0;
+}
+
+void cg_destroy(cg_graph* g) {
+  if (!g) return;
+  if (!g->host_only) {
+    if (g->stream) cudaStreamSynchronize(g->stream);
+    if (g->exec_full) cudaGraphExecDestroy(g->exec_full);
+    cudaFree(g->pool);
+    cudaFree(g->arena);
+    cudaFree(g->ws);
+    cudaFree(g->upd_dev);
+    cudaFree(g->stage_dev);
+    cudaFree(g->stage_buf);
+    if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);
+    if (g->ev_in) cudaEventDestroy(g->ev_in);
+    if (g->ev_out) cudaEventDestroy(g->ev_out);
+    if (g->stream) cudaStreamDestroy(g->stream);
+  }
+  delete g;
+}
+
+const char* cg_last_error(const cg_graph* g) { return g ? g->err.c_str() : g_create_error.c_str(); }
+
+int cg_nccl_unique_id(void* out128) {
+  std::string e;
+  if (!out128) return CG_E_ARG;
+  if (!g_nccl.load(&e)) { g_create_error = e; return CG_E_NCCL; }
+  return g_nccl.GetUniqueId(out128) == 0 ? 0 : CG_E_NCCL;
+}
+
+int64_t cg_dump_json(cg_graph* g, int what, char* buf, size_t cap) {
+  if (!g) return CG_E_ARG;
+  std::string s;
+  if (what == CG_DUMP_GRAPH) {
+    if (g->state < 1) return g->fail(CG_E_STATE, "graph dump needs cg_optimise");
+    s = g->hg.graph_json();
+  } else if (what == CG_DUMP_PLAN) {
+    if (g->state < 2) return g->fail(CG_E_STATE, "plan dump needs cg_plan_memory");
+    s = g->hg.plan_json();
+  } else {
+    return g->fail(CG_E_ARG, "unknown dump kind");
+  }
+  if (buf && cap) {
+    size_t k = std::min(cap - 1, s.size());
+    memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return (int64_t)s.size();
+}
+
+int64_t cg_eval_count(const cg_graph* g, cg_node node) {
+  if (!g || node < 0 || node >= (int)g->hg.nodes.size() || g->count.empty()) return CG_E_BAD_NODE;
+  return g->count[g->hg.resolve(node)];
+}
+
+int32_t cg_node_shape(const cg_graph* g, cg_node node, int64_t* dims8) {
+  if (!g || node < 0 || node >= (int)g->hg.nodes.size()) return CG_E_BAD_NODE;
+  const Shape& s = g->hg.nodes[node].shape;
+  if (dims8)
+    for (size_t k = 0; k < s.size() && k < 8; ++k) dims8[k] = s[k];
+  return (int32_t)s.size();
+}
+
+int64_t cg_launch_count(const cg_graph* g) { return g ? g->launches : CG_E_ARG; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- debug: codegen check without a GPU
+extern "C" int64_t cgx_codegen_check(cg_graph* g, int num_sms, char* log, size_t cap) {
+  if (!g || g->state != 2) return CG_E_STATE;
+  int64_t ok = 0;
+  std::string all;
+  for (const Group& G : g->hg.groups) {
+    if (G.kind != G_EW && G.kind != G_RED) continue;
+    KernelSpec ks = gen_group(g->hg, G, num_sms);
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, ks.source.c_str(), "check.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return CG_E_NVRTC;
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-default-device", "--std=c++17"};
+    nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+    if (r != NVRTC_SUCCESS) {
+      size_t n = 0;
+      nvrtcGetProgramLogSize(prog, &n);
+      std::string l(n, '\0');
+      nvrtcGetProgramLog(prog, &l[0]);
+      all += "== " + ks.name + " (" + ks.mode + ")\n" + l + "\n--- source ---\n" + ks.source + "\n";
+      nvrtcDestroyProgram(&prog);
+      if (log && cap) {
+        size_t k = std::min(cap - 1, all.size());
+        memcpy(log, all.data(), k);
+        log[k] = 0;
+      }
+      return CG_E_NVRTC;
+    }
+    nvrtcDestroyProgram(&prog);
+    ++ok;
+  }
+  return ok;
+}
+
+extern "C" void* cgx_work_stream(const cg_graph* g) { return g ? (void*)g->stream : nullptr; }
+
+// source of the kernel generated for group `gi` (inspection / profiling notes)
+extern "C" int64_t cgx_kernel_source(cg_graph* g, int gi, int num_sms, char* buf, size_t cap) {
+  if (!g || g->state != 2 || gi < 0 || gi >= (int)g->hg.groups.size()) return CG_E_ARG;
+  const Group& G = g->hg.groups[gi];
+  if (G.kind != G_EW && G.kind != G_RED) return 0;
+  KernelSpec ks = gen_group(g->hg, G, num_sms);
+  std::string s = "// " + ks.name + " mode=" + ks.mode + " grid=" + std::to_string(ks.grid[0]) + "," +
+                  std::to_string(ks.grid[1]) + "," + std::to_string(ks.grid[2]) + " block=" + std::to_string(ks.block) +
+                  "\n" + ks.source;
+  if (buf && cap) {
+    size_t k = std::min(cap - 1, s.size());
+    memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return (int64_t)s.size();
+}

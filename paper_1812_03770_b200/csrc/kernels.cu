@@ -1,0 +1,374 @@
+// Precompiled sm_100a kernels: update-edge copy, copy, split-reduction finalize,
+// SIMT dot, and the NHWC conv / pool / concat family.
+//
+// Definitions follow SURVEY §8(c) c1-defs (the oracle's op semantics):
+//   CONV2D            y[n,ho,wo,co] = sum_{kh,kw,ci} x[n, ho*sh+kh-pt, wo*sw+kw-pl, ci] w[kh,kw,ci,co]
+//   CONV2D_BWD_INPUT  dx[n,h,w,ci]  = sum dy[n,ho,wo,co] w[kh,kw,ci,co], h = ho*sh+kh-pt, w = wo*sw+kw-pl
+//   CONV2D_BWD_KERNEL dw[kh,kw,ci,co] = sum_{n,ho,wo} x[n, ho*sh+kh-pt, wo*sw+kw-pl, ci] dy[n,ho,wo,co]
+//   MAXPOOL2D_BWD     each window's dy goes to its FIRST maximal element (kh outer, kw inner)
+//   AVGPOOL2D         mean over in-bounds window elements
+// All accumulations are sequential per output in a fixed order; no atomics, so
+// results are run-to-run bit-stable.
+#include "kernels.h"
+
+#include <algorithm>
+
+namespace cg {
+
+namespace {
+
+__global__ void update_copy_kernel(const CopyDesc* __restrict__ d) {
+  const CopyDesc e = d[blockIdx.y];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((e.n & 3) == 0) {
+    const float4* s = reinterpret_cast<const float4*>(e.src);
+    float4* o = reinterpret_cast<float4*>(e.dst);
+    for (long long i = t; i < (e.n >> 2); i += stride) o[i] = s[i];
+  } else {
+    for (long long i = t; i < e.n; i += stride) e.dst[i] = e.src[i];
+  }
+}
+
+__global__ void copy_kernel(const float* __restrict__ src, float* __restrict__ dst, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if ((n & 3) == 0) {
+    const float4* s = reinterpret_cast<const float4*>(src);
+    float4* o = reinterpret_cast<float4*>(dst);
+    for (long long i = t; i < (n >> 2); i += stride) o[i] = s[i];
+  } else {
+    for (long long i = t; i < n; i += stride) dst[i] = src[i];
+  }
+}
+
+__global__ void reduce_finalize_kernel(const float* __restrict__ ws, float* __restrict__ out, long long oi, long long S,
+                                       int op) {
+  long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= oi) return;
+  float acc = ws[j];
+  for (long long s = 1; s < S; ++s) {
+    float v = ws[s * oi + j];
+    acc = op == 0 ? __fadd_rn(acc, v) : fmaxf(acc, v);
+  }
+  out[j] = acc;
+}
+
+// 64x64 output tile, 16-deep k slab, 256 threads x (4x4) outputs, fp32 FFMA
+__global__ void __launch_bounds__(256) dot_simt_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                                                      float* __restrict__ C, int M, int N, int K, int ta, int tb) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tr = tid / 16, tc = tid % 16;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int e = tid; e < 64 * 16; e += 256) {
+      int mm, kk;
+      if (ta) { kk = e / 64; mm = e % 64; } else { mm = e / 16; kk = e % 16; }
+      int gm = m0 + mm, gk = k0 + kk;
+      float v = 0.f;
+      if (gm < M && gk < K) v = ta ? A[(long long)gk * M + gm] : A[(long long)gm * K + gk];
+      As[kk][mm] = v;
+      int nn;
+      if (tb) { nn = e / 16; kk = e % 16; } else { kk = e / 64; nn = e % 64; }
+      int gn = n0 + nn;
+      gk = k0 + kk;
+      v = 0.f;
+      if (gn < N && gk < K) v = tb ? B[(long long)gn * K + gk] : B[(long long)gk * N + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tr * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tc * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gm = m0 + tr * 4 + i, gn = n0 + tc * 4 + j;
+      if (gm < M && gn < N) C[(long long)gm * N + gn] = acc[i][j];
+    }
+}
+
+__global__ void conv_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, ConvGeom g,
+                                long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    int co = (int)(t % g.co);
+    long long q = t / g.co;
+    int wo = (int)(q % g.wo);
+    q /= g.wo;
+    int ho = (int)(q % g.ho);
+    int n = (int)(q / g.ho);
+    float acc = 0.f;
+    for (int kh = 0; kh < g.kh; ++kh) {
+      int hi = ho * g.sh + kh - g.pt;
+      if (hi < 0 || hi >= g.h) continue;
+      for (int kw = 0; kw < g.kw; ++kw) {
+        int wi = wo * g.sw + kw - g.pl;
+        if (wi < 0 || wi >= g.w) continue;
+        const float* xp = x + (((long long)n * g.h + hi) * g.w + wi) * g.ci;
+        const float* wp = w + ((long long)(kh * g.kw + kw) * g.ci) * g.co + co;
+        for (int ci = 0; ci < g.ci; ++ci) acc = fmaf(xp[ci], wp[(long long)ci * g.co], acc);
+      }
+    }
+    y[t] = acc;
+  }
+}
+
+__global__ void conv_bwd_input_kernel(const float* __restrict__ dy, const float* __restrict__ w, float* __restrict__ dx,
+                                      ConvGeom g, long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    int ci = (int)(t % g.ci);
+    long long q = t / g.ci;
+    int wi = (int)(q % g.w);
+    q /= g.w;
+    int hi = (int)(q % g.h);
+    int n = (int)(q / g.h);
+    float acc = 0.f;
+    for (int kh = 0; kh < g.kh; ++kh) {
+      int hs = hi + g.pt - kh;
+      if (hs < 0 || hs % g.sh) continue;
+      int ho = hs / g.sh;
+      if (ho >= g.ho) continue;
+      for (int kw = 0; kw < g.kw; ++kw) {
+        int ws_ = wi + g.pl - kw;
+        if (ws_ < 0 || ws_ % g.sw) continue;
+        int wo = ws_ / g.sw;
+        if (wo >= g.wo) continue;
+        const float* dyp = dy + (((long long)n * g.ho + ho) * g.wo + wo) * g.co;
+        const float* wp = w + ((long long)(kh * g.kw + kw) * g.ci + ci) * g.co;
+        for (int co = 0; co < g.co; ++co) acc = fmaf(dyp[co], wp[co], acc);
+      }
+    }
+    dx[t] = acc;
+  }
+}
+
+// partial[s][kh,kw,ci,co] over positions p in [s*chunk, (s+1)*chunk) of (n, ho, wo)
+__global__ void conv_bwd_kernel_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ part,
+                                       ConvGeom g, long long P, long long chunk, int outs) {
+  int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= outs) return;
+  int co = o % g.co;
+  int r = o / g.co;
+  int ci = r % g.ci;
+  r /= g.ci;
+  int kw = r % g.kw;
+  int kh = r / g.kw;
+  long long p0 = (long long)blockIdx.y * chunk, p1 = min(p0 + chunk, P);
+  float acc = 0.f;
+  for (long long p = p0; p < p1; ++p) {
+    int wo = (int)(p % g.wo);
+    long long q = p / g.wo;
+    int ho = (int)(q % g.ho);
+    int n = (int)(q / g.ho);
+    int hi = ho * g.sh + kh - g.pt, wi = wo * g.sw + kw - g.pl;
+    if (hi < 0 || hi >= g.h || wi < 0 || wi >= g.w) continue;
+    acc = fmaf(x[(((long long)n * g.h + hi) * g.w + wi) * g.ci + ci], dy[p * g.co + co], acc);
+  }
+  part[(long long)blockIdx.y * outs + o] = acc;
+}
+
+__global__ void maxpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(t % g.co);
+    long long q = t / g.co;
+    int wo = (int)(q % g.wo);
+    q /= g.wo;
+    int ho = (int)(q % g.ho);
+    int n = (int)(q / g.ho);
+    float m = -__int_as_float(0x7f800000);
+    for (int kh = 0; kh < g.kh; ++kh) {
+      int hi = ho * g.sh + kh - g.pt;
+      if (hi < 0 || hi >= g.h) continue;
+      for (int kw = 0; kw < g.kw; ++kw) {
+        int wi = wo * g.sw + kw - g.pl;
+        if (wi < 0 || wi >= g.w) continue;
+        m = fmaxf(m, x[(((long long)n * g.h + hi) * g.w + wi) * g.co + c]);
+      }
+    }
+    y[t] = m;
+  }
+}
+
+__global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ dx,
+                                   ConvGeom g, long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(t % g.co);
+    long long q = t / g.co;
+    int wi0 = (int)(q % g.w);
+    q /= g.w;
+    int hi0 = (int)(q % g.h);
+    int n = (int)(q / g.h);
+    float acc = 0.f;
+    // windows containing (hi0, wi0), in ascending (ho, wo) order
+    int ho_lo = max(0, (hi0 + g.pt - g.kh + g.sh) / g.sh), ho_hi = min(g.ho - 1, (hi0 + g.pt) / g.sh);
+    int wo_lo = max(0, (wi0 + g.pl - g.kw + g.sw) / g.sw), wo_hi = min(g.wo - 1, (wi0 + g.pl) / g.sw);
+    if (hi0 + g.pt - g.kh + g.sh < 0) ho_lo = 0;
+    if (wi0 + g.pl - g.kw + g.sw < 0) wo_lo = 0;
+    for (int ho = ho_lo; ho <= ho_hi; ++ho)
+      for (int wo = wo_lo; wo <= wo_hi; ++wo) {
+        // first maximal element of window (ho, wo)
+        float m = -__int_as_float(0x7f800000);
+        int bh = -1, bw = -1;
+        for (int kh = 0; kh < g.kh; ++kh) {
+          int hi = ho * g.sh + kh - g.pt;
+          if (hi < 0 || hi >= g.h) continue;
+          for (int kw = 0; kw < g.kw; ++kw) {
+            int wi = wo * g.sw + kw - g.pl;
+            if (wi < 0 || wi >= g.w) continue;
+            float v = x[(((long long)n * g.h + hi) * g.w + wi) * g.co + c];
+            if (v > m || bh < 0) { m = v; bh = hi; bw = wi; }
+          }
+        }
+        if (bh == hi0 && bw == wi0) acc = __fadd_rn(acc, dy[(((long long)n * g.ho + ho) * g.wo + wo) * g.co + c]);
+      }
+    dx[t] = acc;
+  }
+}
+
+__global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(t % g.co);
+    long long q = t / g.co;
+    int wo = (int)(q % g.wo);
+    q /= g.wo;
+    int ho = (int)(q % g.ho);
+    int n = (int)(q / g.ho);
+    float s = 0.f;
+    int cnt = 0;
+    for (int kh = 0; kh < g.kh; ++kh) {
+      int hi = ho * g.sh + kh - g.pt;
+      if (hi < 0 || hi >= g.h) continue;
+      for (int kw = 0; kw < g.kw; ++kw) {
+        int wi = wo * g.sw + kw - g.pl;
+        if (wi < 0 || wi >= g.w) continue;
+        s = __fadd_rn(s, x[(((long long)n * g.h + hi) * g.w + wi) * g.co + c]);
+        ++cnt;
+      }
+    }
+    y[t] = __fdiv_rn(s, (float)cnt);
+  }
+}
+
+__global__ void concat_kernel(ConcatArgs a, float* __restrict__ dst, long long outer, long long dst_inner) {
+  const long long total = outer * dst_inner;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    long long row = t / dst_inner, col = t % dst_inner;
+    int k = 0;
+    while (k + 1 < a.n && col >= a.offset[k + 1]) ++k;
+    dst[t] = a.src[k][row * a.inner[k] + (col - a.offset[k])];
+  }
+}
+
+int grid_for(long long total, int threads = 256) {
+  long long b = (total + threads - 1) / threads;
+  return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 16));
+}
+
+}  // namespace
+
+cudaError_t launch_update_copy(const CopyDesc* descs_dev, int n_desc, long long max_n, cudaStream_t s) {
+  if (n_desc <= 0) return cudaSuccess;
+  int gx = grid_for((max_n + 3) / 4);
+  update_copy_kernel<<<dim3(gx, n_desc), 256, 0, s>>>(descs_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(const float* src, float* dst, long long n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  copy_kernel<<<grid_for((n + 3) / 4), 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_finalize(const float* ws, float* out, long long oi, long long S, int op, cudaStream_t s) {
+  reduce_finalize_kernel<<<(unsigned)((oi + 255) / 256), 256, 0, s>>>(ws, out, oi, S, op);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot_simt(const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb,
+                            cudaStream_t s) {
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  dot_simt_kernel<<<grid, 256, 0, s>>>(A, B, C, M, N, K, ta, tb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv2d_fwd(const float* x, const float* w, float* y, const ConvGeom& g, cudaStream_t s) {
+  long long total = (long long)g.n * g.ho * g.wo * g.co;
+  conv_fwd_kernel<<<grid_for(total), 256, 0, s>>>(x, w, y, g, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_conv2d_bwd_input(const float* dy, const float* w, float* dx, const ConvGeom& g, cudaStream_t s) {
+  long long total = (long long)g.n * g.h * g.w * g.ci;
+  conv_bwd_input_kernel<<<grid_for(total), 256, 0, s>>>(dy, w, dx, g, total);
+  return cudaGetLastError();
+}
+
+static void bwdk_split(const ConvGeom& g, int num_sms, long long* P, long long* chunk, long long* S, int* outs) {
+  *outs = g.kh * g.kw * g.ci * g.co;
+  *P = (long long)g.n * g.ho * g.wo;
+  long long want_threads = (long long)num_sms * 2048;
+  long long sp = std::max<long long>(1, want_threads / std::max(1, *outs));
+  sp = std::min<long long>(sp, std::max<long long>(1, *P / 64));
+  sp = std::min<long long>(sp, 65535);
+  *chunk = (*P + sp - 1) / sp;
+  *S = (*P + *chunk - 1) / *chunk;
+}
+
+size_t conv2d_bwd_kernel_ws(const ConvGeom& g, int num_sms) {
+  long long P, chunk, S;
+  int outs;
+  bwdk_split(g, num_sms, &P, &chunk, &S, &outs);
+  return (size_t)(S * outs);
+}
+
+cudaError_t launch_conv2d_bwd_kernel(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g,
+                                     int num_sms, cudaStream_t s) {
+  long long P, chunk, S;
+  int outs;
+  bwdk_split(g, num_sms, &P, &chunk, &S, &outs);
+  dim3 grid((outs + 127) / 128, (unsigned)S);
+  conv_bwd_kernel_kernel<<<grid, 128, 0, s>>>(x, dy, ws, g, P, chunk, outs);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_reduce_finalize(ws, dw, outs, S, 0, s);
+}
+
+cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
+  long long total = (long long)g.n * g.ho * g.wo * g.co;
+  maxpool_kernel<<<grid_for(total), 256, 0, s>>>(x, y, g, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s) {
+  long long total = (long long)g.n * g.h * g.w * g.co;
+  maxpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(x, dy, dx, g, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
+  long long total = (long long)g.n * g.ho * g.wo * g.co;
+  avgpool_kernel<<<grid_for(total), 256, 0, s>>>(x, y, g, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long long dst_inner, cudaStream_t s) {
+  concat_kernel<<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, outer, dst_inner);
+  return cudaGetLastError();
+}
+
+}  // namespace cg

@@ -1,0 +1,43 @@
+"""Helpers for the GPU parity tests: build a workloads spec on the CUDA path
+(through the C ABI) and on the oracle, with the same seeded inputs."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle.eager import evaluate, leaf_values, run_iterations
+from oracle.graph import from_spec
+from paper_1812_03770_b200 import cg
+from workloads.gen import materialise
+
+
+def leaf_data(rec, seed=1812):
+    if rec["op"] in ("VAR", "CONST"):
+        return materialise(rec["data"], rec["shape"], seed)
+    return None
+
+
+def gpu_graph(spec, flags=0, optimise=True, device=0):
+    g, outs = cg.build_from_spec(spec, device=device, data_fn=leaf_data)
+    rep = g.optimise(outs) if optimise else None
+    info = g.plan_memory(outs, flags)
+    return g, outs, rep, info
+
+
+def normwise(got, ref):
+    """E(g, o) = max|g - o| / max|o|; max|g| if o == 0."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert got.shape == ref.shape, (got.shape, ref.shape)
+    fin = np.isfinite(ref)
+    assert np.array_equal(np.isfinite(got), fin), "non-finite pattern differs"
+    if not fin.any():
+        return 0.0
+    d = np.max(np.abs(got[fin] - ref[fin]))
+    m = np.max(np.abs(ref[fin]))
+    return float(d / m) if m > 0 else float(np.max(np.abs(got[fin])))
+
+
+def oracle_outputs(spec, overrides=None):
+    og, oo = from_spec(spec)
+    vals = evaluate(og, leaf_values(og, overrides))
+    return {o: vals[o] for o in oo}, og, oo

@@ -1,0 +1,157 @@
+"""Host-compiler parity (CPU): the C++ library in host-only mode vs the oracle.
+
+The structural products — rewritten graph (CSE/CF/DCE), gamma, fusion groups,
+Algorithm 1 memory plan — must match the oracle BYTE-FOR-BYTE (north star:
+"Memory plans, CSE and fusion groupings must match bit-exactly").  Both sides
+implement DESIGN.md's readings independently and share no code.
+Also: the library exports every symbol include/*.h declares, reports the
+documented error codes, and every generated kernel compiles for sm_100a with
+NVRTC (no GPU needed).
+"""
+import ctypes
+import glob
+import os
+import re
+
+import pytest
+
+from oracle.dump import compile_graph, graph_json, plan_json
+from oracle.graph import from_spec
+from paper_1812_03770_b200 import cg
+from tests.randgraph import random_spec
+from workloads import configs
+from workloads.gen import materialise
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MODES = [0, cg.PLAN_INCREMENTAL, cg.PLAN_NO_FUSION, cg.PLAN_INCREMENTAL | cg.PLAN_NO_FUSION]
+
+
+def _const_data(rec):
+    return materialise(rec["data"], rec["shape"]) if rec["op"] == "CONST" else None
+
+
+def host_graph(spec, flags, optimise=True):
+    g, outs = cg.build_from_spec(spec, device=-1, data_fn=_const_data)
+    rep = g.optimise(outs) if optimise else None
+    info = g.plan_memory(outs, flags)
+    return g, outs, rep, info
+
+
+def check_parity(spec, flags):
+    g, outs, rep, info = host_graph(spec, flags)
+    og, oo = from_spec(spec)
+    c = compile_graph(og, oo, flags, compute_values=False)
+    assert rep == c.opt.report
+    assert g.dump_json(cg.DUMP_GRAPH) == graph_json(c.opt)
+    assert g.dump_json(cg.DUMP_PLAN) == plan_json(c)
+    assert info["n_groups"] == len(c.groups) and info["n_blocks"] == len(c.plan.size)
+    assert info["pool_bytes"] == c.plan.pool_bytes and info["unshared_bytes"] == c.unshared_bytes
+    return g
+
+
+def test_abi_symbols_exported():
+    L = ctypes.CDLL(cg.LIB_PATH)
+    declared = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        txt = open(h).read()
+        # function declarations: a line starting with a return type, then the name and "("
+        declared |= set(re.findall(r"^[A-Za-z_][\w \*]*?\b(cgx?_[a-z0-9_]+)\s*\(", txt, re.M))
+    assert {"cg_create", "cg_add_node", "cg_add_update", "cg_optimise", "cg_plan_memory", "cg_assign",
+            "cg_eval", "cg_destroy"} <= declared
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+@pytest.mark.parametrize("flags", MODES)
+def test_config_parity(name, flags):
+    spec = {"C1": lambda: configs.c1(), "C2": lambda: configs.c2(),
+            "C3": lambda: configs.c3(), "C4": lambda: configs.c4()}[name]()
+    check_parity(spec, flags)
+
+
+def test_c5_parity_and_memory():
+    """InceptionV3-shaped graph at batch 256: plan exact, peak << unshared (P:379 motivation)."""
+    spec = configs.c5()
+    g = check_parity(spec, 0)
+    info = g.plan_memory.__self__ if False else None  # noqa: F841
+    og, oo = from_spec(spec)
+    c = compile_graph(og, oo, 0, compute_values=False)
+    assert c.opt.report["cf_folded"] == 94 and c.opt.report["dce_removed"] >= 94
+    assert c.plan.pool_bytes < c.unshared_bytes / 10
+
+
+@pytest.mark.parametrize("flags", MODES)
+def test_random_dag_parity(flags):
+    for seed in range(250):
+        check_parity(random_spec(seed), flags)
+
+
+def test_no_optimise_parity():
+    for seed in range(100):
+        spec = random_spec(1000 + seed)
+        g, outs, _, _ = host_graph(spec, 0, optimise=False)
+        og, oo = from_spec(spec)
+        c = compile_graph(og, oo, 0, do_optimise=False)
+        assert g.dump_json(cg.DUMP_PLAN) == plan_json(c)
+
+
+def test_abi_errors():
+    g = cg.Graph(-1)
+    x = g.var([2, 3])
+    y = g.var([3, 2])
+    with pytest.raises(cg.CGError) as e:
+        g.add_node("ADD", [x])
+    assert e.value.code == "CG_E_ARITY"
+    with pytest.raises(cg.CGError) as e:
+        g.add_node("NEG", [9])
+    assert e.value.code == "CG_E_BAD_NODE"
+    with pytest.raises(cg.CGError) as e:
+        g.add_node("ADD", [x, y])
+    assert e.value.code == "CG_E_SHAPE"
+    m = g.add_node("NEG", [x])
+    with pytest.raises(cg.CGError) as e:
+        g.add_update(x, m)
+    assert e.value.code == "CG_E_NOT_VAR"
+    with pytest.raises(cg.CGError) as e:
+        g.add_update(m, y)
+    assert e.value.code == "CG_E_UPDATE_SHAPE"
+    g.add_update(m, x)
+    with pytest.raises(cg.CGError) as e:
+        g.add_update(m, x)
+    assert e.value.code == "CG_E_DUP_UPDATE"
+    g.plan_memory([m])
+    with pytest.raises(cg.CGError) as e:
+        g.add_node("NEG", [m])
+    assert e.value.code == "CG_E_STATE"
+    with pytest.raises(cg.CGError) as e:
+        g.eval([m])
+    assert e.value.code == "CG_E_NO_DEVICE"
+
+
+def _codegen_check(g, sms=148):
+    L = cg.lib()
+    f = L.cgx_codegen_check
+    f.restype = ctypes.c_int64
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    buf = ctypes.create_string_buffer(1 << 20)
+    r = f(g.h, sms, buf, len(buf))
+    assert r >= 0, buf.value.decode()[:6000]
+    return r
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_generated_kernels_compile(name):
+    spec = {"C1": lambda: configs.c1(), "C2": lambda: configs.c2(),
+            "C3": lambda: configs.c3(), "C4": lambda: configs.c4()}[name]()
+    for flags in (0, cg.PLAN_NO_FUSION):
+        g, _, _, _ = host_graph(spec, flags)
+        assert _codegen_check(g) >= 1
+
+
+def test_generated_kernels_compile_random():
+    n = 0
+    for seed in range(0, 60):
+        g, _, _, _ = host_graph(random_spec(seed), 0)
+        n += _codegen_check(g)
+    assert n > 60
