@@ -318,6 +318,7 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
     }
     b << "  }\n}\n";
     int64_t work = (R + TY * U - 1) / (TY * U);
+    ks.work_blocks = work;
     ks.grid[0] = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)num_sms * 8));
     ks.source = finish("ew", b.str(), &ks.name);
     return ks;
@@ -380,6 +381,7 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
   }
   b << "  }\n}\n";
   int64_t work = (NV + 256 * U - 1) / (256 * U);
+  ks.work_blocks = work;
   ks.grid[0] = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)num_sms * 8));
   ks.source = finish("ew", b.str(), &ks.name);
   return ks;

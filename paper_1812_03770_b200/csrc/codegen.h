@@ -15,6 +15,7 @@ struct KernelSpec {
   std::string source;   // complete translation unit
   uint32_t grid[3] = {1, 1, 1};
   uint32_t block = 256;
+  int64_t work_blocks = 1;   // grid-stride kernels: blocks that still have work (upper bound for grid.x)
   std::vector<int> in_ids;   // kernel args: input pointers (group inputs order)
   std::vector<int> out_ids;  // then output pointers (materialised values, gamma order)
   bool uses_ws = false;      // last arg: float* workspace (reduction partials)

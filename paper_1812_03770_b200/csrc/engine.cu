@@ -257,6 +257,12 @@ static int build_launches(cg_graph* g) {
       if (ks.uses_ws) argv.push_back(g->ws);
       dim3 grid(ks.grid[0], ks.grid[1], ks.grid[2]);
       unsigned block = ks.block;
+      if (ks.mode != "red") {  // grid-stride kernels: exactly one full wave of resident blocks
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k, (int)block, 0) == cudaSuccess && occ > 0)
+          grid.x = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ks.work_blocks, (int64_t)g->num_sms * occ));
+        cudaGetLastError();
+      }
       auto st = std::make_shared<std::vector<void*>>(argv);
       L.push_back({[k, grid, block, st](cudaStream_t s) {
                      std::vector<void*> ap(st->size());
@@ -754,7 +760,9 @@ int cg_read(cg_graph* g, cg_node node, void* host_dst, size_t nbytes) {
   if (node < 0 || node >= (int)hg.nodes.size()) return g->fail(CG_E_BAD_NODE, "unknown node");
   int v = hg.resolve(node);
   if (nbytes != 4 * (size_t)numel(hg.nodes[v].shape)) return g->fail(CG_E_SIZE, "byte count != numel*4");
-  if (!g->ptr[v] || (!hg.is_external(v) && !valid(g, v)))
+  // a root's block keeps the value of its last evaluation until another group
+  // overwrites it (an update edge makes it stale w.r.t. the Vars, not unreadable)
+  if (!g->ptr[v] || (!hg.is_external(v) && (g->count[v] == 0 || g->owner[hg.pl.block_of[v]] != v)))
     return g->fail(CG_E_NOT_PLANNED, "node " + std::to_string(node) + " holds no current value");
   g->join_in();
   CUDA_TRY(g, cudaMemcpyAsync(host_dst, g->ptr[v], nbytes, cudaMemcpyDeviceToHost, g->stream), "cudaMemcpyAsync(read)");
