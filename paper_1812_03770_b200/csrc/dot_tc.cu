@@ -1,0 +1,331 @@
+// DOT nodes on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+//   C[M,N] = op(A)[M,K] . op(B)[K,N]      fp32 in, fp32 out  (SURVEY §8(c) c1-defs DOT)
+//
+// tcgen05 has no fp32-input MMA, so every fp32 operand x is split into
+// hi = x & 0xFFFFE000 (exactly representable in TF32) and lo = x - hi (exact in
+// fp32), and the product is accumulated as  hi.hi + hi.lo + lo.hi  ("3xTF32",
+// SURVEY §8(c) c12) in fp32 TMEM accumulators.  The dropped lo.lo term is
+// < 2^-20 relative, so the result has fp32-GEMM accuracy.
+// Integer-valued operands with |x| < 2^11 have lo == 0 and are multiplied exactly.
+//
+// One CTA computes a BM x BN = 128 x 128 output tile:
+//   warp 0      TMA producer: loads the raw fp32 A/B k-slab (BK = 32, one 128-byte
+//               swizzle row) of stage s with cp.async.bulk.tensor (OOB -> 0, so
+//               ragged M/N/K need no masking on the load side)
+//   warp 1      TMEM allocator + MMA issuer (one elected thread): 3 x 4
+//               tcgen05.mma.kind::tf32 per stage, tcgen05.commit -> empty[s]
+//   warps 2-5   split hi/lo in shared memory (elementwise, layout-preserving, so
+//               the swizzle of the TMA tile is the swizzle of the hi and lo
+//               tiles), then the epilogue: tcgen05.ld TMEM -> registers -> C.
+// Operand majorness comes from the transposes: A is K-major when ta = 0 and
+// M-major when ta = 1; B is N-major when tb = 0 and K-major when tb = 1.  Both
+// are native UMMA smem layouts for TF32 (instruction-descriptor bits 15/16),
+// so transposed operands never take a transpose pass.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "dot_tc.h"
+
+namespace cg {
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 32;
+constexpr int STAGES = 3;
+constexpr int TILE_BYTES = BM * BK * 4;             // 16 KiB: one operand tile (BN == BM)
+constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // A hi, B hi, A lo, B lo
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+constexpr int THREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  long long spins = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (++spins > (1LL << 28)) __trap();  // watchdog: a lost arrival must fail the launch, not hang the GPU
+  }
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor (SWIZZLE_128B, version 1 = sm_100)
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+// Descriptor of one K=8 slice `kk` (0..3) of a 128 x 32 operand tile.
+//  K-major tile : 128 rows (M or N) x 128 B (32 k), row r at r*128 B (TMA SW128)
+//                 -> SBO = 1024 B (8-row groups), LBO unused (16 B); slice kk at +32 B
+//  MN-major tile: 4 boxes of [32 k-rows][32 mn] (4 KiB each), box j at j*4 KiB
+//                 -> LBO = 4096 B (next 32 mn), SBO = 1024 B (next 8 k-rows); slice kk at +1024 B
+__device__ __forceinline__ uint64_t tile_desc(uint32_t tile, int mn_major, int kk) {
+  return mn_major ? sdesc(tile + kk * 1024, 4096, 1024) : sdesc(tile + kk * 32, 16, 1024);
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    dot_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
+                  int M, int N, int K, int a_mn, int b_mn) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  // full[s] (TMA landed), conv[s] (hi/lo split done), empty[s] (MMAs of stage s done), tfull
+  const uint32_t bar0 = smem_u32(bars);
+  auto full = [&](int s) { return bar0 + 8u * s; };
+  auto conv = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto empty = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
+  const uint32_t tfull = bar0 + 8u * (3 * STAGES);
+  uint32_t* tmem_slot = (uint32_t*)(smem + STAGES * STAGE_BYTES + 512);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nk = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full(s), 1);
+      mbar_init(conv(s), 4);
+      mbar_init(empty(s), 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(empty(s), ph ^ 1);
+        const uint32_t st = sbase + s * STAGE_BYTES;
+        mbar_expect_tx(full(s), 2 * TILE_BYTES);
+        const int k0 = kb * BK;
+        if (a_mn) {
+          for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &mapA, m0 + 32 * j, k0, full(s));
+        } else {
+          tma_load_2d(st, &mapA, k0, m0, full(s));
+        }
+        if (b_mn) {
+          for (int j = 0; j < BN / 32; ++j) tma_load_2d(st + TILE_BYTES + j * 4096, &mapB, n0 + 32 * j, k0, full(s));
+        } else {
+          tma_load_2d(st + TILE_BYTES, &mapB, k0, n0, full(s));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      // instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (kb / STAGES) & 1;
+        mbar_wait(conv(s), ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t st = sbase + s * STAGE_BYTES;
+        const uint32_t ahi = st, bhi = st + TILE_BYTES, alo = st + 2 * TILE_BYTES, blo = st + 3 * TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+          // small terms first, then the leading hi.hi product
+          mma_tf32(tmem, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
+          mma_tf32(tmem, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
+          mma_tf32(tmem, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, 1u);
+        }
+        mma_commit(empty(s));  // frees the stage once these MMAs have read it
+      }
+      mma_commit(tfull);
+    }
+  } else {
+    // ---------------- warps 2..5: hi/lo split of each stage, then the epilogue
+    const int t = threadIdx.x - 64;  // 0..127
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(full(s), ph);
+      float4* hi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES);
+      float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * TILE_BYTES);
+#pragma unroll 4
+      for (int i = t; i < 2 * TILE_BYTES / 16; i += 128) {
+        float4 v = hi[i];
+        float4 h, l;
+        h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+        h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+        h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+        h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+        l.x = __fsub_rn(v.x, h.x);
+        l.y = __fsub_rn(v.y, h.y);
+        l.z = __fsub_rn(v.z, h.z);
+        l.w = __fsub_rn(v.w, h.w);
+        hi[i] = h;
+        lo[i] = l;
+      }
+      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(conv(s));
+    }
+    // epilogue: this warp may touch TMEM lanes [32*(warp%4), +32)
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int sub = warp % 4;
+    const int row = m0 + sub * 32 + lane;
+    const bool vec = (N % 4) == 0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+            "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < M) {
+        float* crow = C + (size_t)row * N;
+        const int n = n0 + c0;
+        if (vec && n + 16 <= N) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<float4*>(crow + n + 4 * q) =
+                make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                            __uint_as_float(r[4 * q + 3]));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (n + q < N) crow[n + q] = __uint_as_float(r[q]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                  const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  });
+  return fn;
+}
+
+// 2-D fp32 row-major matrix [rows, cols] (cols contiguous), box {32 cols, box_rows}
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool dot_tc_supported(int M, int N, int K, int ta, int tb) {
+  // TMA: global row pitch must be a multiple of 16 B, i.e. the contiguous extent % 4 == 0
+  const int64_t a_cols = ta ? M : K, b_cols = tb ? K : N;
+  if (a_cols % 4 || b_cols % 4) return false;
+  if (M < 1 || N < 1 || K < 1) return false;
+  // skinny products are HBM-bound; they stay on the SIMT path
+  return M >= 64 && N >= 32 && K >= 8;
+}
+
+int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb) {
+  if (!dot_tc_supported(M, N, K, ta, tb)) return -1;
+  std::memset(p, 0, sizeof(*p));
+  p->M = M; p->N = N; p->K = K;
+  p->a_mn = ta; p->b_mn = tb ? 0 : 1;
+  p->C = C;
+  // A: ta = 0 -> [M, K] (K-major, box 32 k x 128 m); ta = 1 -> [K, M] (M-major, box 32 m x 32 k)
+  bool ok = ta ? make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, K, M, 32)
+               : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM);
+  // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x 128 n)
+  ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, BN)
+                 : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32));
+  return ok ? 0 : -2;
+}
+
+cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(dot_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM);
+  const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
+  const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
+  dot_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b, p.C, p.M, p.N, p.K, p.a_mn, p.b_mn);
+  return cudaGetLastError();
+}
+
+}  // namespace cg

@@ -27,6 +27,7 @@
 #include "../../include/cg.h"
 #include "codegen.h"
 #include "host.h"
+#include "dot_tc.h"
 #include "kernels.h"
 
 using namespace cg;
@@ -305,6 +306,13 @@ static int build_launches(cg_graph* g) {
         int M = (int)ys[0], N = (int)ys[1], K = (int)(nd.attr.ta ? as[0] : as[1]);
         int ta = nd.attr.ta, tb = nd.attr.tb;
         const float *A = in[0], *B = in[1];
+        if (dot_tc_supported(M, N, K, ta, tb)) {  // tensor cores (tcgen05, 3xTF32)
+          auto plan = std::make_shared<DotTcPlan>();
+          if (dot_tc_prepare(plan.get(), A, B, out, M, N, K, ta, tb) != 0)
+            return g->fail(CG_E_CUDA, "DOT node " + std::to_string(G.sink) + ": cuTensorMapEncodeTiled failed");
+          L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, 1});
+          break;
+        }
         L.push_back({[A, B, out, M, N, K, ta, tb](cudaStream_t s) { return launch_dot_simt(A, B, out, M, N, K, ta, tb, s); }, 1});
         break;
       }

@@ -184,6 +184,43 @@ def test_dot_integer_exact(m, n, k, ta, tb):
     assert np.array_equal(got, ref)
 
 
+# shapes the tcgen05 path takes (16-byte row pitches), with ragged M / N / K tails
+TC_SHAPES = [(128, 128, 32), (300, 136, 100), (129, 260, 36), (784, 1024, 512), (4096, 1024, 784)]
+
+
+@pytest.mark.parametrize("m,n,k", TC_SHAPES)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_dot_tc_integer_exact(m, n, k, ta, tb):
+    """|x| <= 4 integers: hi == x, lo == 0 and every partial sum is exact in fp32,
+    so the 3xTF32 tensor-core product must equal the f64 oracle bit for bit."""
+    sa = (k, m) if ta else (m, k)
+    sb = (n, k) if tb else (k, n)
+    got, ref = _run_single("DOT", [sa, sb], {"ta": ta, "tb": tb})
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("m,n,k", [(512, 384, 1000), (4096, 1024, 1024), (1024, 1024, 4096)])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1)])
+def test_dot_tc_float_3xtf32(m, n, k, ta, tb):
+    """U[-1, 1) operands: 3xTF32 has fp32-GEMM accuracy.  A 1xTF32
+    product would show ~1e-4 normwise error here; the bound is 1e-5."""
+    rng = np.random.default_rng(7)
+    sa = (k, m) if ta else (m, k)
+    sb = (n, k) if tb else (k, n)
+    a = rng.uniform(-1, 1, sa).astype(np.float32)
+    b = rng.uniform(-1, 1, sb).astype(np.float32)
+    g = cg.Graph(0)
+    va, vb = g.var(sa), g.var(sb)
+    o = g.add_node("DOT", [va, vb], ta=ta, tb=tb)
+    g.plan_memory([o])
+    g.assign(va, a)
+    g.assign(vb, b)
+    g.eval([o])
+    A = a.astype(np.float64).T if ta else a.astype(np.float64)
+    B = b.astype(np.float64).T if tb else b.astype(np.float64)
+    assert normwise(g.read(o), A @ B) <= 1e-5
+
+
 @pytest.mark.parametrize("sh,pad", [(1, 0), (1, 1), (2, 0), (2, 1)])
 def test_conv_family_integer_exact(sh, pad):
     a = {"sh": sh, "sw": sh, "pad": pad}
