@@ -74,14 +74,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-// UMMA shared-memory descriptor (SWIZZLE_128B, version 1 = sm_100)
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor (version 1 = sm_100).  layout: 2 = SWIZZLE_128B
+// (16-byte chunks), 1 = SWIZZLE_128B_BASE32B (32-byte chunks; the only swizzled
+// MN-major layout TF32 operands have).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // version
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -96,17 +98,18 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 }
 
 // Descriptor of one K=8 slice `kk` (0..3) of a 128 x 32 operand tile.
-//  K-major tile : 128 rows (M or N) x 128 B (32 k), row r at r*128 B (TMA SW128)
+//  K-major tile : 128 rows (M or N) x 128 B (32 k), row r at r*128 B, TMA SWIZZLE_128B
 //                 -> SBO = 1024 B (8-row groups), LBO unused (16 B); slice kk at +32 B
-//  MN-major tile: 4 boxes of [32 k-rows][32 mn] (4 KiB each), box j at j*4 KiB
-//                 -> LBO = 4096 B (next 32 mn), SBO = 1024 B (next 8 k-rows); slice kk at +1024 B
+//  MN-major tile: 4 boxes of [32 k-rows][32 mn] (4 KiB each), box j at j*4 KiB, k-row
+//                 r at r*128 B, TMA SWIZZLE_128B_ATOM_32B (32-byte chunks, 4-row period)
+//                 -> LBO = 4096 B (next 32 mn), SBO = 512 B (next 4 k-rows); slice kk at +1024 B
 __device__ __forceinline__ uint64_t tile_desc(uint32_t tile, int mn_major, int kk) {
-  return mn_major ? sdesc(tile + kk * 1024, 4096, 1024) : sdesc(tile + kk * 32, 16, 1024);
+  return mn_major ? sdesc(tile + kk * 1024, 4096, 512, 1) : sdesc(tile + kk * 32, 16, 1024, 2);
 }
 
 __global__ void __launch_bounds__(THREADS, 1)
     dot_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
-                  int M, int N, int K, int a_mn, int b_mn) {
+                  int M, int N, int K, int a_mn, int b_mn, float* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -195,6 +198,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = kb % STAGES;
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(full(s), ph);
+      if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && kb == 0 && t < 8) {
+        dbg[t] = reinterpret_cast<float*>(smem)[t];                    // A raw
+        dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_BYTES)[t];   // B raw
+      }
       float4* hi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES);
       float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * TILE_BYTES);
 #pragma unroll 4
@@ -220,6 +227,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     // epilogue: this warp may touch TMEM lanes [32*(warp%4), +32)
     mbar_wait(tfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+      dbg[16] = __uint_as_float(tmem);
+      dbg[17] = (float)nk;
+      const uint32_t* lo32 = reinterpret_cast<const uint32_t*>(smem + 2 * TILE_BYTES);
+      dbg[18] = __uint_as_float(lo32[0]);
+      dbg[19] = reinterpret_cast<float*>(smem)[0];
+    }
     const int sub = warp % 4;
     const int row = m0 + sub * 32 + lane;
     const bool vec = (N % 4) == 0;
@@ -276,8 +290,9 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2-D fp32 row-major matrix [rows, cols] (cols contiguous), box {32 cols, box_rows}
-bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int box_rows) {
+// 2-D fp32 row-major matrix [rows, cols] (cols contiguous), box {32 cols, box_rows}.
+// K-major operand tiles use SWIZZLE_128B; MN-major ones the 32-byte-atom variant.
+bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int box_rows, bool mn_major) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -285,7 +300,8 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
   cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -306,11 +322,11 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   p->a_mn = ta; p->b_mn = tb ? 0 : 1;
   p->C = C;
   // A: ta = 0 -> [M, K] (K-major, box 32 k x 128 m); ta = 1 -> [K, M] (M-major, box 32 m x 32 k)
-  bool ok = ta ? make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, K, M, 32)
-               : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM);
+  bool ok = ta ? make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, K, M, 32, true)
+               : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM, false);
   // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x 128 n)
-  ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, BN)
-                 : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32));
+  ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, BN, false)
+                 : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32, true));
   return ok ? 0 : -2;
 }
 
@@ -324,8 +340,19 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM);
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
-  dot_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b, p.C, p.M, p.N, p.K, p.a_mn, p.b_mn);
+  dot_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b, p.C, p.M, p.N, p.K, p.a_mn, p.b_mn, p.dbg);
   return cudaGetLastError();
 }
 
 }  // namespace cg
+
+// ---- debug entry (tests/tools only): one DOT on device buffers, optional dump
+extern "C" int cgx_dot_tc(const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb, float* dbg) {
+  cg::DotTcPlan p;
+  int rc = cg::dot_tc_prepare(&p, A, B, C, M, N, K, ta, tb);
+  if (rc) return rc;
+  p.dbg = dbg;
+  cudaError_t e = cg::launch_dot_tc(p, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? 0 : -100 - (int)e;
+}
