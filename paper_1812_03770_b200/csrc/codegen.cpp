@@ -52,8 +52,8 @@ std::string expr(int op, const std::vector<std::string>& a) {
     case CG_MUL: return "__fmul_rn(" + a[0] + "," + a[1] + ")";
     case CG_DIV: return "__fdiv_rn(" + a[0] + "," + a[1] + ")";
     case CG_POW: return "powf(" + a[0] + "," + a[1] + ")";
-    case CG_MAX2: return "fmaxf(" + a[0] + "," + a[1] + ")";
-    case CG_MIN2: return "fminf(" + a[0] + "," + a[1] + ")";
+    case CG_MAX2: return "cg_max(" + a[0] + "," + a[1] + ")";
+    case CG_MIN2: return "cg_min(" + a[0] + "," + a[1] + ")";
     case CG_RELU_GRAD: return "(" + a[0] + " > 0.f ? " + a[1] + " : 0.f)";
     case CG_FMA: return "__fmaf_rn(" + a[0] + "," + a[1] + "," + a[2] + ")";
     case CG_NEG: return "(-" + a[0] + ")";
@@ -80,6 +80,13 @@ __device__ __forceinline__ float4 cg_ld4(const float* p) {
 __device__ __forceinline__ void cg_st4(float* p, float a, float b, float c, float d) {
   asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+// NaN-propagating max/min (numpy maximum/minimum, the oracle's definition)
+__device__ __forceinline__ float cg_max(float a, float b) {
+  float r; asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b)); return r;
+}
+__device__ __forceinline__ float cg_min(float a, float b) {
+  float r; asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b)); return r;
 }
 __device__ __forceinline__ float cg_lane(const float4& v, int l) {
   return l == 0 ? v.x : (l == 1 ? v.y : (l == 2 ? v.z : v.w));
@@ -462,7 +469,7 @@ KernelSpec gen_red(const HostGraph& hg, const Group& G, int num_sms) {
   const bool is_sum = sink.op == CG_SUM;
   const std::string ident = is_sum ? "0.f" : "(-__int_as_float(0x7f800000))";
   auto comb = [&](const std::string& a, const std::string& bb) {
-    return is_sum ? "__fadd_rn(" + a + ", " + bb + ")" : "fmaxf(" + a + ", " + bb + ")";
+    return is_sum ? "__fadd_rn(" + a + ", " + bb + ")" : "cg_max(" + a + ", " + bb + ")";
   };
   std::vector<Seg> sO, sR, sI;
   for (int p : G.inputs) {

@@ -49,7 +49,8 @@ __global__ void reduce_finalize_kernel(const float* __restrict__ ws, float* __re
   float acc = ws[j];
   for (long long s = 1; s < S; ++s) {
     float v = ws[s * oi + j];
-    acc = op == 0 ? __fadd_rn(acc, v) : fmaxf(acc, v);
+    if (op == 0) acc = __fadd_rn(acc, v);
+    else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v));  // NaN-propagating, as numpy max
   }
   out[j] = acc;
 }
@@ -197,7 +198,7 @@ __global__ void maxpool_kernel(const float* __restrict__ x, float* __restrict__ 
       for (int kw = 0; kw < g.kw; ++kw) {
         int wi = wo * g.sw + kw - g.pl;
         if (wi < 0 || wi >= g.w) continue;
-        m = fmaxf(m, x[(((long long)n * g.h + hi) * g.w + wi) * g.co + c]);
+        asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(x[(((long long)n * g.h + hi) * g.w + wi) * g.co + c]));
       }
     }
     y[t] = m;
