@@ -41,3 +41,25 @@ def oracle_outputs(spec, overrides=None):
     og, oo = from_spec(spec)
     vals = evaluate(og, leaf_values(og, overrides))
     return {o: vals[o] for o in oo}, og, oo
+
+
+def evaluate_pinned(og, leaf_vals, pinned, needed=None):
+    """The oracle's eager evaluation (oracle.ops.eval_op node by node, creation
+    order) with the values of the nodes in ``pinned`` (id -> array) taken as given
+    instead of computed.  Used to compare everything downstream of a ReLU / max-pool
+    decision under the SAME decision the GPU took (the pinned values themselves are
+    checked against the unpinned oracle separately)."""
+    from oracle.ops import eval_op
+    vals = dict(leaf_vals)
+    for n in og.nodes:
+        if n.op in ("VAR", "CONST"):
+            if n.id not in vals:
+                vals[n.id] = og.const_value(n.id) if n.op == "CONST" else np.zeros(n.shape, np.float32)
+            continue
+        if n.id in pinned:
+            vals[n.id] = pinned[n.id]
+            continue
+        if needed is not None and n.id not in needed:
+            continue
+        vals[n.id] = eval_op(n.op, [vals[p] for p in n.preds], n.attrs, n.shape)
+    return vals
