@@ -30,6 +30,9 @@
 #include <mutex>
 
 #include "dot_tc.h"
+#include "kernels.h"
+
+#include <algorithm>
 
 namespace cg {
 
@@ -109,7 +112,7 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t tile, int mn_major, int k
 
 __global__ void __launch_bounds__(THREADS, 1)
     dot_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
-                  int M, int N, int K, int a_mn, int b_mn, float* __restrict__ dbg) {
+                  int M, int N, int K, int a_mn, int b_mn, int kb_per_split, float* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -124,7 +127,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int nk = (K + BK - 1) / BK;
+  // split-K: CTA z covers k-blocks [kb0, kb0 + nk) and writes partial plane z
+  const int kb0 = blockIdx.z * kb_per_split;
+  const int nk = min((K + BK - 1) / BK - kb0, kb_per_split);
+  C += (size_t)blockIdx.z * M * N;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(empty(s), ph ^ 1);
         const uint32_t st = sbase + s * STAGE_BYTES;
         mbar_expect_tx(full(s), 2 * TILE_BYTES);
-        const int k0 = kb * BK;
+        const int k0 = (kb0 + kb) * BK;
         if (a_mn) {
           for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &mapA, m0 + 32 * j, k0, full(s));
         } else {
@@ -315,10 +321,30 @@ bool dot_tc_supported(int M, int N, int K, int ta, int tb) {
   return M >= 64 && N >= 32 && K >= 8;
 }
 
-int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb) {
+void dot_tc_split(int M, int N, int K, int num_sms, int* splits, int* kb_per_split) {
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int nk = (K + BK - 1) / BK;
+  int S = 1;
+  if (tiles < num_sms) S = std::max(1, std::min((num_sms + tiles - 1) / tiles, nk / 4));
+  const int per = (nk + S - 1) / S;
+  *kb_per_split = per;
+  *splits = (nk + per - 1) / per;
+}
+
+size_t dot_tc_ws_floats(int M, int N, int K, int num_sms) {
+  int S, per;
+  dot_tc_split(M, N, K, num_sms, &S, &per);
+  return S > 1 ? (size_t)S * M * N : 0;
+}
+
+int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb,
+                   float* ws, int num_sms) {
   if (!dot_tc_supported(M, N, K, ta, tb)) return -1;
   std::memset(p, 0, sizeof(*p));
   p->M = M; p->N = N; p->K = K;
+  dot_tc_split(M, N, K, num_sms, &p->splits, &p->kb_per_split);
+  p->ws = ws;
+  if (p->splits > 1 && !ws) return -3;
   p->a_mn = ta; p->b_mn = tb ? 0 : 1;
   p->C = C;
   // A: ta = 0 -> [M, K] (K-major, box 32 k x 128 m); ta = 1 -> [K, M] (M-major, box 32 m x 32 k)
@@ -337,11 +363,14 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
     attr_err = cudaFuncSetAttribute(dot_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM);
+  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
-  dot_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b, p.C, p.M, p.N, p.K, p.a_mn, p.b_mn, p.dbg);
-  return cudaGetLastError();
+  float* out = p.splits > 1 ? p.ws : p.C;
+  dot_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, p.a_mn, p.b_mn, p.kb_per_split, p.dbg);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || p.splits == 1) return e;
+  return launch_reduce_finalize(p.ws, p.C, (long long)p.M * p.N, p.splits, 0, s);
 }
 
 }  // namespace cg
@@ -349,7 +378,7 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
 // ---- debug entry (tests/tools only): one DOT on device buffers, optional dump
 extern "C" int cgx_dot_tc(const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb, float* dbg) {
   cg::DotTcPlan p;
-  int rc = cg::dot_tc_prepare(&p, A, B, C, M, N, K, ta, tb);
+  int rc = cg::dot_tc_prepare(&p, A, B, C, M, N, K, ta, tb, nullptr, 1);
   if (rc) return rc;
   p.dbg = dbg;
   cudaError_t e = cg::launch_dot_tc(p, nullptr);

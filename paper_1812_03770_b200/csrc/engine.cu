@@ -27,6 +27,7 @@
 #include "../../include/cg.h"
 #include "codegen.h"
 #include "host.h"
+#include "dot_small.h"
 #include "dot_tc.h"
 #include "kernels.h"
 
@@ -226,6 +227,14 @@ static int build_launches(cg_graph* g) {
     if (G.kind == G_EW || G.kind == G_RED) {
       specs[gi] = gen_group(hg, G, g->num_sms);
       ws_need = std::max<size_t>(ws_need, specs[gi].ws_floats);
+    } else if (hg.nodes[G.sink].op == CG_DOT) {
+      const Node& nd = hg.nodes[G.sink];
+      const Shape& as = hg.nodes[nd.preds[0]].shape;
+      const int M = (int)nd.shape[0], N = (int)nd.shape[1], K = (int)(nd.attr.ta ? as[0] : as[1]);
+      if (dot_small_kind(M, N, K) != DOT_SMALL_NONE)
+        ws_need = std::max(ws_need, dot_small_ws_floats(M, N, K, nd.attr.ta, g->num_sms));
+      else if (dot_tc_supported(M, N, K, nd.attr.ta, nd.attr.tb))
+        ws_need = std::max(ws_need, dot_tc_ws_floats(M, N, K, g->num_sms));
     } else if (hg.nodes[G.sink].op == CG_CONV2D_BWD_KERNEL) {
       const Node& nd = hg.nodes[G.sink];
       ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
@@ -306,11 +315,21 @@ static int build_launches(cg_graph* g) {
         int M = (int)ys[0], N = (int)ys[1], K = (int)(nd.attr.ta ? as[0] : as[1]);
         int ta = nd.attr.ta, tb = nd.attr.tb;
         const float *A = in[0], *B = in[1];
+        if (dot_small_kind(M, N, K) != DOT_SMALL_NONE) {  // one small extent: HBM-bound SIMT
+          float* ws = g->ws;
+          int sms = g->num_sms;
+          const bool split = dot_small_ws_floats(M, N, K, ta, sms) > 0;
+          L.push_back({[A, B, out, ws, M, N, K, ta, tb, sms](cudaStream_t s) {
+                         return launch_dot_small(A, B, out, ws, M, N, K, ta, tb, sms, s);
+                       },
+                       split ? 2 : 1});
+          break;
+        }
         if (dot_tc_supported(M, N, K, ta, tb)) {  // tensor cores (tcgen05, 3xTF32)
           auto plan = std::make_shared<DotTcPlan>();
-          if (dot_tc_prepare(plan.get(), A, B, out, M, N, K, ta, tb) != 0)
+          if (dot_tc_prepare(plan.get(), A, B, out, M, N, K, ta, tb, g->ws, g->num_sms) != 0)
             return g->fail(CG_E_CUDA, "DOT node " + std::to_string(G.sink) + ": cuTensorMapEncodeTiled failed");
-          L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, 1});
+          L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, plan->splits > 1 ? 2 : 1});
           break;
         }
         L.push_back({[A, B, out, M, N, K, ta, tb](cudaStream_t s) { return launch_dot_simt(A, B, out, M, N, K, ta, tb, s); }, 1});

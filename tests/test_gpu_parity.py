@@ -199,6 +199,20 @@ def test_dot_tc_integer_exact(m, n, k, ta, tb):
     assert np.array_equal(got, ref)
 
 
+# small-extent (HBM-bound SIMT) kernels and split-K tensor-core shapes of C3 / C4
+SMALL_SHAPES = [(4096, 10, 1024), (1024, 10, 4096), (4096, 1024, 10), (84, 10, 8192), (8192, 84, 10),
+                (300, 17, 33), (33, 300, 17), (120, 84, 8192), (400, 120, 8192), (7, 5, 3)]
+
+
+@pytest.mark.parametrize("m,n,k", SMALL_SHAPES)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_dot_small_and_splitk_integer_exact(m, n, k, ta, tb):
+    sa = (k, m) if ta else (m, k)
+    sb = (n, k) if tb else (k, n)
+    got, ref = _run_single("DOT", [sa, sb], {"ta": ta, "tb": tb}, -2, 3)
+    assert np.array_equal(got, ref)
+
+
 @pytest.mark.parametrize("m,n,k", [(512, 384, 1000), (4096, 1024, 1024), (1024, 1024, 4096)])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1)])
 def test_dot_tc_float_3xtf32(m, n, k, ta, tb):
