@@ -27,6 +27,7 @@
 #include "../../include/cg.h"
 #include "codegen.h"
 #include "host.h"
+#include "conv_small.h"
 #include "dot_small.h"
 #include "dot_tc.h"
 #include "kernels.h"
@@ -238,7 +239,8 @@ static int build_launches(cg_graph* g) {
     } else if (hg.nodes[G.sink].op == CG_CONV2D_BWD_KERNEL) {
       const Node& nd = hg.nodes[G.sink];
       ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
-      ws_need = std::max(ws_need, conv2d_bwd_kernel_ws(cgm, g->num_sms));
+      ws_need = std::max(ws_need, conv_small_bwdk_ok(cgm) ? conv_small_bwdk_ws(cgm, g->num_sms)
+                                                          : conv2d_bwd_kernel_ws(cgm, g->num_sms));
     }
   }
   if (ws_need) {
@@ -339,14 +341,22 @@ static int build_launches(cg_graph* g) {
         ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, ys, (int)hg.nodes[nd.preds[1]].shape[0],
                             (int)hg.nodes[nd.preds[1]].shape[1]);
         const float *x = in[0], *w = in[1];
-        L.push_back({[x, w, out, cgm](cudaStream_t s) { return launch_conv2d_fwd(x, w, out, cgm, s); }, 1});
+        int sms = g->num_sms;
+        if (conv_small_fwd_ok(cgm))  // whole images in shared memory (few channels)
+          L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
+        else
+          L.push_back({[x, w, out, cgm](cudaStream_t s) { return launch_conv2d_fwd(x, w, out, cgm, s); }, 1});
         break;
       }
       case CG_CONV2D_BWD_INPUT: {
         const Shape& ws = hg.nodes[nd.preds[1]].shape;
         ConvGeom cgm = geom(nd, ys, hg.nodes[nd.preds[0]].shape, (int)ws[0], (int)ws[1]);
         const float *dy = in[0], *w = in[1];
-        L.push_back({[dy, w, out, cgm](cudaStream_t s) { return launch_conv2d_bwd_input(dy, w, out, cgm, s); }, 1});
+        int sms = g->num_sms;
+        if (conv_small_bwdin_ok(cgm))
+          L.push_back({[dy, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_bwdin(dy, w, out, cgm, sms, s); }, 1});
+        else
+          L.push_back({[dy, w, out, cgm](cudaStream_t s) { return launch_conv2d_bwd_input(dy, w, out, cgm, s); }, 1});
         break;
       }
       case CG_CONV2D_BWD_KERNEL: {
@@ -354,8 +364,12 @@ static int build_launches(cg_graph* g) {
         const float *x = in[0], *dy = in[1];
         float* ws = g->ws;
         int sms = g->num_sms;
-        L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv2d_bwd_kernel(x, dy, out, ws, cgm, sms, s); },
-                     2});
+        if (conv_small_bwdk_ok(cgm))
+          L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv_small_bwdk(x, dy, out, ws, cgm, sms, s); },
+                       2});
+        else
+          L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv2d_bwd_kernel(x, dy, out, ws, cgm, sms, s); },
+                       2});
         break;
       }
       case CG_MAXPOOL2D:

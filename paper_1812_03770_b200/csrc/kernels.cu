@@ -241,6 +241,34 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __r
   }
 }
 
+// Non-overlapping windows that tile the input exactly (kh == sh, kw == sw, no
+// padding, h == ho*sh, w == wo*sw): one thread per window routes dy to the first
+// maximal element (kh outer, kw inner) and writes zeros elsewhere — a scatter
+// without conflicts, each element written exactly once.
+__global__ void maxpool_bwd_tiled_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ dx,
+                                         ConvGeom g, long long total) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+    int c = (int)(t % g.co);
+    long long q = t / g.co;
+    int wo = (int)(q % g.wo);
+    q /= g.wo;
+    int ho = (int)(q % g.ho);
+    int n = (int)(q / g.ho);
+    const long long base = ((long long)n * g.h + ho * g.sh) * g.w + wo * g.sw;
+    float m = -__int_as_float(0x7f800000);
+    int best = -1;
+    for (int kh = 0; kh < g.kh; ++kh)
+      for (int kw = 0; kw < g.kw; ++kw) {
+        const float v = x[(base + (long long)kh * g.w + kw) * g.co + c];
+        if (v > m || best < 0) { m = v; best = kh * g.kw + kw; }
+      }
+    const float d = dy[t];
+    for (int kh = 0; kh < g.kh; ++kh)
+      for (int kw = 0; kw < g.kw; ++kw)
+        dx[(base + (long long)kh * g.w + kw) * g.co + c] = (kh * g.kw + kw == best) ? d : 0.f;
+  }
+}
+
 __global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, long long total) {
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
     int c = (int)(t % g.co);
@@ -356,6 +384,11 @@ cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStre
 }
 
 cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s) {
+  if (g.kh == g.sh && g.kw == g.sw && g.pt == 0 && g.pl == 0 && g.h == g.ho * g.sh && g.w == g.wo * g.sw) {
+    long long windows = (long long)g.n * g.ho * g.wo * g.co;
+    maxpool_bwd_tiled_kernel<<<grid_for(windows), 256, 0, s>>>(x, dy, dx, g, windows);
+    return cudaGetLastError();
+  }
   long long total = (long long)g.n * g.h * g.w * g.co;
   maxpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(x, dy, dx, g, total);
   return cudaGetLastError();

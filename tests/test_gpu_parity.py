@@ -256,6 +256,44 @@ def test_conv_family_integer_exact(sh, pad):
     assert np.array_equal(got, ref)
 
 
+# C4's conv geometries (whole-image shared-memory kernels) and a wide-channel
+# geometry that takes the generic kernels; every conv op, integer-valued => exact
+CONV_CASES = [((8, 28, 28, 1), (5, 5, 1, 6), 1, 1), ((8, 14, 14, 6), (5, 5, 6, 16), 1, 0),
+              ((4, 13, 11, 3), (3, 3, 3, 8), 2, 1), ((4, 12, 12, 5), (5, 3, 5, 20), 2, 0),
+              ((2, 9, 9, 40), (3, 3, 40, 48), 1, 1), ((2, 9, 9, 40), (3, 3, 40, 48), 2, 0)]
+
+
+@pytest.mark.parametrize("xs,ws,st,pad", CONV_CASES)
+def test_conv_geometries_integer_exact(xs, ws, st, pad):
+    a = {"sh": st, "sw": st, "pad": pad}
+    got, ref = _run_single("CONV2D", [xs, ws], a, -2, 3)
+    assert np.array_equal(got, ref)
+    ys = ref.shape
+    got, ref = _run_single("CONV2D_BWD_INPUT", [ys, ws], dict(a, h=xs[1], w=xs[2]), -2, 3)
+    assert np.array_equal(got, ref)
+    got, ref = _run_single("CONV2D_BWD_KERNEL", [xs, ys], dict(a, kh=ws[0], kw=ws[1]), -2, 3)
+    assert np.array_equal(got, ref)
+
+
+def test_maxpool_bwd_tiled_exact():
+    """2x2/2 windows tiling a 28x28 input (the scatter kernel), ties included."""
+    rng = np.random.default_rng(3)
+    x = rng.integers(0, 3, (4, 28, 28, 6)).astype(np.float32)
+    dy = rng.integers(1, 5, (4, 14, 14, 6)).astype(np.float32)
+    a = {"kh": 2, "kw": 2, "sh": 2, "sw": 2, "pad": 0}
+    g = cg.Graph(0)
+    vx, vd = g.var(x.shape), g.var(dy.shape)
+    o = g.add_node("MAXPOOL2D_BWD", [vx, vd], **a)
+    g.plan_memory([o])
+    g.assign(vx, x)
+    g.assign(vd, dy)
+    g.eval([o])
+    og = OGraph()
+    ox, od = og.add_leaf("VAR", x.shape), og.add_leaf("VAR", dy.shape)
+    oo = og.add_node("MAXPOOL2D_BWD", [ox, od], a)
+    assert np.array_equal(g.read(o), evaluate(og, {ox: x, od: dy})[oo])
+
+
 @pytest.mark.parametrize("k,s,pad", [(2, 2, 0), (3, 2, 0), (3, 1, 1), (3, 2, 1)])
 def test_pools_exact(k, s, pad):
     a = {"kh": k, "kw": k, "sh": s, "sw": s, "pad": pad}
