@@ -24,15 +24,16 @@ namespace {
 
 constexpr int SMEM_LIMIT = 96 * 1024;
 
-// zero-padded image n of x [N,H,W,C] into s [(H+pt+pb)][(W+pl+pr)][C]
+// zero-padded image n of x [N,H,W,C] into s, channel-planar [C][Hp][Wp] so that
+// threads on adjacent pixels read adjacent words (no bank conflicts)
 __device__ __forceinline__ void load_padded(float* s, const float* __restrict__ x, int n, int H, int W, int C, int Hp,
                                             int Wp, int pt, int pl) {
   const int tot = Hp * Wp * C;
   const float* xi = x + (size_t)n * H * W * C;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {  // e walks the NHWC source order (coalesced)
     const int c = e % C, q = e / C, wp = q % Wp, hp = q / Wp;
     const int h = hp - pt, w = wp - pl;
-    s[e] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xi + ((size_t)h * W + w) * C + c) : 0.f;
+    s[(c * Hp + hp) * Wp + wp] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xi + ((size_t)h * W + w) * C + c) : 0.f;
   }
 }
 
@@ -59,10 +60,10 @@ __global__ void __launch_bounds__(256) conv_fwd_img(const float* __restrict__ x,
       for (int c = 0; c < CO; ++c) acc[c] = 0.f;
       for (int kh = 0; kh < g.kh; ++kh)
         for (int kw = 0; kw < g.kw; ++kw) {
-          const float* xp = xs + ((ho * g.sh + kh) * Wp + wo * g.sw + kw) * g.ci;
+          const float* xp = xs + (ho * g.sh + kh) * Wp + wo * g.sw + kw;
           const float* wp = ws + ((kh * g.kw + kw) * g.ci) * CO;
           for (int ci = 0; ci < g.ci; ++ci) {
-            const float a = xp[ci];
+            const float a = xp[ci * Hp * Wp];
 #pragma unroll
             for (int c = 0; c < CO; c += 4) {
               const float4 b = *reinterpret_cast<const float4*>(wp + ci * CO + c);
@@ -87,16 +88,16 @@ __global__ void __launch_bounds__(256) conv_bwdin_img(const float* __restrict__ 
   extern __shared__ float sm[];
   const int taps = g.kh * g.kw;
   float* wt = sm;                            // [tap][co][CI] (ci padded)
-  float* ds = sm + taps * g.co * CI;         // dy image [ho][wo][co]
+  float* ds = sm + taps * g.co * CI;         // dy image, channel-planar [co][ho*wo]
   for (int e = threadIdx.x; e < taps * g.co * CI; e += blockDim.x) {
     const int ci = e % CI, q = e / CI, co = q % g.co, t = q / g.co;
     wt[e] = ci < g.ci ? w[((size_t)t * g.ci + ci) * g.co + co] : 0.f;
   }
-  const int P = g.h * g.w, PO = g.ho * g.wo * g.co;
+  const int P = g.h * g.w, PO = g.ho * g.wo * g.co, PP = g.ho * g.wo;
   for (int n = blockIdx.x; n < g.n; n += gridDim.x) {
     __syncthreads();
     const float* dyi = dy + (size_t)n * PO;
-    for (int e = threadIdx.x; e < PO; e += blockDim.x) ds[e] = __ldg(dyi + e);
+    for (int e = threadIdx.x; e < PO; e += blockDim.x) ds[(e % g.co) * PP + e / g.co] = __ldg(dyi + e);
     __syncthreads();
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       const int hi = p / g.w, wi = p % g.w;
@@ -113,10 +114,10 @@ __global__ void __launch_bounds__(256) conv_bwdin_img(const float* __restrict__ 
           if (wsn < 0 || wsn % g.sw) continue;
           const int wo = wsn / g.sw;
           if (wo >= g.wo) continue;
-          const float* dp = ds + (ho * g.wo + wo) * g.co;
+          const float* dp = ds + ho * g.wo + wo;
           const float* wp = wt + (kh * g.kw + kw) * g.co * CI;
           for (int co = 0; co < g.co; ++co) {
-            const float d = dp[co];
+            const float d = dp[co * PP];
 #pragma unroll
             for (int c = 0; c < CI; c += 4) {
               const float4 b = *reinterpret_cast<const float4*>(wp + co * CI + c);
@@ -169,11 +170,11 @@ __global__ void __launch_bounds__(256) conv_bwdk_img(const float* __restrict__ x
       for (int p = ph; p < P; p += PH) {
         const int ho = p / g.wo, wo = p % g.wo;
         const float4 d = *reinterpret_cast<const float4*>(ds + p * co4 + q * 4);
-        const float* xp = xs + ((ho * g.sh + kh) * Wp + wo * g.sw + kw) * g.ci;
+        const float* xp = xs + (ho * g.sh + kh) * Wp + wo * g.sw + kw;
 #pragma unroll
         for (int c = 0; c < CI; ++c) {
           if (c < g.ci) {
-            const float a = xp[c];
+            const float a = xp[c * Hp * Wp];
             acc[c][0] = fmaf(a, d.x, acc[c][0]);
             acc[c][1] = fmaf(a, d.y, acc[c][1]);
             acc[c][2] = fmaf(a, d.z, acc[c][2]);
@@ -235,7 +236,7 @@ size_t bwdk_smem(const ConvGeom& g) {
   size_t red = (size_t)PH * g.kh * g.kw * g.ci * co4;
   return std::max(img, red) * 4;
 }
-int bwdk_blocks(const ConvGeom& g, int num_sms) { return std::min(g.n, num_sms * 2); }
+int bwdk_blocks(const ConvGeom& g, int num_sms) { return std::min(g.n, num_sms * 8); }
 
 template <typename F>
 void set_smem(F f) {
