@@ -37,7 +37,7 @@ __device__ __forceinline__ void load_padded(float* s, const float* __restrict__ 
   }
 }
 
-template <int CO>
+template <int CO, int KS>  // KS > 0: square KS x KS kernel known at compile time (unrolled taps)
 __global__ void __launch_bounds__(256) conv_fwd_img(const float* __restrict__ x, const float* __restrict__ w,
                                                     float* __restrict__ y, ConvGeom g, int Hp, int Wp) {
   extern __shared__ float sm[];
@@ -58,10 +58,13 @@ __global__ void __launch_bounds__(256) conv_fwd_img(const float* __restrict__ x,
       float acc[CO];
 #pragma unroll
       for (int c = 0; c < CO; ++c) acc[c] = 0.f;
-      for (int kh = 0; kh < g.kh; ++kh)
-        for (int kw = 0; kw < g.kw; ++kw) {
+      const int KH = KS ? KS : g.kh, KW = KS ? KS : g.kw;
+#pragma unroll
+      for (int kh = 0; kh < KH; ++kh)
+#pragma unroll
+        for (int kw = 0; kw < KW; ++kw) {
           const float* xp = xs + (ho * g.sh + kh) * Wp + wo * g.sw + kw;
-          const float* wp = ws + ((kh * g.kw + kw) * g.ci) * CO;
+          const float* wp = ws + ((kh * KW + kw) * g.ci) * CO;
           for (int ci = 0; ci < g.ci; ++ci) {
             const float a = xp[ci * Hp * Wp];
 #pragma unroll
@@ -82,7 +85,7 @@ __global__ void __launch_bounds__(256) conv_fwd_img(const float* __restrict__ x,
   }
 }
 
-template <int CI>
+template <int CI, int KS>
 __global__ void __launch_bounds__(256) conv_bwdin_img(const float* __restrict__ dy, const float* __restrict__ w,
                                                       float* __restrict__ dx, ConvGeom g) {
   extern __shared__ float sm[];
@@ -104,18 +107,21 @@ __global__ void __launch_bounds__(256) conv_bwdin_img(const float* __restrict__ 
       float acc[CI];
 #pragma unroll
       for (int c = 0; c < CI; ++c) acc[c] = 0.f;
-      for (int kh = 0; kh < g.kh; ++kh) {
+      const int KH = KS ? KS : g.kh, KW = KS ? KS : g.kw;
+#pragma unroll
+      for (int kh = 0; kh < KH; ++kh) {
         const int hs = hi + g.pt - kh;
         if (hs < 0 || hs % g.sh) continue;
         const int ho = hs / g.sh;
         if (ho >= g.ho) continue;
-        for (int kw = 0; kw < g.kw; ++kw) {
+#pragma unroll
+        for (int kw = 0; kw < KW; ++kw) {
           const int wsn = wi + g.pl - kw;
           if (wsn < 0 || wsn % g.sw) continue;
           const int wo = wsn / g.sw;
           if (wo >= g.wo) continue;
           const float* dp = ds + ho * g.wo + wo;
-          const float* wp = wt + (kh * g.kw + kw) * g.co * CI;
+          const float* wp = wt + (kh * KW + kw) * g.co * CI;
           for (int co = 0; co < g.co; ++co) {
             const float d = dp[co * PP];
 #pragma unroll
@@ -167,8 +173,12 @@ __global__ void __launch_bounds__(256) conv_bwdk_img(const float* __restrict__ x
     }
     __syncthreads();
     if (active) {
+      int ho = ph / g.wo, wo = ph % g.wo;  // (ho, wo) of pixel p, advanced incrementally
       for (int p = ph; p < P; p += PH) {
-        const int ho = p / g.wo, wo = p % g.wo;
+        if (p != ph) {
+          wo += PH;
+          while (wo >= g.wo) { wo -= g.wo; ++ho; }
+        }
         const float4 d = *reinterpret_cast<const float4*>(ds + p * co4 + q * 4);
         const float* xp = xs + (ho * g.sh + kh) * Wp + wo * g.sw + kw;
 #pragma unroll
@@ -262,11 +272,16 @@ cudaError_t launch_conv_small_fwd(const float* x, const float* w, float* y, cons
   const int Hp = std::max(p.Hp, g.h + g.pt), Wp = std::max(p.Wp, g.w + g.pl);
   const size_t smem = fwd_smem(g);
   const int grid = std::min(g.n, num_sms * 8);
+  const bool k5 = g.kh == 5 && g.kw == 5;
+#define CG_FWD(CO, KS) \
+  set_smem(conv_fwd_img<CO, KS>);  \
+  conv_fwd_img<CO, KS><<<grid, 256, smem, s>>>(x, w, y, g, Hp, Wp)
   switch (co_pad(g.co)) {
-    case 8: set_smem(conv_fwd_img<8>); conv_fwd_img<8><<<grid, 256, smem, s>>>(x, w, y, g, Hp, Wp); break;
-    case 16: set_smem(conv_fwd_img<16>); conv_fwd_img<16><<<grid, 256, smem, s>>>(x, w, y, g, Hp, Wp); break;
-    default: set_smem(conv_fwd_img<32>); conv_fwd_img<32><<<grid, 256, smem, s>>>(x, w, y, g, Hp, Wp); break;
+    case 8: if (k5) { CG_FWD(8, 5); } else { CG_FWD(8, 0); } break;
+    case 16: if (k5) { CG_FWD(16, 5); } else { CG_FWD(16, 0); } break;
+    default: if (k5) { CG_FWD(32, 5); } else { CG_FWD(32, 0); } break;
   }
+#undef CG_FWD
   return cudaGetLastError();
 }
 
@@ -274,11 +289,16 @@ cudaError_t launch_conv_small_bwdin(const float* dy, const float* w, float* dx, 
                                     cudaStream_t s) {
   const size_t smem = bwdin_smem(g);
   const int grid = std::min(g.n, num_sms * 8);
+  const bool k5 = g.kh == 5 && g.kw == 5;
+#define CG_BIN(CI, KS) \
+  set_smem(conv_bwdin_img<CI, KS>);  \
+  conv_bwdin_img<CI, KS><<<grid, 256, smem, s>>>(dy, w, dx, g)
   switch (co_pad(g.ci)) {
-    case 8: set_smem(conv_bwdin_img<8>); conv_bwdin_img<8><<<grid, 256, smem, s>>>(dy, w, dx, g); break;
-    case 16: set_smem(conv_bwdin_img<16>); conv_bwdin_img<16><<<grid, 256, smem, s>>>(dy, w, dx, g); break;
-    default: set_smem(conv_bwdin_img<32>); conv_bwdin_img<32><<<grid, 256, smem, s>>>(dy, w, dx, g); break;
+    case 8: if (k5) { CG_BIN(8, 5); } else { CG_BIN(8, 0); } break;
+    case 16: if (k5) { CG_BIN(16, 5); } else { CG_BIN(16, 0); } break;
+    default: if (k5) { CG_BIN(32, 5); } else { CG_BIN(32, 0); } break;
   }
+#undef CG_BIN
   return cudaGetLastError();
 }
 

@@ -55,6 +55,32 @@ __global__ void reduce_finalize_kernel(const float* __restrict__ ws, float* __re
   out[j] = acc;
 }
 
+// Few outputs, many partials: one block per output, each thread a strided
+// sequential sum, then a fixed-order shared-memory tree (deterministic).
+__global__ void __launch_bounds__(256) reduce_finalize_tree_kernel(const float* __restrict__ ws, float* __restrict__ out,
+                                                                   long long oi, long long S, int op) {
+  __shared__ float sm[256];
+  const long long j = blockIdx.x;
+  float acc = op == 0 ? 0.f : -__int_as_float(0x7f800000);
+  for (long long s = threadIdx.x; s < S; s += 256) {
+    const float v = ws[s * oi + j];
+    if (op == 0) acc = __fadd_rn(acc, v);
+    else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v));
+  }
+  sm[threadIdx.x] = acc;
+  __syncthreads();
+  for (int h = 128; h >= 1; h /= 2) {
+    if (threadIdx.x < h) {
+      float a = sm[threadIdx.x], b = sm[threadIdx.x + h];
+      if (op == 0) a = __fadd_rn(a, b);
+      else asm("max.NaN.f32 %0, %0, %1;" : "+f"(a) : "f"(b));
+      sm[threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = sm[0];
+}
+
 // 64x64 output tile, 16-deep k slab, 256 threads x (4x4) outputs, fp32 FFMA
 __global__ void __launch_bounds__(256) dot_simt_kernel(const float* __restrict__ A, const float* __restrict__ B,
                                                       float* __restrict__ C, int M, int N, int K, int ta, int tb) {
@@ -324,6 +350,10 @@ cudaError_t launch_copy(const float* src, float* dst, long long n, cudaStream_t 
 }
 
 cudaError_t launch_reduce_finalize(const float* ws, float* out, long long oi, long long S, int op, cudaStream_t s) {
+  if (S >= 64 && oi <= 16384) {
+    reduce_finalize_tree_kernel<<<(unsigned)oi, 256, 0, s>>>(ws, out, oi, S, op);
+    return cudaGetLastError();
+  }
   reduce_finalize_kernel<<<(unsigned)((oi + 255) / 256), 256, 0, s>>>(ws, out, oi, S, op);
   return cudaGetLastError();
 }
