@@ -44,6 +44,7 @@ constexpr int TILE_BYTES = BM * BK * 4;             // 16 KiB: one operand tile 
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // A hi, B hi, A lo, B lo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
 constexpr int THREADS = 192;
+constexpr int THREADS_GATHER = 320;  // + 4 warps gathering the im2col A tile
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -110,9 +111,18 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t tile, int mn_major, int k
   return mn_major ? sdesc(tile + kk * 1024, 4096, 512, 1) : sdesc(tile + kk * 32, 16, 1024, 2);
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
-    dot_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
-                  int M, int N, int K, int a_mn, int b_mn, int kb_per_split, float* __restrict__ dbg) {
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+// GATHER = false: A and B by TMA (DOT).  GATHER = true: A is the implicit im2col
+// matrix of an NHWC convolution, gathered row by row with 16-byte cp.async by
+// warps 6..9 straight into the SWIZZLE_128B K-major layout (zero-fill outside
+// the image = the padding); B (HWIO weights = [K, Co] row-major) by TMA.
+template <bool GATHER>
+__global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
+                   int M, int N, int K, int a_mn, int b_mn, int kb_per_split, ConvA cv, float* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -134,13 +144,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full(s), 1);
+      mbar_init(full(s), GATHER ? 1 + 128 : 1);
       mbar_init(conv(s), 4);
       mbar_init(empty(s), 1);
     }
     mbar_init(tfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    if (!GATHER) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
   }
   if (warp == 1) {
@@ -159,9 +169,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t ph = (kb / STAGES) & 1;
         mbar_wait(empty(s), ph ^ 1);
         const uint32_t st = sbase + s * STAGE_BYTES;
-        mbar_expect_tx(full(s), 2 * TILE_BYTES);
+        mbar_expect_tx(full(s), GATHER ? TILE_BYTES : 2 * TILE_BYTES);
         const int k0 = (kb0 + kb) * BK;
-        if (a_mn) {
+        if (GATHER) {
+        } else if (a_mn) {
           for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &mapA, m0 + 32 * j, k0, full(s));
         } else {
           tma_load_2d(st, &mapA, k0, m0, full(s));
@@ -196,6 +207,36 @@ __global__ void __launch_bounds__(THREADS, 1)
         mma_commit(empty(s));  // frees the stage once these MMAs have read it
       }
       mma_commit(tfull);
+    }
+  } else if (GATHER && warp >= 6) {
+    // ---------------- warps 6..9: im2col gather of A, one tile row (output pixel) per thread
+    const int r = threadIdx.x - 192;
+    const int m = m0 + r;
+    int n = 0, ho = 0, wo = 0;
+    if (m < M) {
+      const int hw = cv.Ho * cv.Wo;
+      n = m / hw;
+      const int q = m - n * hw;
+      ho = q / cv.Wo;
+      wo = q - ho * cv.Wo;
+    }
+    const int hb = ho * cv.sh - cv.pt, wb = wo * cv.sw - cv.pl;
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      mbar_wait(empty(s), ph ^ 1);
+      const uint32_t row = sbase + s * STAGE_BYTES + r * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int k = (kb0 + kb) * BK + 4 * j;
+        const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
+        const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
+        const int hi = hb + kh, wi = wb + kw;
+        const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
+        const float* src = ok ? cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci : cv.x;
+        cp_async16(row + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
     }
   } else {
     // ---------------- warps 2..5: hi/lo split of each stage, then the epilogue
@@ -360,17 +401,46 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(dot_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
   dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
   float* out = p.splits > 1 ? p.ws : p.C;
-  dot_tc_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, p.a_mn, p.b_mn, p.kb_per_split, p.dbg);
+  if (p.conv.x)
+    gemm_tc_kernel<true><<<grid, THREADS_GATHER, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, 0, 1, p.kb_per_split, p.conv,
+                                                                   p.dbg);
+  else
+    gemm_tc_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, p.a_mn, p.b_mn, p.kb_per_split, p.conv,
+                                                             p.dbg);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_reduce_finalize(p.ws, p.C, (long long)p.M * p.N, p.splits, 0, s);
+}
+
+bool conv_tc_supported(int ci, int co, long long m) { return ci % 4 == 0 && co % 4 == 0 && co >= 16 && m >= 128; }
+
+int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int n, int h, int wd, int ci, int kh, int kw,
+                    int co, int ho, int wo, int sh, int sw, int pt, int pl, float* ws, int num_sms) {
+  const long long M = (long long)n * ho * wo;
+  if (!conv_tc_supported(ci, co, M) || M > INT32_MAX) return -1;
+  std::memset(p, 0, sizeof(*p));
+  p->M = (int)M; p->N = co; p->K = kh * kw * ci;
+  dot_tc_split(p->M, p->N, p->K, num_sms, &p->splits, &p->kb_per_split);
+  p->ws = ws;
+  if (p->splits > 1 && !ws) return -3;
+  p->a_mn = 0; p->b_mn = 1;
+  p->C = y;
+  p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl};
+  // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0
+  return make_map(reinterpret_cast<CUtensorMap*>(p->mapB), w, p->K, co, 32, true) ? 0 : -2;
+}
+
+size_t conv_tc_ws_floats(long long M, int co, int K, int num_sms) {
+  return M > INT32_MAX ? 0 : dot_tc_ws_floats((int)M, co, K, num_sms);
 }
 
 }  // namespace cg

@@ -236,6 +236,12 @@ static int build_launches(cg_graph* g) {
         ws_need = std::max(ws_need, dot_small_ws_floats(M, N, K, nd.attr.ta, g->num_sms));
       else if (dot_tc_supported(M, N, K, nd.attr.ta, nd.attr.tb))
         ws_need = std::max(ws_need, dot_tc_ws_floats(M, N, K, g->num_sms));
+    } else if (hg.nodes[G.sink].op == CG_CONV2D) {
+      const Node& nd = hg.nodes[G.sink];
+      const Shape &xs = hg.nodes[nd.preds[0]].shape, &wsh = hg.nodes[nd.preds[1]].shape;
+      const long long M = (long long)nd.shape[0] * nd.shape[1] * nd.shape[2];
+      if (conv_tc_supported((int)xs[3], (int)nd.shape[3], M))
+        ws_need = std::max(ws_need, conv_tc_ws_floats(M, (int)nd.shape[3], (int)(wsh[0] * wsh[1] * wsh[2]), g->num_sms));
     } else if (hg.nodes[G.sink].op == CG_CONV2D_BWD_KERNEL) {
       const Node& nd = hg.nodes[G.sink];
       ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
@@ -342,7 +348,13 @@ static int build_launches(cg_graph* g) {
                             (int)hg.nodes[nd.preds[1]].shape[1]);
         const float *x = in[0], *w = in[1];
         int sms = g->num_sms;
-        if (conv_small_fwd_ok(cgm))  // whole images in shared memory (few channels)
+        if (conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo)) {  // tcgen05 implicit GEMM
+          auto plan = std::make_shared<DotTcPlan>();
+          if (conv_tc_prepare(plan.get(), x, w, out, cgm.n, cgm.h, cgm.w, cgm.ci, cgm.kh, cgm.kw, cgm.co, cgm.ho, cgm.wo,
+                              cgm.sh, cgm.sw, cgm.pt, cgm.pl, g->ws, sms) != 0)
+            return g->fail(CG_E_CUDA, "CONV2D node " + std::to_string(G.sink) + ": tensor-core plan failed");
+          L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, plan->splits > 1 ? 2 : 1});
+        } else if (conv_small_fwd_ok(cgm))  // whole images in shared memory (few channels)
           L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
         else
           L.push_back({[x, w, out, cgm](cudaStream_t s) { return launch_conv2d_fwd(x, w, out, cgm, s); }, 1});

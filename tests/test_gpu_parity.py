@@ -262,6 +262,36 @@ CONV_CASES = [((8, 28, 28, 1), (5, 5, 1, 6), 1, 1), ((8, 14, 14, 6), (5, 5, 6, 1
               ((4, 13, 11, 3), (3, 3, 3, 8), 2, 1), ((4, 12, 12, 5), (5, 3, 5, 20), 2, 0),
               ((2, 9, 9, 40), (3, 3, 40, 48), 1, 1), ((2, 9, 9, 40), (3, 3, 40, 48), 2, 0)]
 
+# geometries of C5's InceptionV3 convolutions (tcgen05 implicit GEMM, forward)
+TC_CONV_CASES = [((2, 35, 35, 64), (3, 3, 64, 96), 1, 1), ((2, 35, 35, 32), (3, 3, 32, 64), 2, 0),
+                 ((4, 17, 17, 48), (7, 1, 48, 64), 1, 1), ((2, 17, 17, 80), (1, 7, 80, 48), 1, 1),
+                 ((2, 8, 8, 1280), (1, 1, 1280, 320), 1, 1), ((3, 15, 13, 12), (5, 5, 12, 20), 1, 1)]
+
+
+@pytest.mark.parametrize("xs,ws,st,pad", TC_CONV_CASES)
+def test_conv_tc_forward_integer_exact(xs, ws, st, pad):
+    got, ref = _run_single("CONV2D", [xs, ws], {"sh": st, "sw": st, "pad": pad}, -2, 3)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("xs,ws,st,pad", TC_CONV_CASES[:3])
+def test_conv_tc_forward_float(xs, ws, st, pad):
+    """U[-1, 1) data: 3xTF32 implicit GEMM within the dot error budget."""
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, xs).astype(np.float32)
+    w = rng.uniform(-1, 1, ws).astype(np.float32)
+    g = cg.Graph(0)
+    vx, vw = g.var(xs), g.var(ws)
+    o = g.add_node("CONV2D", [vx, vw], sh=st, sw=st, pad=pad)
+    g.plan_memory([o])
+    g.assign(vx, x)
+    g.assign(vw, w)
+    g.eval([o])
+    og = OGraph()
+    ox, ow = og.add_leaf("VAR", xs), og.add_leaf("VAR", ws)
+    oo = og.add_node("CONV2D", [ox, ow], {"sh": st, "sw": st, "pad": pad})
+    assert normwise(g.read(o), evaluate(og, {ox: x, ow: w})[oo]) <= 5e-5
+
 
 @pytest.mark.parametrize("xs,ws,st,pad", CONV_CASES)
 def test_conv_geometries_integer_exact(xs, ws, st, pad):
