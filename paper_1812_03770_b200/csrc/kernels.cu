@@ -12,6 +12,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <climits>
 
 namespace cg {
 
@@ -130,11 +131,12 @@ __global__ void __launch_bounds__(256) dot_simt_kernel(const float* __restrict__
     }
 }
 
+template <typename I>
 __global__ void conv_fwd_kernel(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ y, ConvGeom g,
-                                long long total) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+                                I total) {
+  for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
     int co = (int)(t % g.co);
-    long long q = t / g.co;
+    I q = t / g.co;
     int wo = (int)(q % g.wo);
     q /= g.wo;
     int ho = (int)(q % g.ho);
@@ -155,11 +157,12 @@ __global__ void conv_fwd_kernel(const float* __restrict__ x, const float* __rest
   }
 }
 
+template <typename I>
 __global__ void conv_bwd_input_kernel(const float* __restrict__ dy, const float* __restrict__ w, float* __restrict__ dx,
-                                      ConvGeom g, long long total) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+                                      ConvGeom g, I total) {
+  for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
     int ci = (int)(t % g.ci);
-    long long q = t / g.ci;
+    I q = t / g.ci;
     int wi = (int)(q % g.w);
     q /= g.w;
     int hi = (int)(q % g.h);
@@ -209,10 +212,11 @@ __global__ void conv_bwd_kernel_kernel(const float* __restrict__ x, const float*
   part[(long long)blockIdx.y * outs + o] = acc;
 }
 
-__global__ void maxpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, long long total) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+template <typename I>
+__global__ void maxpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, I total) {
+  for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
     int c = (int)(t % g.co);
-    long long q = t / g.co;
+    I q = t / g.co;
     int wo = (int)(q % g.wo);
     q /= g.wo;
     int ho = (int)(q % g.ho);
@@ -231,11 +235,12 @@ __global__ void maxpool_kernel(const float* __restrict__ x, float* __restrict__ 
   }
 }
 
+template <typename I>
 __global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ dx,
-                                   ConvGeom g, long long total) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+                                   ConvGeom g, I total) {
+  for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
     int c = (int)(t % g.co);
-    long long q = t / g.co;
+    I q = t / g.co;
     int wi0 = (int)(q % g.w);
     q /= g.w;
     int hi0 = (int)(q % g.h);
@@ -271,11 +276,12 @@ __global__ void maxpool_bwd_kernel(const float* __restrict__ x, const float* __r
 // padding, h == ho*sh, w == wo*sw): one thread per window routes dy to the first
 // maximal element (kh outer, kw inner) and writes zeros elsewhere — a scatter
 // without conflicts, each element written exactly once.
+template <typename I>
 __global__ void maxpool_bwd_tiled_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ dx,
-                                         ConvGeom g, long long total) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+                                         ConvGeom g, I total) {
+  for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
     int c = (int)(t % g.co);
-    long long q = t / g.co;
+    I q = t / g.co;
     int wo = (int)(q % g.wo);
     q /= g.wo;
     int ho = (int)(q % g.ho);
@@ -295,10 +301,11 @@ __global__ void maxpool_bwd_tiled_kernel(const float* __restrict__ x, const floa
   }
 }
 
-__global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, long long total) {
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+template <typename I>
+__global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, I total) {
+  for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
     int c = (int)(t % g.co);
-    long long q = t / g.co;
+    I q = t / g.co;
     int wo = (int)(q % g.wo);
     q /= g.wo;
     int ho = (int)(q % g.ho);
@@ -319,10 +326,11 @@ __global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ 
   }
 }
 
-__global__ void concat_kernel(ConcatArgs a, float* __restrict__ dst, long long outer, long long dst_inner) {
-  const long long total = outer * dst_inner;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-    long long row = t / dst_inner, col = t % dst_inner;
+template <typename I>
+__global__ void concat_kernel(ConcatArgs a, float* __restrict__ dst, I outer, I dst_inner) {
+  const I total = outer * dst_inner;
+  for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
+    const I row = t / dst_inner, col = t % dst_inner;
     int k = 0;
     while (k + 1 < a.n && col >= a.offset[k + 1]) ++k;
     dst[t] = a.src[k][row * a.inner[k] + (col - a.offset[k])];
@@ -367,13 +375,15 @@ cudaError_t launch_dot_simt(const float* A, const float* B, float* C, int M, int
 
 cudaError_t launch_conv2d_fwd(const float* x, const float* w, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
-  conv_fwd_kernel<<<grid_for(total), 256, 0, s>>>(x, w, y, g, total);
+  if (total < INT32_MAX) conv_fwd_kernel<int><<<grid_for(total), 256, 0, s>>>(x, w, y, g, (int)total);
+  else conv_fwd_kernel<long long><<<grid_for(total), 256, 0, s>>>(x, w, y, g, total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_conv2d_bwd_input(const float* dy, const float* w, float* dx, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.h * g.w * g.ci;
-  conv_bwd_input_kernel<<<grid_for(total), 256, 0, s>>>(dy, w, dx, g, total);
+  if (total < INT32_MAX) conv_bwd_input_kernel<int><<<grid_for(total), 256, 0, s>>>(dy, w, dx, g, (int)total);
+  else conv_bwd_input_kernel<long long><<<grid_for(total), 256, 0, s>>>(dy, w, dx, g, total);
   return cudaGetLastError();
 }
 
@@ -409,29 +419,36 @@ cudaError_t launch_conv2d_bwd_kernel(const float* x, const float* dy, float* dw,
 
 cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
-  maxpool_kernel<<<grid_for(total), 256, 0, s>>>(x, y, g, total);
+  if (total < INT32_MAX) maxpool_kernel<int><<<grid_for(total), 256, 0, s>>>(x, y, g, (int)total);
+  else maxpool_kernel<long long><<<grid_for(total), 256, 0, s>>>(x, y, g, total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s) {
   if (g.kh == g.sh && g.kw == g.sw && g.pt == 0 && g.pl == 0 && g.h == g.ho * g.sh && g.w == g.wo * g.sw) {
     long long windows = (long long)g.n * g.ho * g.wo * g.co;
-    maxpool_bwd_tiled_kernel<<<grid_for(windows), 256, 0, s>>>(x, dy, dx, g, windows);
+    if (windows < INT32_MAX) maxpool_bwd_tiled_kernel<int><<<grid_for(windows), 256, 0, s>>>(x, dy, dx, g, (int)windows);
+    else maxpool_bwd_tiled_kernel<long long><<<grid_for(windows), 256, 0, s>>>(x, dy, dx, g, windows);
     return cudaGetLastError();
   }
   long long total = (long long)g.n * g.h * g.w * g.co;
-  maxpool_bwd_kernel<<<grid_for(total), 256, 0, s>>>(x, dy, dx, g, total);
+  if (total < INT32_MAX) maxpool_bwd_kernel<int><<<grid_for(total), 256, 0, s>>>(x, dy, dx, g, (int)total);
+  else maxpool_bwd_kernel<long long><<<grid_for(total), 256, 0, s>>>(x, dy, dx, g, total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
-  avgpool_kernel<<<grid_for(total), 256, 0, s>>>(x, y, g, total);
+  if (total < INT32_MAX) avgpool_kernel<int><<<grid_for(total), 256, 0, s>>>(x, y, g, (int)total);
+  else avgpool_kernel<long long><<<grid_for(total), 256, 0, s>>>(x, y, g, total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long long dst_inner, cudaStream_t s) {
-  concat_kernel<<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, outer, dst_inner);
+  if (outer * dst_inner < INT32_MAX)
+    concat_kernel<int><<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, (int)outer, (int)dst_inner);
+  else
+    concat_kernel<long long><<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, outer, dst_inner);
   return cudaGetLastError();
 }
 
