@@ -48,6 +48,14 @@ constexpr int THREADS_GATHER = 320;  // + 4 warps gathering the im2col A tile
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
@@ -249,22 +257,25 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         dbg[t] = reinterpret_cast<float*>(smem)[t];                    // A raw
         dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_BYTES)[t];   // B raw
       }
-      float4* hi = reinterpret_cast<float4*>(smem + s * STAGE_BYTES);
-      float4* lo = reinterpret_cast<float4*>(smem + s * STAGE_BYTES + 2 * TILE_BYTES);
-#pragma unroll 4
-      for (int i = t; i < 2 * TILE_BYTES / 16; i += 128) {
-        float4 v = hi[i];
+      // 16 float4 per thread: all loads first (ILP), explicit shared-space ops
+      const uint32_t hb = sbase + s * STAGE_BYTES + t * 16, lb = hb + 2 * TILE_BYTES;
+      constexpr int PER = 2 * TILE_BYTES / 16 / 128;
+      float4 v[PER];
+#pragma unroll
+      for (int j = 0; j < PER; ++j) v[j] = lds128(hb + j * 2048);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
         float4 h, l;
-        h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-        h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-        h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-        h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-        l.x = __fsub_rn(v.x, h.x);
-        l.y = __fsub_rn(v.y, h.y);
-        l.z = __fsub_rn(v.z, h.z);
-        l.w = __fsub_rn(v.w, h.w);
-        hi[i] = h;
-        lo[i] = l;
+        h.x = __uint_as_float(__float_as_uint(v[j].x) & 0xFFFFE000u);
+        h.y = __uint_as_float(__float_as_uint(v[j].y) & 0xFFFFE000u);
+        h.z = __uint_as_float(__float_as_uint(v[j].z) & 0xFFFFE000u);
+        h.w = __uint_as_float(__float_as_uint(v[j].w) & 0xFFFFE000u);
+        l.x = __fsub_rn(v[j].x, h.x);
+        l.y = __fsub_rn(v[j].y, h.y);
+        l.z = __fsub_rn(v[j].z, h.z);
+        l.w = __fsub_rn(v[j].w, h.w);
+        sts128(hb + j * 2048, h);
+        sts128(lb + j * 2048, l);
       }
       // generic-proxy smem writes -> visible to the tensor core (async proxy)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
