@@ -130,7 +130,8 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 template <bool GATHER>
 __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
-                   int M, int N, int K, int a_mn, int b_mn, int kb_per_split, ConvA cv, float* __restrict__ dbg) {
+                   int M, int N, int K, int a_mn, int b_mn, int kb_per_split, ConvA cv, int raw_hi,
+                   float* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         l.y = __fsub_rn(v[j].y, h.y);
         l.z = __fsub_rn(v[j].z, h.z);
         l.w = __fsub_rn(v[j].w, h.w);
-        sts128(hb + j * 2048, h);
+        if (!raw_hi) sts128(hb + j * 2048, h);
         sts128(lb + j * 2048, l);
       }
       // generic-proxy smem writes -> visible to the tensor core (async proxy)
@@ -423,10 +424,10 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   float* out = p.splits > 1 ? p.ws : p.C;
   if (p.conv.x)
     gemm_tc_kernel<true><<<grid, THREADS_GATHER, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, 0, 1, p.kb_per_split, p.conv,
-                                                                   p.dbg);
+                                                                   p.raw_hi, p.dbg);
   else
     gemm_tc_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, p.a_mn, p.b_mn, p.kb_per_split, p.conv,
-                                                             p.dbg);
+                                                             p.raw_hi, p.dbg);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_reduce_finalize(p.ws, p.C, (long long)p.M * p.N, p.splits, 0, s);
@@ -457,11 +458,13 @@ size_t conv_tc_ws_floats(long long M, int co, int K, int num_sms) {
 }  // namespace cg
 
 // ---- debug entry (tests/tools only): one DOT on device buffers, optional dump
-extern "C" int cgx_dot_tc(const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb, float* dbg) {
+extern "C" int cgx_dot_tc(const float* A, const float* B, float* C, int M, int N, int K, int ta, int tb, float* dbg,
+                          int raw_hi) {
   cg::DotTcPlan p;
   int rc = cg::dot_tc_prepare(&p, A, B, C, M, N, K, ta, tb, nullptr, 1);
   if (rc) return rc;
   p.dbg = dbg;
+  p.raw_hi = raw_hi;
   cudaError_t e = cg::launch_dot_tc(p, nullptr);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return e == cudaSuccess ? 0 : -100 - (int)e;
