@@ -5,6 +5,9 @@
 // tcgen05 has no fp32-input MMA, so every fp32 operand x is split into
 // hi = x & 0xFFFFE000 (exactly representable in TF32) and lo = x - hi (exact in
 // fp32), and the product is accumulated as  hi.hi + hi.lo + lo.hi  ("3xTF32",
+// The kind::tf32 datapath itself truncates an fp32 operand to exactly hi (measured:
+// tools/tf32_probe.py, tests test_tf32_truncation_probe), so the raw tile serves
+// as the hi operand and only lo is written back to shared memory.
 // SURVEY §8(c) c12) in fp32 TMEM accumulators.  The dropped lo.lo term is
 // < 2^-20 relative, so the result has fp32-GEMM accuracy.
 // Integer-valued operands with |x| < 2^11 have lo == 0 and are multiplied exactly.
@@ -235,17 +238,35 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       const uint32_t ph = (kb / STAGES) & 1;
       mbar_wait(empty(s), ph ^ 1);
       const uint32_t row = sbase + s * STAGE_BYTES + r * 128;
+      if ((cv.Ci & 3) == 0) {  // 4 consecutive k = 4 channels of one tap: one 16-byte async copy
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int k = (kb0 + kb) * BK + 4 * j;
-        const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
-        const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
-        const int hi = hb + kh, wi = wb + kw;
-        const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
-        const float* src = ok ? cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci : cv.x;
-        cp_async16(row + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+        for (int j = 0; j < 8; ++j) {
+          const int k = (kb0 + kb) * BK + 4 * j;
+          const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
+          const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
+          const int hi = hb + kh, wi = wb + kw;
+          const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
+          const float* src = ok ? cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci : cv.x;
+          cp_async16(row + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
+      } else {  // few input channels (e.g. RGB): element-wise gather, 16-byte shared stores
+#pragma unroll 2
+        for (int j = 0; j < 8; ++j) {
+          float e[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int k = (kb0 + kb) * BK + 4 * j + u;
+            const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
+            const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
+            const int hi = hb + kh, wi = wb + kw;
+            const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
+            e[u] = ok ? __ldg(cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci) : 0.f;
+          }
+          sts128(row + ((j ^ (r & 7)) << 4), make_float4(e[0], e[1], e[2], e[3]));
+        }
+        mbar_arrive(full(s));
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
     }
   } else {
     // ---------------- warps 2..5: hi/lo split of each stage, then the epilogue
@@ -395,6 +416,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   if (!dot_tc_supported(M, N, K, ta, tb)) return -1;
   std::memset(p, 0, sizeof(*p));
   p->M = M; p->N = N; p->K = K;
+  p->raw_hi = 1;  // tcgen05 kind::tf32 truncates fp32 operands (tests: test_tf32_truncation_probe)
   dot_tc_split(M, N, K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
   if (p->splits > 1 && !ws) return -3;
@@ -433,7 +455,7 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   return launch_reduce_finalize(p.ws, p.C, (long long)p.M * p.N, p.splits, 0, s);
 }
 
-bool conv_tc_supported(int ci, int co, long long m) { return ci % 4 == 0 && co % 4 == 0 && co >= 16 && m >= 128; }
+bool conv_tc_supported(int ci, int co, long long m) { return co % 4 == 0 && co >= 16 && m >= 128; }
 
 int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int n, int h, int wd, int ci, int kh, int kw,
                     int co, int ho, int wo, int sh, int sw, int pt, int pl, float* ws, int num_sms) {
@@ -441,6 +463,7 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   if (!conv_tc_supported(ci, co, M) || M > INT32_MAX) return -1;
   std::memset(p, 0, sizeof(*p));
   p->M = (int)M; p->N = co; p->K = kh * kw * ci;
+  p->raw_hi = 1;
   dot_tc_split(p->M, p->N, p->K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
   if (p->splits > 1 && !ws) return -3;

@@ -337,6 +337,59 @@ __global__ void concat_kernel(ConcatArgs a, float* __restrict__ dst, I outer, I 
   }
 }
 
+// ---- channel-vectorised pools / concat (C % 4 == 0): one thread per 4 channels,
+// the same per-lane operation order as the scalar kernels (bit-identical results)
+__device__ __forceinline__ float nanmax(float a, float b) {
+  asm("max.NaN.f32 %0, %0, %1;" : "+f"(a) : "f"(b));
+  return a;
+}
+
+template <bool MAXP>
+__global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ y, ConvGeom g, int total4) {
+  const int C4 = g.co / 4;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total4; t += gridDim.x * blockDim.x) {
+    const int c = t % C4;
+    int q = t / C4;
+    const int wo = q % g.wo;
+    q /= g.wo;
+    const int ho = q % g.ho, n = q / g.ho;
+    const float ninf = -__int_as_float(0x7f800000);
+    float4 acc = MAXP ? make_float4(ninf, ninf, ninf, ninf) : make_float4(0.f, 0.f, 0.f, 0.f);
+    int cnt = 0;
+    for (int kh = 0; kh < g.kh; ++kh) {
+      const int hi = ho * g.sh + kh - g.pt;
+      if (hi < 0 || hi >= g.h) continue;
+      for (int kw = 0; kw < g.kw; ++kw) {
+        const int wi = wo * g.sw + kw - g.pl;
+        if (wi < 0 || wi >= g.w) continue;
+        const float4 v = __ldg(x + (((size_t)n * g.h + hi) * g.w + wi) * C4 + c);
+        if (MAXP) {
+          acc.x = nanmax(acc.x, v.x); acc.y = nanmax(acc.y, v.y); acc.z = nanmax(acc.z, v.z); acc.w = nanmax(acc.w, v.w);
+        } else {
+          acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
+          acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
+        }
+        ++cnt;
+      }
+    }
+    if (!MAXP) {
+      const float f = (float)cnt;
+      acc = make_float4(__fdiv_rn(acc.x, f), __fdiv_rn(acc.y, f), __fdiv_rn(acc.z, f), __fdiv_rn(acc.w, f));
+    }
+    y[t] = acc;
+  }
+}
+
+__global__ void concat4_kernel(ConcatArgs a, float4* __restrict__ dst, int outer, int dst_inner4) {
+  const int total = outer * dst_inner4;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int row = t / dst_inner4, col = (t - row * dst_inner4) * 4;
+    int k = 0;
+    while (k + 1 < a.n && col >= a.offset[k + 1]) ++k;
+    dst[t] = __ldg(reinterpret_cast<const float4*>(a.src[k] + (size_t)row * a.inner[k] + (col - a.offset[k])));
+  }
+}
+
 int grid_for(long long total, int threads = 256) {
   long long b = (total + threads - 1) / threads;
   return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 16));
@@ -419,6 +472,10 @@ cudaError_t launch_conv2d_bwd_kernel(const float* x, const float* dy, float* dw,
 
 cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
+  if (g.co % 4 == 0 && total < INT32_MAX) {
+    pool4_kernel<true><<<grid_for(total / 4), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
+    return cudaGetLastError();
+  }
   if (total < INT32_MAX) maxpool_kernel<int><<<grid_for(total), 256, 0, s>>>(x, y, g, (int)total);
   else maxpool_kernel<long long><<<grid_for(total), 256, 0, s>>>(x, y, g, total);
   return cudaGetLastError();
@@ -439,12 +496,22 @@ cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const
 
 cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
+  if (g.co % 4 == 0 && total < INT32_MAX) {
+    pool4_kernel<false><<<grid_for(total / 4), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
+    return cudaGetLastError();
+  }
   if (total < INT32_MAX) avgpool_kernel<int><<<grid_for(total), 256, 0, s>>>(x, y, g, (int)total);
   else avgpool_kernel<long long><<<grid_for(total), 256, 0, s>>>(x, y, g, total);
   return cudaGetLastError();
 }
 
 cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long long dst_inner, cudaStream_t s) {
+  bool vec = dst_inner % 4 == 0 && outer * dst_inner < INT32_MAX;
+  for (int k = 0; k < a.n; ++k) vec = vec && a.inner[k] % 4 == 0 && a.offset[k] % 4 == 0;
+  if (vec) {
+    concat4_kernel<<<grid_for(outer * dst_inner / 4), 256, 0, s>>>(a, (float4*)dst, (int)outer, (int)(dst_inner / 4));
+    return cudaGetLastError();
+  }
   if (outer * dst_inner < INT32_MAX)
     concat_kernel<int><<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, (int)outer, (int)dst_inner);
   else

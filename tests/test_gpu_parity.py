@@ -213,6 +213,24 @@ def test_dot_small_and_splitk_integer_exact(m, n, k, ta, tb):
     assert np.array_equal(got, ref)
 
 
+def test_tf32_truncation_probe():
+    """The production 3xTF32 path feeds the raw fp32 tile as the hi operand, relying
+    on tcgen05.mma.kind::tf32 truncating fp32 inputs to TF32.  Check that against
+    an explicitly masked hi tile: the two products must be bit-identical."""
+    import ctypes
+    import torch
+    f = cg.lib().cgx_dot_tc
+    f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 5 + [ctypes.c_void_p, ctypes.c_int]
+    torch.manual_seed(0)
+    A = torch.rand(384, 512, device="cuda") * 2 - 1
+    B = torch.rand(512, 256, device="cuda") * 2 - 1
+    C0 = torch.zeros(384, 256, device="cuda")
+    C1 = torch.zeros(384, 256, device="cuda")
+    assert f(A.data_ptr(), B.data_ptr(), C0.data_ptr(), 384, 256, 512, 0, 0, None, 0) == 0
+    assert f(A.data_ptr(), B.data_ptr(), C1.data_ptr(), 384, 256, 512, 0, 0, None, 1) == 0
+    assert torch.equal(C0, C1)
+
+
 @pytest.mark.parametrize("m,n,k", [(512, 384, 1000), (4096, 1024, 1024), (1024, 1024, 4096)])
 @pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1)])
 def test_dot_tc_float_3xtf32(m, n, k, ta, tb):
@@ -265,7 +283,8 @@ CONV_CASES = [((8, 28, 28, 1), (5, 5, 1, 6), 1, 1), ((8, 14, 14, 6), (5, 5, 6, 1
 # geometries of C5's InceptionV3 convolutions (tcgen05 implicit GEMM, forward)
 TC_CONV_CASES = [((2, 35, 35, 64), (3, 3, 64, 96), 1, 1), ((2, 35, 35, 32), (3, 3, 32, 64), 2, 0),
                  ((4, 17, 17, 48), (7, 1, 48, 64), 1, 1), ((2, 17, 17, 80), (1, 7, 80, 48), 1, 1),
-                 ((2, 8, 8, 1280), (1, 1, 1280, 320), 1, 1), ((3, 15, 13, 12), (5, 5, 12, 20), 1, 1)]
+                 ((2, 8, 8, 1280), (1, 1, 1280, 320), 1, 1), ((3, 15, 13, 12), (5, 5, 12, 20), 1, 1),
+                 ((2, 31, 29, 3), (3, 3, 3, 32), 2, 0), ((2, 20, 20, 6), (5, 5, 6, 16), 1, 1)]
 
 
 @pytest.mark.parametrize("xs,ws,st,pad", TC_CONV_CASES)
@@ -322,6 +341,30 @@ def test_maxpool_bwd_tiled_exact():
     ox, od = og.add_leaf("VAR", x.shape), og.add_leaf("VAR", dy.shape)
     oo = og.add_node("MAXPOOL2D_BWD", [ox, od], a)
     assert np.array_equal(g.read(o), evaluate(og, {ox: x, od: dy})[oo])
+
+
+@pytest.mark.parametrize("k,s,pad", [(2, 2, 0), (3, 2, 0), (3, 1, 1), (3, 2, 1), (8, 8, 0)])
+@pytest.mark.parametrize("c", [4, 12])
+def test_pools_channel_vectorised(k, s, pad, c):
+    """C % 4 == 0: the float4-over-channels pool kernels (C5's pools)."""
+    a = {"kh": k, "kw": k, "sh": s, "sw": s, "pad": pad}
+    got, ref = _run_single("MAXPOOL2D", [(2, 17, 16, c)], a, -3, 4)
+    assert np.array_equal(got, ref)
+    got, ref = _run_single("AVGPOOL2D", [(2, 17, 16, c)], a, -3, 4)
+    assert normwise(got, ref) <= 1e-6
+
+
+def test_concat_vectorised():
+    rng = np.random.default_rng(4)
+    xs = [rng.standard_normal((2, 5, 3, c)).astype(np.float32) for c in (64, 96, 32, 128)]
+    g = cg.Graph(0)
+    ids = [g.var(x.shape) for x in xs]
+    cat = g.add_node("CONCAT", ids, axis=3)
+    g.plan_memory([cat])
+    for i, x in zip(ids, xs):
+        g.assign(i, x)
+    g.eval([cat])
+    assert np.array_equal(g.read(cat), np.concatenate(xs, axis=3))
 
 
 @pytest.mark.parametrize("k,s,pad", [(2, 2, 0), (3, 2, 0), (3, 1, 1), (3, 2, 1)])
