@@ -240,7 +240,7 @@ static int build_launches(cg_graph* g) {
       const Node& nd = hg.nodes[G.sink];
       const Shape &xs = hg.nodes[nd.preds[0]].shape, &wsh = hg.nodes[nd.preds[1]].shape;
       const long long M = (long long)nd.shape[0] * nd.shape[1] * nd.shape[2];
-      if (conv_tc_supported((int)xs[3], (int)nd.shape[3], M))
+      if (conv_tc_supported((int)xs[3], (int)nd.shape[3], M))  // (may still take the small-channel kernel: ws is harmless)
         ws_need = std::max(ws_need, conv_tc_ws_floats(M, (int)nd.shape[3], (int)(wsh[0] * wsh[1] * wsh[2]), g->num_sms));
     } else if (hg.nodes[G.sink].op == CG_CONV2D_BWD_KERNEL) {
       const Node& nd = hg.nodes[G.sink];
@@ -348,7 +348,9 @@ static int build_launches(cg_graph* g) {
                             (int)hg.nodes[nd.preds[1]].shape[1]);
         const float *x = in[0], *w = in[1];
         int sms = g->num_sms;
-        if (conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo)) {  // tcgen05 implicit GEMM
+        if (conv_small_fwd_ok(cgm) && cgm.co <= 16) {  // few channels: whole images in shared memory (HBM-bound)
+          L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
+        } else if (conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo)) {  // tcgen05 implicit GEMM
           auto plan = std::make_shared<DotTcPlan>();
           if (conv_tc_prepare(plan.get(), x, w, out, cgm.n, cgm.h, cgm.w, cgm.ci, cgm.kh, cgm.kw, cgm.co, cgm.ho, cgm.wo,
                               cgm.sh, cgm.sw, cgm.pt, cgm.pl, g->ws, sms) != 0)
