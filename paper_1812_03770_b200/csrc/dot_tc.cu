@@ -46,8 +46,8 @@ constexpr int STAGES = 3;
 constexpr int TILE_BYTES = BM * BK * 4;             // 16 KiB: one operand tile (BN == BM)
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // A hi, B hi, A lo, B lo
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
-constexpr int THREADS = 192;
-constexpr int THREADS_GATHER = 320;  // + 4 warps gathering the im2col A tile
+constexpr int THREADS = 320;         // TMA, MMA, 4 split warps, 4 epilogue warps
+constexpr int THREADS_GATHER = 448;  // + 4 warps gathering the im2col A tile
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -126,33 +126,51 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 
-// GATHER = false: A and B by TMA (DOT).  GATHER = true: A is the implicit im2col
-// matrix of an NHWC convolution, gathered row by row with 16-byte cp.async by
-// warps 6..9 straight into the SWIZZLE_128B K-major layout (zero-fill outside
-// the image = the padding); B (HWIO weights = [K, Co] row-major) by TMA.
+// Persistent, warp-specialised kernel; one CTA per SM walks the work units
+// u = (split z, m-tile, n-tile) with the n-tile fastest.  Roles:
+//   warp 0        TMA producer (B; and A for DOT)
+//   warp 1        TMEM allocator + MMA issuer (one thread); two 128-column
+//                 accumulators so the epilogue of unit j overlaps the MMAs of j+1
+//   warps 2-5     hi/lo split of each stage (writes lo; the raw tile is the hi operand)
+//   warps 6-9     epilogue: tcgen05.ld TMEM -> registers -> C (TMEM lane quadrant = warp % 4)
+//   warps 10-13   (GATHER) implicit im2col: A rows gathered from the NHWC input,
+//                 16-byte cp.async straight into the SWIZZLE_128B K-major layout
+//                 (zero-fill outside the image = the padding)
+// Pipelines: full/conv/empty per smem stage (producer -> split -> MMA -> producer)
+// and tfull/tempty per accumulator (MMA -> epilogue -> MMA); the stage index and
+// phase run on a k-block counter that continues across units, so the producers
+// prefetch the next unit while the current one finishes.
 template <bool GATHER>
 __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
-                   int M, int N, int K, int a_mn, int b_mn, int kb_per_split, ConvA cv, int raw_hi,
+                   int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
                    float* __restrict__ dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
-  // full[s] (TMA landed), conv[s] (hi/lo split done), empty[s] (MMAs of stage s done), tfull
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
   auto conv = [&](int s) { return bar0 + 8u * (STAGES + s); };
   auto empty = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
-  const uint32_t tfull = bar0 + 8u * (3 * STAGES);
+  auto tfull = [&](int b) { return bar0 + 8u * (3 * STAGES + b); };
+  auto tempty = [&](int b) { return bar0 + 8u * (3 * STAGES + 2 + b); };
   uint32_t* tmem_slot = (uint32_t*)(smem + STAGES * STAGE_BYTES + 512);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  // split-K: CTA z covers k-blocks [kb0, kb0 + nk) and writes partial plane z
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int nk = min((K + BK - 1) / BK - kb0, kb_per_split);
-  C += (size_t)blockIdx.z * M * N;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int units = tiles_m * tiles_n * splits;
+  const int nkt = (K + BK - 1) / BK;
+  // unit -> (z, m0, n0, kb0, nk)
+  auto unit = [&](int u, int& z, int& m0, int& n0, int& kb0, int& nk) {
+    const int per = tiles_m * tiles_n;
+    z = u / per;
+    const int rem = u - z * per;
+    m0 = (rem / tiles_n) * BM;
+    n0 = (rem % tiles_n) * BN;
+    kb0 = z * kb_per_split;
+    nk = min(nkt - kb0, kb_per_split);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -160,13 +178,17 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       mbar_init(conv(s), 4);
       mbar_init(empty(s), 1);
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (!GATHER) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(BN));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -176,23 +198,28 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(empty(s), ph ^ 1);
-        const uint32_t st = sbase + s * STAGE_BYTES;
-        mbar_expect_tx(full(s), GATHER ? TILE_BYTES : 2 * TILE_BYTES);
-        const int k0 = (kb0 + kb) * BK;
-        if (GATHER) {
-        } else if (a_mn) {
-          for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &mapA, m0 + 32 * j, k0, full(s));
-        } else {
-          tma_load_2d(st, &mapA, k0, m0, full(s));
-        }
-        if (b_mn) {
-          for (int j = 0; j < BN / 32; ++j) tma_load_2d(st + TILE_BYTES + j * 4096, &mapB, n0 + 32 * j, k0, full(s));
-        } else {
-          tma_load_2d(st + TILE_BYTES, &mapB, k0, n0, full(s));
+      int it = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int z, m0, n0, kb0, nk;
+        unit(u, z, m0, n0, kb0, nk);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(empty(s), ph ^ 1);
+          const uint32_t st = sbase + s * STAGE_BYTES;
+          mbar_expect_tx(full(s), GATHER ? TILE_BYTES : 2 * TILE_BYTES);
+          const int k0 = (kb0 + kb) * BK;
+          if (GATHER) {
+          } else if (a_mn) {
+            for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &mapA, m0 + 32 * j, k0, full(s));
+          } else {
+            tma_load_2d(st, &mapA, k0, m0, full(s));
+          }
+          if (b_mn) {
+            for (int j = 0; j < BN / 32; ++j) tma_load_2d(st + TILE_BYTES + j * 4096, &mapB, n0 + 32 * j, k0, full(s));
+          } else {
+            tma_load_2d(st + TILE_BYTES, &mapB, k0, n0, full(s));
+          }
         }
       }
     }
@@ -201,145 +228,172 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       // instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(conv(s), ph);
+      int it = 0, j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+        int z, m0, n0, kb0, nk;
+        unit(u, z, m0, n0, kb0, nk);
+        const int b = j & 1;
+        mbar_wait(tempty(b), ((j >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = sbase + s * STAGE_BYTES;
-        const uint32_t ahi = st, bhi = st + TILE_BYTES, alo = st + 2 * TILE_BYTES, blo = st + 3 * TILE_BYTES;
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(conv(s), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t st = sbase + s * STAGE_BYTES;
+          const uint32_t ahi = st, bhi = st + TILE_BYTES, alo = st + 2 * TILE_BYTES, blo = st + 3 * TILE_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-          // small terms first, then the leading hi.hi product
-          mma_tf32(tmem, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
-          mma_tf32(tmem, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
-          mma_tf32(tmem, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, 1u);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+            // small terms first, then the leading hi.hi product
+            mma_tf32(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
+            mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
+            mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, 1u);
+          }
+          mma_commit(empty(s));  // frees the stage once these MMAs have read it
         }
-        mma_commit(empty(s));  // frees the stage once these MMAs have read it
+        mma_commit(tfull(b));
       }
-      mma_commit(tfull);
     }
-  } else if (GATHER && warp >= 6) {
-    // ---------------- warps 6..9: im2col gather of A, one tile row (output pixel) per thread
-    const int r = threadIdx.x - 192;
-    const int m = m0 + r;
-    int n = 0, ho = 0, wo = 0;
-    if (m < M) {
-      const int hw = cv.Ho * cv.Wo;
-      n = m / hw;
-      const int q = m - n * hw;
-      ho = q / cv.Wo;
-      wo = q - ho * cv.Wo;
-    }
-    const int hb = ho * cv.sh - cv.pt, wb = wo * cv.sw - cv.pl;
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(empty(s), ph ^ 1);
-      const uint32_t row = sbase + s * STAGE_BYTES + r * 128;
-      if ((cv.Ci & 3) == 0) {  // 4 consecutive k = 4 channels of one tap: one 16-byte async copy
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int k = (kb0 + kb) * BK + 4 * j;
-          const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
-          const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
-          const int hi = hb + kh, wi = wb + kw;
-          const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
-          const float* src = ok ? cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci : cv.x;
-          cp_async16(row + ((j ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+  } else if (warp < 6) {
+    // ---------------- warps 2..5: hi/lo split of each stage
+    const int t = threadIdx.x - 64;  // 0..127
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int z, m0, n0, kb0, nk;
+      unit(u, z, m0, n0, kb0, nk);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(full(s), ph);
+        if (dbg && u == 0 && kb == 0 && t < 8) {
+          dbg[t] = reinterpret_cast<float*>(smem)[t];                   // A raw
+          dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_BYTES)[t];  // B raw
         }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
-      } else {  // few input channels (e.g. RGB): element-wise gather, 16-byte shared stores
-#pragma unroll 2
-        for (int j = 0; j < 8; ++j) {
-          float e[4];
+        // 16 float4 per thread: all loads first (ILP), explicit shared-space ops
+        const uint32_t hb = sbase + s * STAGE_BYTES + t * 16, lb = hb + 2 * TILE_BYTES;
+        constexpr int PER = 2 * TILE_BYTES / 16 / 128;
+        float4 v[PER];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int k = (kb0 + kb) * BK + 4 * j + u;
+        for (int q = 0; q < PER; ++q) v[q] = lds128(hb + q * 2048);
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+          float4 h, l;
+          h.x = __uint_as_float(__float_as_uint(v[q].x) & 0xFFFFE000u);
+          h.y = __uint_as_float(__float_as_uint(v[q].y) & 0xFFFFE000u);
+          h.z = __uint_as_float(__float_as_uint(v[q].z) & 0xFFFFE000u);
+          h.w = __uint_as_float(__float_as_uint(v[q].w) & 0xFFFFE000u);
+          l.x = __fsub_rn(v[q].x, h.x);
+          l.y = __fsub_rn(v[q].y, h.y);
+          l.z = __fsub_rn(v[q].z, h.z);
+          l.w = __fsub_rn(v[q].w, h.w);
+          if (!raw_hi) sts128(hb + q * 2048, h);
+          sts128(lb + q * 2048, l);
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(conv(s));
+      }
+    }
+  } else if (warp < 10) {
+    // ---------------- warps 6..9: epilogue; this warp may touch TMEM lanes [32*(warp%4), +32)
+    const int sub = warp % 4;
+    const bool vec = (N % 4) == 0;
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      int z, m0, n0, kb0, nk;
+      unit(u, z, m0, n0, kb0, nk);
+      const int b = j & 1;
+      mbar_wait(tfull(b), (j >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (dbg && u == 0 && sub == 0 && lane == 0) {
+        dbg[16] = __uint_as_float(tmem);
+        dbg[17] = (float)nk;
+      }
+      const int row = m0 + sub * 32 + lane;
+      float* Cz = C + (size_t)z * M * N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t r[16];
+        const uint32_t taddr = tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)(b * BN + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+              "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < M && n0 + c0 < N) {
+          float* crow = Cz + (size_t)row * N;
+          const int n = n0 + c0;
+          if (vec && n + 16 <= N) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<float4*>(crow + n + 4 * q) =
+                  make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                              __uint_as_float(r[4 * q + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              if (n + q < N) crow[n + q] = __uint_as_float(r[q]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(b));
+    }
+  } else if (GATHER) {
+    // ---------------- warps 10..13: im2col gather of A, one tile row (output pixel) per thread
+    const int r = threadIdx.x - 320;
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int z, m0, n0, kb0, nk;
+      unit(u, z, m0, n0, kb0, nk);
+      const int m = m0 + r;
+      int n = 0, ho = 0, wo = 0;
+      if (m < M) {
+        const int hw = cv.Ho * cv.Wo;
+        n = m / hw;
+        const int q = m - n * hw;
+        ho = q / cv.Wo;
+        wo = q - ho * cv.Wo;
+      }
+      const int hb = ho * cv.sh - cv.pt, wb = wo * cv.sw - cv.pl;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES;
+        const uint32_t ph = (it / STAGES) & 1;
+        mbar_wait(empty(s), ph ^ 1);
+        const uint32_t row = sbase + s * STAGE_BYTES + r * 128;
+        if ((cv.Ci & 3) == 0) {  // 4 consecutive k = 4 channels of one tap: one 16-byte async copy
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const int k = (kb0 + kb) * BK + 4 * jj;
             const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
             const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
             const int hi = hb + kh, wi = wb + kw;
             const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
-            e[u] = ok ? __ldg(cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci) : 0.f;
+            const float* src = ok ? cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci : cv.x;
+            cp_async16(row + ((jj ^ (r & 7)) << 4), src, ok ? 16u : 0u);
           }
-          sts128(row + ((j ^ (r & 7)) << 4), make_float4(e[0], e[1], e[2], e[3]));
-        }
-        mbar_arrive(full(s));
-      }
-    }
-  } else {
-    // ---------------- warps 2..5: hi/lo split of each stage, then the epilogue
-    const int t = threadIdx.x - 64;  // 0..127
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(full(s), ph);
-      if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && kb == 0 && t < 8) {
-        dbg[t] = reinterpret_cast<float*>(smem)[t];                    // A raw
-        dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_BYTES)[t];   // B raw
-      }
-      // 16 float4 per thread: all loads first (ILP), explicit shared-space ops
-      const uint32_t hb = sbase + s * STAGE_BYTES + t * 16, lb = hb + 2 * TILE_BYTES;
-      constexpr int PER = 2 * TILE_BYTES / 16 / 128;
-      float4 v[PER];
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
+        } else {  // few input channels (e.g. RGB): element-wise gather, 16-byte shared stores
+#pragma unroll 2
+          for (int jj = 0; jj < 8; ++jj) {
+            float e[4];
 #pragma unroll
-      for (int j = 0; j < PER; ++j) v[j] = lds128(hb + j * 2048);
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        float4 h, l;
-        h.x = __uint_as_float(__float_as_uint(v[j].x) & 0xFFFFE000u);
-        h.y = __uint_as_float(__float_as_uint(v[j].y) & 0xFFFFE000u);
-        h.z = __uint_as_float(__float_as_uint(v[j].z) & 0xFFFFE000u);
-        h.w = __uint_as_float(__float_as_uint(v[j].w) & 0xFFFFE000u);
-        l.x = __fsub_rn(v[j].x, h.x);
-        l.y = __fsub_rn(v[j].y, h.y);
-        l.z = __fsub_rn(v[j].z, h.z);
-        l.w = __fsub_rn(v[j].w, h.w);
-        if (!raw_hi) sts128(hb + j * 2048, h);
-        sts128(lb + j * 2048, l);
-      }
-      // generic-proxy smem writes -> visible to the tensor core (async proxy)
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(conv(s));
-    }
-    // epilogue: this warp may touch TMEM lanes [32*(warp%4), +32)
-    mbar_wait(tfull, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (dbg && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
-      dbg[16] = __uint_as_float(tmem);
-      dbg[17] = (float)nk;
-      const uint32_t* lo32 = reinterpret_cast<const uint32_t*>(smem + 2 * TILE_BYTES);
-      dbg[18] = __uint_as_float(lo32[0]);
-      dbg[19] = reinterpret_cast<float*>(smem)[0];
-    }
-    const int sub = warp % 4;
-    const int row = m0 + sub * 32 + lane;
-    const bool vec = (N % 4) == 0;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t r[16];
-      const uint32_t taddr = tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)c0;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-            "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < M) {
-        float* crow = C + (size_t)row * N;
-        const int n = n0 + c0;
-        if (vec && n + 16 <= N) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            *reinterpret_cast<float4*>(crow + n + 4 * q) =
-                make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                            __uint_as_float(r[4 * q + 3]));
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (n + q < N) crow[n + q] = __uint_as_float(r[q]);
+            for (int q = 0; q < 4; ++q) {
+              const int k = (kb0 + kb) * BK + 4 * jj + q;
+              const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
+              const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
+              const int hi = hb + kh, wi = wb + kw;
+              const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
+              e[q] = ok ? __ldg(cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci) : 0.f;
+            }
+            sts128(row + ((jj ^ (r & 7)) << 4), make_float4(e[0], e[1], e[2], e[3]));
+          }
+          mbar_arrive(full(s));
         }
       }
     }
@@ -348,7 +402,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -416,6 +470,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   if (!dot_tc_supported(M, N, K, ta, tb)) return -1;
   std::memset(p, 0, sizeof(*p));
   p->M = M; p->N = N; p->K = K;
+  p->num_sms = num_sms;
   p->raw_hi = 1;  // tcgen05 kind::tf32 truncates fp32 operands (tests: test_tf32_truncation_probe)
   dot_tc_split(M, N, K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
@@ -440,16 +495,17 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
       attr_err = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  dim3 grid((p.N + BN - 1) / BN, (p.M + BM - 1) / BM, p.splits);
+  const int units = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.splits;
+  const int grid = std::max(1, std::min(units, p.num_sms));
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
   float* out = p.splits > 1 ? p.ws : p.C;
   if (p.conv.x)
-    gemm_tc_kernel<true><<<grid, THREADS_GATHER, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, 0, 1, p.kb_per_split, p.conv,
-                                                                   p.raw_hi, p.dbg);
+    gemm_tc_kernel<true><<<grid, THREADS_GATHER, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, 0, 1, p.kb_per_split, p.splits,
+                                                                   p.conv, p.raw_hi, p.dbg);
   else
-    gemm_tc_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, p.a_mn, p.b_mn, p.kb_per_split, p.conv,
-                                                             p.raw_hi, p.dbg);
+    gemm_tc_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, p.a_mn, p.b_mn, p.kb_per_split,
+                                                             p.splits, p.conv, p.raw_hi, p.dbg);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_reduce_finalize(p.ws, p.C, (long long)p.M * p.N, p.splits, 0, s);
@@ -463,6 +519,7 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   if (!conv_tc_supported(ci, co, M) || M > INT32_MAX) return -1;
   std::memset(p, 0, sizeof(*p));
   p->M = (int)M; p->N = co; p->K = kh * kw * ci;
+  p->num_sms = num_sms;
   p->raw_hi = 1;
   dot_tc_split(p->M, p->N, p->K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
@@ -485,6 +542,10 @@ extern "C" int cgx_dot_tc(const float* A, const float* B, float* C, int M, int N
                           int raw_hi) {
   cg::DotTcPlan p;
   int rc = cg::dot_tc_prepare(&p, A, B, C, M, N, K, ta, tb, nullptr, 1);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p.num_sms = sms;
   if (rc) return rc;
   p.dbg = dbg;
   p.raw_hi = raw_hi;
