@@ -217,6 +217,10 @@ def run_c2(args):
         e2e_ms = float(t[0])
     e2e_val = world * algo / (e2e_ms * 1e-3) / 1e9
 
+    secondary = None
+    if not args.no_secondary:
+        secondary = run_secondary(rank, world, local, max(5, args.steps))
+
     if rank == 0:
         hbm, how = peaks()
         achieved = algo / (kernel_ms * 1e-3) / 1e9
@@ -247,10 +251,137 @@ def run_c2(args):
                     "d2h_bytes_per_step": rows * cols * 4, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "cpu_baseline": cpu,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- secondary workloads
+def _time_region(ws, fn, iters):
+    import torch
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(ws)
+    for k in range(iters):
+        fn(k)
+    e.record(ws)
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def _max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def run_secondary(rank, world, local, iters):
+    """BASELINE.json's other metrics on the other configs: C1 full / incremental
+    eval latency, C3 / C4 data-parallel training iterations per second (global
+    batch fixed: 4096 / 8192, split over the ranks), C5 images/s with the plan's
+    peak bytes vs the unshared (eager) allocation."""
+    import torch
+
+    from paper_1812_03770_b200 import cg
+    from paper_1812_03770_b200.dist import dp_spec, make_graph, shard_range
+    from workloads import configs
+    from workloads.gen import materialise, retag
+
+    out = {}
+    dev = torch.device("cuda", local)
+
+    def leaf(rec, off=0):
+        if rec["op"] not in ("VAR", "CONST"):
+            return None
+        return materialise(rec["data"], rec["shape"], row_offset=off)
+
+    # C1: Fig. 1 graph, full eval and incremental re-eval after cg_assign(x3) (P:42)
+    spec = configs.c1(1024)
+    g, outs = cg.build_from_spec(spec, device=local, data_fn=leaf)
+    g.plan_memory(outs, cg.PLAN_INCREMENTAL)
+    ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
+    x3 = [torch.from_numpy(materialise(retag(spec["nodes"][3]["data"], f"x3#{k}"), [1024])).to(dev) for k in range(2)]
+    for _ in range(5):
+        g.eval(outs, cg.EVAL_FULL)
+    torch.cuda.synchronize()
+    full_ms = _time_region(ws, lambda k: g.eval(outs, cg.EVAL_FULL), 200)
+
+    def inc(k):
+        g.assign(3, x3[k % 2])
+        g.eval(outs)
+    inc_ms = _time_region(ws, inc, 200)
+    out["C1"] = {"metric": "eval latency", "unit": "us", "full_eval_us": full_ms * 1e3,
+                 "incremental_eval_us (assign x3 + eval)": inc_ms * 1e3, "x2_evaluations": g.eval_count(2),
+                 "x5_evaluations": g.eval_count(5)}
+    g.destroy()
+
+    # C3 / C4: data-parallel training, global batch split over ranks (strong scaling)
+    for name, fn, gb in (("C3", configs.c3, 4096), ("C4", configs.c4, 8192)):
+        spec = dp_spec(fn, gb, rank, world)
+        start, count = shard_range(gb, rank, world)
+        g = make_graph(local, world, rank)
+        for rec in spec["nodes"]:
+            data = leaf(rec)
+            if rec["op"] in ("VAR", "CONST"):
+                g.add_node(rec["op"], (), dims=rec["shape"], **({"data": data} if data is not None else {}))
+            else:
+                g.add_node(rec["op"], rec["preds"], **rec.get("attrs", {}))
+        for u, v in spec["updates"]:
+            g.add_update(u, v)
+        outs = spec["outputs"]
+        g.optimise(outs)
+        info = g.plan_memory(outs, 0)
+        ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
+        ids = {n["name"]: n["id"] for n in spec["nodes"] if n["op"] == "VAR"}
+        staged = []
+        for it in range(4):
+            d = {}
+            for nm in spec["meta"]["per_iteration"]:
+                rec = spec["nodes"][ids[nm]]
+                d[ids[nm]] = torch.from_numpy(materialise(retag(rec["data"], f"{rec['data']['tag']}@{it}"),
+                                                          rec["shape"], row_offset=start)).to(dev)
+            staged.append(d)
+
+        def step(k):
+            for i, t in staged[k % 4].items():
+                g.assign(i, t)
+            g.eval(outs, cg.EVAL_FULL)
+        for k in range(3):
+            step(k)
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        ms = _max_over_ranks(_time_region(ws, step, iters), world)
+        out[name] = {"metric": "train iters/s", "value": 1e3 / ms, "unit": "iters/s", "ms_per_iter": ms,
+                     "global_batch": gb, "local_batch": count, "scaling": "strong",
+                     "parallelism": f"dp{world}" + (" (NCCL AllReduce nodes)" if world > 1 else ""),
+                     "plan_peak_bytes": info["pool_bytes"] + info["external_bytes"] + info["workspace_bytes"],
+                     "unshared_bytes": info["unshared_bytes"] + info["external_bytes"]}
+        g.destroy()
+
+    # C5: InceptionV3 inference, 256 images per GPU (batch-sharded replicas)
+    spec = configs.c5()
+    g, outs = cg.build_from_spec(spec, device=local, data_fn=leaf)
+    g.optimise(outs)
+    info = g.plan_memory(outs, 0)
+    ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
+    for _ in range(2):
+        g.eval(outs, cg.EVAL_FULL)
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(_time_region(ws, lambda k: g.eval(outs, cg.EVAL_FULL), max(2, iters // 4)), world)
+    peak = info["pool_bytes"] + info["external_bytes"] + info["workspace_bytes"]
+    unshared = info["unshared_bytes"] + info["external_bytes"]
+    out["C5"] = {"metric": "images/s", "value": world * 256 / (ms * 1e-3), "unit": "images/s", "ms_per_eval": ms,
+                 "batch_per_gpu": 256, "scaling": "weak", "plan_peak_bytes": peak, "unshared_bytes": unshared,
+                 "peak_vs_unshared": peak / unshared, "n_groups": info["n_groups"], "n_blocks": info["n_blocks"]}
+    g.destroy()
+    return out
 
 
 def main():
@@ -261,6 +392,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="C2 only (skip the C1/C3/C4/C5 lines)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     if args.impl == "reference":

@@ -528,3 +528,25 @@ def test_c3_full_training():
 
 def test_c4_small_training():
     _teacher_forced(configs.c4(batch=64), 10, 1e-4)
+
+
+def test_c5_inception_sampled_images():
+    """BASELINE configs[4] at full size: InceptionV3 at 299x299x3, batch 256, in the
+    bench's launch configuration; the oracle evaluates images {0, 255} (inference is
+    independent per image) and logits + softmax must agree to 1e-3 normwise."""
+    spec = configs.c5()
+    g, outs, rep, info = gpu_graph(spec, 0)
+    assert info["pool_bytes"] < info["unshared_bytes"]
+    g.eval(outs)
+    logits, probs = g.read(outs[0]), g.read(outs[1])
+    small = configs.c5(batch=2)
+    og, oo = from_spec(small)
+    xrec = spec["nodes"][0]
+    assert xrec["name"] == "X"
+    xs = materialise(xrec["data"], xrec["shape"], rows=[0, 255])
+    vals = evaluate(og, leaf_values(og, {0: xs}))
+    for i, row in enumerate([0, 255]):
+        e_l = normwise(logits[row], vals[oo[0]][i])
+        e_p = normwise(probs[row], vals[oo[1]][i])
+        print(f"C5 image {row}: logits {e_l:.2e} softmax {e_p:.2e}")
+        assert e_l <= 1e-3 and e_p <= 1e-3
