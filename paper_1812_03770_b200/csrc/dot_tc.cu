@@ -288,7 +288,11 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           l.y = __fsub_rn(v[q].y, h.y);
           l.z = __fsub_rn(v[q].z, h.z);
           l.w = __fsub_rn(v[q].w, h.w);
-          if (!raw_hi) sts128(hb + q * 2048, h);
+          // The A tile of a GATHER stage was written by cp.async / st.shared of other
+          // threads (generic proxy); rewriting it here, followed by this thread's
+          // proxy fence, is what makes it visible to the tensor core.  TMA tiles are
+          // async-proxy writes already, so with raw_hi they are read as they are.
+          if (!raw_hi || (GATHER && q < PER / 2)) sts128(hb + q * 2048, h);
           sts128(lb + q * 2048, l);
         }
         // generic-proxy smem writes -> visible to the tensor core (async proxy)

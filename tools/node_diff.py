@@ -29,6 +29,7 @@ SPECS = {
     "C4small": lambda: configs.c4(batch=64),
     "C1": lambda: configs.c1(1024),
     "C2small": lambda: configs.c2(rows=64, cols=1024),
+    "C5small": lambda: configs.c5(batch=2),
 }
 
 
@@ -37,6 +38,7 @@ def main():
     ap.add_argument("spec")
     ap.add_argument("--top", type=int, default=15)
     ap.add_argument("--iters", type=int, default=1, help="compare at the last of N training iterations")
+    ap.add_argument("--first", type=float, default=0.0, help="also print the first nodes (creation order) above this error")
     a = ap.parse_args()
     spec = SPECS[a.spec]()
     ops = [n["id"] for n in spec["nodes"] if n["op"] not in ("VAR", "CONST")]
@@ -80,6 +82,10 @@ def main():
         rows.append((err, n["id"], n["op"], n.get("attrs", {}), list(want.shape), n["preds"]))
     for r in sorted(rows, key=lambda t: -t[0])[: a.top]:
         print(f"err {r[0]:.3e}  id {r[1]} {r[2]} {r[3]} shape {r[4]} preds {r[5]}")
+    if a.first > 0:
+        print("-- first nodes above", a.first)
+        for r in [r for r in rows if r[0] > a.first][: a.top]:
+            print(f"err {r[0]:.3e}  id {r[1]} {r[2]} {r[3]} shape {r[4]} preds {r[5]}")
 
 
 if __name__ == "__main__":
