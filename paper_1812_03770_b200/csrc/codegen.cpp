@@ -254,9 +254,13 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
     const int64_t WV = W / V;
     int TX = (int)std::min<int64_t>(256, (WV + 31) / 32 * 32);
     int TY = 256 / TX;
+    // block = exactly TX x TY threads: a thread with ty >= TY would revisit rows of
+    // the next block, which in an in-place (slid) group reads already-written output
+    ks.block = (uint32_t)(TX * TY);
     int KC = (int)((WV + TX - 1) / TX);
     bool hoist = KC <= 4;
-    b << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(" << args_decl(G, G.materialised, false) << ") {\n";
+    b << "extern \"C\" __global__ void __launch_bounds__(" << TX * TY << ") KNAME(" << args_decl(G, G.materialised, false)
+      << ") {\n";
     b << "  const int tx = threadIdx.x % " << TX << ", ty = threadIdx.x / " << TX << ";\n";
     // hoisted operands (do not depend on the row)
     for (size_t q = 0; q < nin; ++q) {

@@ -350,7 +350,8 @@ static int build_launches(cg_graph* g) {
         int sms = g->num_sms;
         if (conv_small_fwd_ok(cgm) && cgm.co <= 16) {  // few channels: whole images in shared memory (HBM-bound)
           L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
-        } else if (conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo)) {  // tcgen05 implicit GEMM
+        } else if (conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo) &&
+                   !getenv("CG_DEBUG_CONV_SIMT")) {  // tcgen05 implicit GEMM
           auto plan = std::make_shared<DotTcPlan>();
           if (conv_tc_prepare(plan.get(), x, w, out, cgm.n, cgm.h, cgm.w, cgm.ci, cgm.kh, cgm.kw, cgm.co, cgm.ho, cgm.wo,
                               cgm.sh, cgm.sw, cgm.pt, cgm.pl, g->ws, sms) != 0)
@@ -515,7 +516,7 @@ static void mark_dirty_from_var(cg_graph* g, int var) {
 
 static int run_launches(cg_graph* g, const std::vector<char>& R, bool full) {
   HostGraph& hg = g->hg;
-  if (full && !g->graph_failed) {
+  if (full && !g->graph_failed && !getenv("CG_DEBUG_CLOBBER")) {
     if (!g->exec_full) {  // capture once: Gamma order, static addresses
       cudaGraph_t graph;
       bool ok = cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
@@ -545,13 +546,36 @@ static int run_launches(cg_graph* g, const std::vector<char>& R, bool full) {
       return 0;
     }
   }
+  // CG_DEBUG_CLOBBER: verify that every pooled input still holds the bytes its
+  // producer wrote (device checksums); reports the first block overwritten early.
+  static const bool clobber_check = getenv("CG_DEBUG_CLOBBER") != nullptr;
+  std::vector<unsigned long long> produced;
+  std::vector<int> producer;
+  if (clobber_check) {
+    produced.assign(hg.nodes.size(), 0);
+    producer.assign(hg.nodes.size(), -1);
+  }
   for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
     if (!R[gi]) continue;
+    if (clobber_check) {
+      for (int p : hg.groups[gi].inputs) {
+        if (hg.is_external(p) || producer[p] < 0) continue;
+        unsigned long long h = debug_checksum(g->ptr[p], numel(hg.nodes[p].shape), g->stream);
+        if (h != produced[p])
+          fprintf(stderr, "CG_DEBUG_CLOBBER: value %d (block %d, made by group %d) changed before group %zu (sink %d) read it\n",
+                  p, hg.pl.block_of[p], producer[p], gi, hg.groups[gi].sink);
+      }
+    }
     for (auto& L : g->glaunch[gi]) {
       cudaError_t e = L.fn(g->stream);
       if (e != cudaSuccess) return g->cuda_fail(e, "group launch");
       g->launches += L.kernels;
     }
+    if (clobber_check)
+      for (int m : hg.groups[gi].materialised) {
+        produced[m] = debug_checksum(g->ptr[m], numel(hg.nodes[m].shape), g->stream);
+        producer[m] = (int)gi;
+      }
   }
   return 0;
 }

@@ -390,6 +390,15 @@ __global__ void concat4_kernel(ConcatArgs a, float4* __restrict__ dst, int outer
   }
 }
 
+// Debug: position-weighted 64-bit checksum of a buffer (integer atomics: deterministic)
+__global__ void checksum_kernel(const unsigned* __restrict__ w, long long n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc += (unsigned long long)w[i] * (unsigned long long)((i * 2654435761ULL) | 1ULL);
+  for (int o = 16; o >= 1; o /= 2) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
 int grid_for(long long total, int threads = 256) {
   long long b = (total + threads - 1) / threads;
   return (int)std::max<long long>(1, std::min<long long>(b, 148LL * 16));
@@ -517,6 +526,17 @@ cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long
   else
     concat_kernel<long long><<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, outer, dst_inner);
   return cudaGetLastError();
+}
+
+unsigned long long debug_checksum(const float* p, long long n, cudaStream_t s) {
+  static unsigned long long* d = nullptr;
+  if (!d) cudaMalloc(&d, sizeof(unsigned long long));
+  cudaMemsetAsync(d, 0, sizeof(unsigned long long), s);
+  checksum_kernel<<<grid_for(n), 256, 0, s>>>(reinterpret_cast<const unsigned*>(p), n, d);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  return h;
 }
 
 }  // namespace cg

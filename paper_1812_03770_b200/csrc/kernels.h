@@ -48,4 +48,7 @@ struct ConcatArgs {
 };
 cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long long dst_inner, cudaStream_t s);
 
+// Debug only (CG_DEBUG_CLOBBER): checksum of n floats, synchronous on stream s.
+unsigned long long debug_checksum(const float* p, long long n, cudaStream_t s);
+
 }  // namespace cg

@@ -550,3 +550,28 @@ def test_c5_inception_sampled_images():
         e_p = normwise(probs[row], vals[oo[1]][i])
         print(f"C5 image {row}: logits {e_l:.2e} softmax {e_p:.2e}")
         assert e_l <= 1e-3 and e_p <= 1e-3
+
+
+@pytest.mark.parametrize("c", [96, 288, 320, 384, 1000])
+def test_in_place_elementwise_group(c):
+    """An elementwise group that slides onto its dying input's block (Alg. 1 in-place
+    reuse) must read every element before any thread overwrites it: rows of
+    width 288/320/384 give thread blocks that are not a multiple of the row width."""
+    rng = np.random.default_rng(5)
+    R = 4099
+    x1 = rng.standard_normal((R, c // 2)).astype(np.float32)
+    x2 = rng.standard_normal((R, c - c // 2)).astype(np.float32)
+    g = cg.Graph(0)
+    v1, v2 = g.var(x1.shape), g.var(x2.shape)
+    cat = g.add_node("CONCAT", [v1, v2], axis=1)
+    two = g.const(np.float32(2.0))
+    one = g.const(np.float32(1.0))
+    out = g.add_node("RELU", [g.add_node("SUB", [g.add_node("MUL", [cat, two]), one])])
+    info = g.plan_memory([out])
+    assert info["n_blocks"] == 1, "the elementwise group must slide onto the concat's block"
+    g.assign(v1, x1)
+    g.assign(v2, x2)
+    for _ in range(3):
+        g.eval([out], cg.EVAL_FULL)
+        ref = np.maximum(np.concatenate([x1, x2], axis=1) * np.float32(2) - np.float32(1), 0)
+        assert np.array_equal(g.read(out), ref)

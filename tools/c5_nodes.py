@@ -84,6 +84,13 @@ def main():
         if have is None:
             continue
         e = nw(have, want)
+        if n["op"] == "CONCAT" and e > a.first:
+            off = 0
+            for pidx in n["preds"]:
+                c = ref[pidx].shape[-1]
+                print(f"    segment pred {pidx} channels [{off},{off + c}): err {nw(have[..., off:off + c], want[..., off:off + c]):.3e}"
+                      f"  rows: " + " ".join(f"{nw(have[r, ..., off:off + c], want[r, ..., off:off + c]):.1e}" for r in range(2)))
+                off += c
         if e > a.first or (a.ids and str(i) in a.ids.split(",")):
             print(f"err {e:.3e} id {i} {n['op']} {n.get('attrs', {})} shape {g.shape(i)} preds {n['preds']}")
             shown += 1
