@@ -235,18 +235,16 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
   int64_t R = 1;
   std::vector<int64_t> so(nin), si(nin);
   bool row = false;
-  if (k == 1 && W >= 65536 && W % 4096 == 0 && V == 4) {
-    R = W / 4096;
-    for (size_t q = 0; q < nin; ++q) { si[q] = st[q][0]; so[q] = st[q][0] * 4096; }
-    W = 4096;
-    row = true;
-  } else if (k <= 2) {
-    R = k == 2 ? ext[0] : 1;
+  // row mode needs a 2-D view whose rows are short enough to unroll (KC <= 8 column
+  // chunks per thread) and numerous enough to fill the grid; a fully collapsed 1-D
+  // domain (only full-size and scalar operands) is exactly the flat mode's case.
+  if (k == 2 && W / V >= 32 && (W / V + 255) / 256 <= 8) {
+    R = ext[0];
     for (size_t q = 0; q < nin; ++q) {
-      si[q] = st[q][k - 1];
-      so[q] = k == 2 ? st[q][0] : 0;
+      si[q] = st[q][1];
+      so[q] = st[q][0];
     }
-    row = (W / V >= 32) || R == 1;
+    row = true;
   }
   const int U = 2;
   if (row) {
