@@ -73,6 +73,8 @@ typedef enum cg_op {
   CG_CONCAT,           /* n >= 1 inputs along attr axis */
   CG_RESHAPE,          /* row-major reinterpretation to attr dims (numel preserved) */
   CG_ALLREDUCE_SUM,    /* sum over data-parallel ranks (identity at world = 1) [P:26, P:42] */
+  CG_FUSED_ADAGRAD,    /* (g, s, lr, eps) -> lr*g / (sqrt(s) + eps), computed in f64, one rounding;
+                          produced by the AdaGrad rewrite (cg_set_rewrites) [Fused_Adagrad, P:273-277] */
   CG_NUM_OPS
 } cg_op;
 
@@ -120,6 +122,11 @@ typedef struct cg_dist {
 /* Structural effect of cg_optimise; equal to the oracle's counts. */
 typedef struct cg_report {
   int32_t cse_merged, cf_folded, dce_removed;
+  /* pattern rewrites requested with cg_set_rewrites (0 otherwise) [P:273-279] */
+  int32_t rw_identity;   /* x+0, 0+x, x-0, x*1, 1*x, x/1 -> x */
+  int32_t rw_zeroed;     /* x*0, 0*x -> Const zeros */
+  int32_t rw_fma;        /* ADD(MUL(a,b), c) -> FMA(a,b,c) */
+  int32_t rw_adagrad;    /* DIV(MUL(lr,g), ADD(SQRT(s),eps)) -> FUSED_ADAGRAD(g,s,lr,eps) */
 } cg_report;
 
 /* Memory plan summary [P:292-364]. */
@@ -142,6 +149,7 @@ enum { CG_EVAL_NO_UPDATE = 1u,   /* skip update_iopair at the end of this evalua
        CG_EVAL_FULL = 2u,        /* ignore validity: recompute every group */
        CG_EVAL_SYNC = 4u         /* block the host until the evaluation finished */ };
 enum { CG_DUMP_GRAPH = 0, CG_DUMP_PLAN = 1 };
+enum { CG_RW_IDENTITY = 1u, CG_RW_FMA = 2u, CG_RW_ADAGRAD = 4u, CG_RW_ALL = 7u };
 
 /* Create a graph on CUDA `device` (-1: host-only planning mode).  `cuda_stream`
  * is a cudaStream_t (NULL: default stream).  Returns NULL on failure
@@ -158,6 +166,14 @@ cg_node cg_add_node(cg_graph* g, cg_op op, const cg_node* inputs, int32_t n_inpu
  * of every evaluation var <- copy(value(u)) with parallel-assignment semantics.
  * var must be a Var with u's shape; at most one edge per Var. */
 int cg_add_update(cg_graph* g, cg_node u, cg_node var);
+
+/* Request the paper's pattern rewrites [Optimiser, P:273-279] for the next
+ * cg_optimise (BUILD state only): CG_RW_IDENTITY removes "useless calculations"
+ * (adding zero, dividing by one, multiplying by zero or one), CG_RW_FMA fuses a
+ * single-consumer MUL into its ADD, CG_RW_ADAGRAD fuses the AdaGrad
+ * adjusted-gradient subgraph.  They run to a fixpoint before CSE/CF/DCE; kept
+ * values (outputs, update sources) are never removed or absorbed.  Default: none. */
+int cg_set_rewrites(cg_graph* g, uint32_t flags);
 
 /* Declare the graph's outputs [a graph is "defined by its inputs and outputs
  * nodes", P:283] and run CSE -> constant folding -> DCE [P:264-272].  Folded

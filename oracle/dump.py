@@ -42,8 +42,8 @@ class Compiled:
         self.unshared_bytes = sum(4 * numel(n.shape) for n in raw.nodes if n.op not in LEAF)
 
 
-def compile_graph(g, outputs, flags=0, do_optimise=True, compute_values=True) -> Compiled:
-    opt = optimise(g, outputs, compute_values) if do_optimise else no_optimise(g, outputs)
+def compile_graph(g, outputs, flags=0, do_optimise=True, compute_values=True, rewrites=0) -> Compiled:
+    opt = optimise(g, outputs, compute_values, rewrites) if do_optimise else no_optimise(g, outputs)
     return Compiled(g, opt, outputs, flags)
 
 
@@ -55,8 +55,11 @@ def graph_json(opt) -> str:
             continue
         nodes.append({"attrs": dict(n.attrs), "id": n.id, "op": n.op, "preds": list(n.preds),
                       "shape": list(n.shape)})
-    return canon({"dead": sorted(opt.dead), "folded": sorted(opt.folded), "nodes": nodes,
-                  "rep": [[k, opt.rep[k]] for k in sorted(opt.rep)]})
+    d = {"dead": sorted(opt.dead), "folded": sorted(opt.folded), "nodes": nodes,
+         "rep": [[k, opt.rep[k]] for k in sorted(opt.rep)]}
+    if opt.rewrites is not None:
+        d["rewrites"] = {k: sorted(v) for k, v in opt.rewrites.items()}
+    return canon(d)
 
 
 def plan_json(c: Compiled) -> str:

@@ -27,7 +27,8 @@ class CGError(Exception):
 UNARY = ("NEG", "ABS", "SQRT", "EXP", "LOG", "SIN", "COS", "TANH", "RELU")
 BINARY = ("ADD", "SUB", "MUL", "DIV", "POW", "MAX2", "MIN2", "RELU_GRAD")
 TERNARY = ("FMA",)
-EW = frozenset(UNARY + BINARY + TERNARY)
+QUATERNARY = ("FUSED_ADAGRAD",)   # produced by the f1 rewrite (oracle/rewrite.py)
+EW = frozenset(UNARY + BINARY + TERNARY + QUATERNARY)
 RED = frozenset(("SUM", "MAX"))
 COMMUTATIVE = frozenset(("ADD", "MUL", "MAX2", "MIN2"))
 LEAF = frozenset(("VAR", "CONST"))
@@ -41,6 +42,7 @@ for _o in UNARY:
 for _o in BINARY:
     ARITY[_o] = 2
 ARITY["FMA"] = 3
+ARITY["FUSED_ADAGRAD"] = 4
 OPS = tuple(ARITY)
 
 # integer attributes each op carries (canonical keys; the structural JSON dump lists exactly these)
@@ -307,6 +309,9 @@ def eval_op(op: str, ins, attrs, out_shape, dtype=np.float32):
         r = np.where(x[0] > 0, x[1], 0.0)
     elif op == "FMA":
         r = x[0] * x[1] + x[2]
+    elif op == "FUSED_ADAGRAD":  # lr * g / (sqrt(s) + eps)   (g, s, lr, eps), SPEC S:205-212 reading
+        with np.errstate(divide="ignore", invalid="ignore"):
+            r = x[2] * x[0] / (np.sqrt(x[1]) + x[3])
     elif op == "NEG":
         r = -x[0]
     elif op == "ABS":

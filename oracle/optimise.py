@@ -27,13 +27,15 @@ def _attrs_key(attrs):
 
 
 class OptResult:
-    def __init__(self, g, outputs, rep, dead, folded, cse, cf, dce):
+    def __init__(self, g, outputs, rep, dead, folded, cse, cf, dce, rw_counts=None, rw_lists=None):
         self.g = g                # optimised graph (dead nodes kept in the table, marked in ``dead``)
         self.outputs = outputs    # outputs redirected through rep
         self.rep = rep            # CSE representative map old -> new
         self.dead = dead          # ids removed by CSE or DCE
         self.folded = folded      # ids turned into Const by CF
         self.report = {"cse_merged": cse, "cf_folded": cf, "dce_removed": dce}
+        self.report.update(rw_counts or {"rw_identity": 0, "rw_zeroed": 0, "rw_fma": 0, "rw_adagrad": 0})
+        self.rewrites = rw_lists  # None unless the f1 rewrites were requested
 
     def live(self):
         return [n.id for n in self.g.nodes if n.id not in self.dead]
@@ -106,16 +108,31 @@ def dce(g: Graph, dead: set, roots) -> int:
     return removed
 
 
-def optimise(g: Graph, outputs, compute_values=True) -> OptResult:
+def optimise(g: Graph, outputs, compute_values=True, rewrites=0) -> OptResult:
+    """[rewrites (f1, oracle/rewrite.py) ->] CSE -> CF -> DCE.  ``rep`` maps every
+    removed id (identity rewrite or CSE merge) to its final representative."""
     g = g.clone()
     dead = set()
-    rep = cse(g, dead)
-    outs = [rep.get(o, o) for o in outputs]
-    g.updates = [(rep.get(u, u), v) for u, v in g.updates]
+    rw_rep, rw_counts, rw_lists = {}, None, None
+    if rewrites:
+        from .rewrite import rewrite
+        rw_rep, rw_counts, rw_lists = rewrite(g, outputs, rewrites, dead)
+
+    def rw(v):
+        while v in rw_rep:
+            v = rw_rep[v]
+        return v
+    outputs = [rw(o) for o in outputs]
+    g.updates = [(rw(u), v) for u, v in g.updates]
+    crep = cse(g, dead)
+    rep = {v: crep.get(rw(v), rw(v)) for v in rw_rep}
+    rep.update(crep)
+    outs = [crep.get(o, o) for o in outputs]
+    g.updates = [(crep.get(u, u), v) for u, v in g.updates]
     roots = outs + [u for u, _ in g.updates]
     folded = constant_fold(g, dead, roots, compute_values)
     removed = dce(g, dead, roots)
-    return OptResult(g, outs, rep, dead, folded, len(rep), len(folded), removed)
+    return OptResult(g, outs, rep, dead, folded, len(crep), len(folded), removed, rw_counts, rw_lists)
 
 
 def no_optimise(g: Graph, outputs) -> OptResult:

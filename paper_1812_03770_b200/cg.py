@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libcg.so")
 OPS = ["VAR", "CONST", "ADD", "SUB", "MUL", "DIV", "POW", "MAX2", "MIN2", "RELU_GRAD", "FMA",
        "NEG", "ABS", "SQRT", "EXP", "LOG", "SIN", "COS", "TANH", "RELU", "SUM", "MAX", "DOT",
        "CONV2D", "CONV2D_BWD_INPUT", "CONV2D_BWD_KERNEL", "MAXPOOL2D", "MAXPOOL2D_BWD", "AVGPOOL2D",
-       "CONCAT", "RESHAPE", "ALLREDUCE_SUM"]
+       "CONCAT", "RESHAPE", "ALLREDUCE_SUM", "FUSED_ADAGRAD"]
 OP_CODE = {n: i for i, n in enumerate(OPS)}
 
 STATUS = {0: "CG_OK", -1: "CG_E_ARITY", -2: "CG_E_BAD_NODE", -3: "CG_E_SHAPE", -4: "CG_E_NOT_VAR",
@@ -32,13 +32,17 @@ PLAN_NO_FUSION = 2
 EVAL_NO_UPDATE = 1
 EVAL_FULL = 2
 EVAL_SYNC = 4
+RW_IDENTITY = 1
+RW_FMA = 2
+RW_ADAGRAD = 4
+RW_ALL = 7
 DUMP_GRAPH = 0
 DUMP_PLAN = 1
 
 # names exported by include/cg.h (tests check the library exports every one)
 ABI_SYMBOLS = ["cg_create", "cg_add_node", "cg_add_update", "cg_optimise", "cg_plan_memory", "cg_assign",
                "cg_eval", "cg_read", "cg_destroy", "cg_last_error", "cg_nccl_unique_id", "cg_dump_json",
-               "cg_eval_count", "cg_node_shape", "cg_launch_count"]
+               "cg_eval_count", "cg_node_shape", "cg_launch_count", "cg_set_rewrites"]
 
 
 class cg_attr(ctypes.Structure):
@@ -54,7 +58,9 @@ class cg_dist(ctypes.Structure):
 
 
 class cg_report(ctypes.Structure):
-    _fields_ = [("cse_merged", ctypes.c_int32), ("cf_folded", ctypes.c_int32), ("dce_removed", ctypes.c_int32)]
+    _fields_ = [("cse_merged", ctypes.c_int32), ("cf_folded", ctypes.c_int32), ("dce_removed", ctypes.c_int32),
+                ("rw_identity", ctypes.c_int32), ("rw_zeroed", ctypes.c_int32), ("rw_fma", ctypes.c_int32),
+                ("rw_adagrad", ctypes.c_int32)]
 
 
 class cg_plan_info(ctypes.Structure):
@@ -81,6 +87,7 @@ def lib():
             "cg_add_node": (I32, [P, ctypes.c_int, P, I32, P]),
             "cg_add_update": (ctypes.c_int, [P, I32, I32]),
             "cg_optimise": (ctypes.c_int, [P, P, I32, P]),
+            "cg_set_rewrites": (ctypes.c_int, [P, U32]),
             "cg_plan_memory": (ctypes.c_int, [P, P, I32, U32, P]),
             "cg_assign": (ctypes.c_int, [P, I32, P, SZ, ctypes.c_int]),
             "cg_eval": (ctypes.c_int, [P, P, I32, P, U32]),
@@ -189,7 +196,11 @@ class Graph:
     def optimise(self, outputs) -> dict:
         r = cg_report()
         self._check(lib().cg_optimise(self.h, _ids(outputs), len(outputs), ctypes.byref(r)))
-        return {"cse_merged": r.cse_merged, "cf_folded": r.cf_folded, "dce_removed": r.dce_removed}
+        return {f: getattr(r, f) for f, _ in cg_report._fields_}
+
+    def set_rewrites(self, flags: int = 7):
+        """cg_set_rewrites: the paper's pattern rewrites for the next optimise (RW_* flags)."""
+        self._check(lib().cg_set_rewrites(self.h, int(flags)))
 
     def plan_memory(self, outputs, flags: int = 0) -> dict:
         info = cg_plan_info()

@@ -65,6 +65,8 @@ std::string expr(int op, const std::vector<std::string>& a) {
     case CG_COS: return "cosf(" + a[0] + ")";
     case CG_TANH: return "tanhf(" + a[0] + ")";
     case CG_RELU: return "(" + a[0] + " > 0.f ? " + a[0] + " : 0.f)";
+    case CG_FUSED_ADAGRAD:  // lr*g / (sqrt(s) + eps) in f64, one rounding (the oracle's definition)
+      return "((float)((double)" + a[2] + " * (double)" + a[0] + " / (sqrt((double)" + a[1] + ") + (double)" + a[3] + ")))";
   }
   return "0.f";
 }

@@ -647,6 +647,14 @@ int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint3
 int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float** out_dev_ptrs, uint32_t flags);
 int cg_read(cg_graph* g, cg_node node, void* host_dst, size_t nbytes);
 
+int cg_set_rewrites(cg_graph* g, uint32_t flags) {
+  if (!g) return CG_E_ARG;
+  if (g->state != 0) return g->fail(CG_E_STATE, "cg_set_rewrites after cg_optimise/cg_plan_memory");
+  if (flags & ~(uint32_t)CG_RW_ALL) return g->fail(CG_E_ARG, "unknown rewrite flag");
+  g->hg.rw_flags = flags;
+  return 0;
+}
+
 int cg_optimise(cg_graph* g, const cg_node* outputs, int32_t n_outputs, cg_report* report) {
   if (!g) return CG_E_ARG;
   if (g->state != 0) return g->fail(CG_E_STATE, "cg_optimise called twice or after planning");

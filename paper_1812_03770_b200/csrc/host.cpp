@@ -27,6 +27,7 @@ static const OpInfo kOps[CG_NUM_OPS] = {
     {"MAXPOOL2D", 1, false, false, false},    {"MAXPOOL2D_BWD", 2, false, false, false},
     {"AVGPOOL2D", 1, false, false, false},    {"CONCAT", -1, false, false, false},
     {"RESHAPE", 1, false, false, false},      {"ALLREDUCE_SUM", 1, false, false, false},
+    {"FUSED_ADAGRAD", 4, true, false, false},
 };
 
 const OpInfo& op_info(int op) { return kOps[op]; }
@@ -276,17 +277,160 @@ static void reach_back(const std::vector<Node>& nodes, const std::vector<int>& r
   }
 }
 
-int HostGraph::optimise(const std::vector<int>& outs_in, cg_report* report, std::vector<int>* frontier, Error* err) {
+static void json_ints(std::ostringstream& o, const std::vector<int>& v);
+
+// ---------------------------------------------------------------- pattern rewrites (f1)
+// [Optimiser, P:273-279]; readings in DESIGN.md "f1 rewrites": ascending-id sweeps
+// of identities, AdaGrad, FMA repeated to a fixpoint; keep nodes never removed or
+// absorbed; "single consumer" = one consuming edge among live nodes.
+static bool const_all(const Node& nd, float x) {
+  if (nd.op != CG_CONST || nd.host.empty()) return false;
+  for (float v : nd.host)
+    if (!(v == x)) return false;
+  return true;
+}
+static bool scalar_const(const Node& nd) {
+  if (nd.op != CG_CONST) return false;
+  for (auto d : nd.shape)
+    if (d != 1) return false;
+  return true;
+}
+
+void HostGraph::apply_rewrites(const std::vector<int>& outs, std::map<int, int>* rwrep) {
+  const int n = (int)nodes.size();
+  std::vector<char> keep(n, 0);
+  for (int o : outs) keep[o] = 1;
+  for (auto& e : updates) keep[e.first] = 1;
+  auto res = [&](int v) {
+    for (auto it = rwrep->find(v); it != rwrep->end(); it = rwrep->find(v)) v = it->second;
+    return v;
+  };
+  auto redirect = [&]() {
+    for (int v = 0; v < n; ++v)
+      if (!dead[v])
+        for (int& p : nodes[v].preds) p = res(p);
+  };
+  auto uses = [&]() {
+    std::vector<int> u(n, 0);
+    for (int v = 0; v < n; ++v)
+      if (!dead[v])
+        for (int p : nodes[v].preds) u[p]++;
+    return u;
+  };
+  for (;;) {
+    bool changed = false;
+    if (rw_flags & CG_RW_IDENTITY) {
+      redirect();
+      for (int v = 0; v < n; ++v) {
+        Node& nd = nodes[v];
+        if (dead[v] || keep[v]) continue;
+        if (nd.op != CG_ADD && nd.op != CG_SUB && nd.op != CG_MUL && nd.op != CG_DIV) continue;
+        for (int& p : nd.preds) p = res(p);
+        const int a = nd.preds[0], b = nd.preds[1];
+        const bool sa = nodes[a].shape == nd.shape, sb = nodes[b].shape == nd.shape;
+        int to = -1;
+        if (nd.op == CG_ADD) {
+          if (const_all(nodes[b], 0.f) && sa) to = a;
+          else if (const_all(nodes[a], 0.f) && sb) to = b;
+        } else if (nd.op == CG_SUB) {
+          if (const_all(nodes[b], 0.f) && sa) to = a;
+        } else if (nd.op == CG_MUL) {
+          if (const_all(nodes[b], 1.f) && sa) to = a;
+          else if (const_all(nodes[a], 1.f) && sb) to = b;
+          else if (const_all(nodes[a], 0.f) || const_all(nodes[b], 0.f)) {
+            nd.op = CG_CONST;
+            nd.preds.clear();
+            nd.attr = Attr();
+            nd.host.assign((size_t)numel(nd.shape), 0.f);
+            rw_zeroed.push_back(v);
+            changed = true;
+            continue;
+          }
+        } else if (nd.op == CG_DIV) {
+          if (const_all(nodes[b], 1.f) && sa) to = a;
+        }
+        if (to >= 0) {
+          (*rwrep)[v] = to;
+          dead[v] = 1;
+          rw_identity.push_back(v);
+          changed = true;
+        }
+      }
+    }
+    if (rw_flags & CG_RW_ADAGRAD) {
+      redirect();
+      std::vector<int> cnt = uses();
+      auto interior = [&](int v) { return !dead[v] && !keep[v] && cnt[v] == 1; };
+      for (int v = 0; v < n; ++v) {
+        Node& nd = nodes[v];
+        if (dead[v] || nd.op != CG_DIV) continue;
+        const int num = nd.preds[0], den = nd.preds[1];
+        const Node &N = nodes[num], &D = nodes[den];
+        if (N.op != CG_MUL || D.op != CG_ADD || !interior(num) || !interior(den)) continue;
+        int lr, gg;
+        if (scalar_const(nodes[N.preds[0]])) { lr = N.preds[0]; gg = N.preds[1]; }
+        else if (scalar_const(nodes[N.preds[1]])) { lr = N.preds[1]; gg = N.preds[0]; }
+        else continue;
+        int q, eps;
+        if (nodes[D.preds[0]].op == CG_SQRT && scalar_const(nodes[D.preds[1]])) { q = D.preds[0]; eps = D.preds[1]; }
+        else if (nodes[D.preds[1]].op == CG_SQRT && scalar_const(nodes[D.preds[0]])) { q = D.preds[1]; eps = D.preds[0]; }
+        else continue;
+        if (!interior(q)) continue;
+        const int sv = nodes[q].preds[0];
+        nd.op = CG_FUSED_ADAGRAD;
+        nd.preds = {gg, sv, lr, eps};
+        dead[num] = dead[den] = dead[q] = 1;
+        rw_adagrad.push_back(v);
+        changed = true;
+      }
+    }
+    if (rw_flags & CG_RW_FMA) {
+      redirect();
+      std::vector<int> cnt = uses();
+      for (int v = 0; v < n; ++v) {
+        Node& nd = nodes[v];
+        if (dead[v] || nd.op != CG_ADD) continue;
+        for (int side = 0; side < 2; ++side) {
+          const int m = nd.preds[side], c = nd.preds[1 - side];
+          if (nodes[m].op == CG_MUL && !dead[m] && !keep[m] && cnt[m] == 1) {
+            const int a = nodes[m].preds[0], b = nodes[m].preds[1];
+            nd.op = CG_FMA;
+            nd.preds = {a, b, c};
+            dead[m] = 1;
+            rw_fma.push_back(v);
+            changed = true;
+            break;
+          }
+        }
+      }
+    }
+    if (!changed) break;
+  }
+  redirect();
+}
+
+int HostGraph::optimise(const std::vector<int>& outs_raw, cg_report* report, std::vector<int>* frontier, Error* err) {
   int n = (int)nodes.size();
-  for (int o : outs_in)
+  for (int o : outs_raw)
     if (o < 0 || o >= n) return err_set(err, CG_E_BAD_NODE, "unknown output " + std::to_string(o)), CG_E_BAD_NODE;
   dead.assign(n, 0);
   rep.clear();
   folded.clear();
+  rw_identity.clear(); rw_zeroed.clear(); rw_fma.clear(); rw_adagrad.clear();
+  std::map<int, int> rwrep;
+  if (rw_flags) apply_rewrites(outs_raw, &rwrep);
+  auto rw = [&](int v) {
+    for (auto it = rwrep.find(v); it != rwrep.end(); it = rwrep.find(v)) v = it->second;
+    return v;
+  };
+  std::vector<int> outs_in;
+  for (int o : outs_raw) outs_in.push_back(rw(o));
+  for (auto& e : updates) e.first = rw(e.first);
   // CSE
   std::map<std::string, int> seen;
   for (int v = 0; v < n; ++v) {
     Node& nd = nodes[v];
+    if (dead[v]) continue;  // removed by a rewrite
     for (int& p : nd.preds) p = resolve(p);
     if (nd.op == CG_VAR) continue;
     auto key = cse_key(nd);
@@ -301,6 +445,11 @@ int HostGraph::optimise(const std::vector<int>& outs_in, cg_report* report, std:
   std::vector<int> outs;
   for (int o : outs_in) outs.push_back(resolve(o));
   for (auto& e : updates) e.first = resolve(e.first);
+  // every id removed by an identity rewrite resolves to its final representative
+  for (auto& kv : rwrep) {
+    const int t = rw(kv.first);
+    rep[kv.first] = resolve(t);
+  }
   std::vector<int> rts = outs;
   for (auto& e : updates) rts.push_back(e.first);
   // CF: C = Consts + non-(Var, ALLREDUCE) nodes with preds, all in C (ascending pass)
@@ -337,7 +486,11 @@ int HostGraph::optimise(const std::vector<int>& outs_in, cg_report* report, std:
     for (int v = 0; v < n; ++v)
       if (!dead[v] && nodes[v].op != CG_VAR && !live[v]) { dead[v] = 1; ++removed; }
     if (report) {
-      report->cse_merged = (int)rep.size();
+      report->cse_merged = (int)(rep.size() - rwrep.size());
+      report->rw_identity = (int)rw_identity.size();
+      report->rw_zeroed = (int)rw_zeroed.size();
+      report->rw_fma = (int)rw_fma.size();
+      report->rw_adagrad = (int)rw_adagrad.size();
       report->cf_folded = (int)folded.size();
       report->dce_removed = removed;
     }
@@ -648,7 +801,20 @@ std::string HostGraph::graph_json() const {
     o << (first ? "" : ",") << "[" << kv.first << "," << kv.second << "]";
     first = false;
   }
-  o << "]}";
+  o << "]";
+  if (rw_flags) {
+    auto srt = [](std::vector<int> v) { std::sort(v.begin(), v.end()); return v; };
+    o << ",\"rewrites\":{\"adagrad\":";
+    json_ints(o, srt(rw_adagrad));
+    o << ",\"fma\":";
+    json_ints(o, srt(rw_fma));
+    o << ",\"identity\":";
+    json_ints(o, srt(rw_identity));
+    o << ",\"zeroed\":";
+    json_ints(o, srt(rw_zeroed));
+    o << "}";
+  }
+  o << "}";
   return o.str();
 }
 

@@ -79,6 +79,10 @@ class HostGraph {
   // ---- build ----
   int add_node(int op, const int* inputs, int n, const cg_attr* a, Error* err);
   int add_update(int u, int var, Error* err);
+  // ---- f1 pattern rewrites (cg_set_rewrites), applied at the start of optimise
+  uint32_t rw_flags = 0;
+  std::vector<int> rw_identity, rw_zeroed, rw_fma, rw_adagrad;
+  void apply_rewrites(const std::vector<int>& outs, std::map<int, int>* rwrep);
   // ---- optimise (CSE -> CF -> DCE); returns the CF frontier whose values the device must produce
   int optimise(const std::vector<int>& outputs, cg_report* rep, std::vector<int>* frontier, Error* err);
   // rewrite the CF frontier into Consts (same id).  values[i] (may be empty in

@@ -16,8 +16,10 @@ def leaf_data(rec, seed=1812):
     return None
 
 
-def gpu_graph(spec, flags=0, optimise=True, device=0):
+def gpu_graph(spec, flags=0, optimise=True, device=0, rewrites=0):
     g, outs = cg.build_from_spec(spec, device=device, data_fn=leaf_data)
+    if rewrites:
+        g.set_rewrites(rewrites)
     rep = g.optimise(outs) if optimise else None
     info = g.plan_memory(outs, flags)
     return g, outs, rep, info

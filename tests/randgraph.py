@@ -16,7 +16,7 @@ BINARY = ["ADD", "SUB", "MUL", "DIV", "MAX2", "MIN2", "RELU_GRAD"]
 LEAF_SHAPES = [[4, 8], [1, 8], [4, 1], [8], []]
 
 
-def random_spec(seed: int, n_ops=None, allow_updates=True, simple_values=False):
+def random_spec(seed: int, n_ops=None, allow_updates=True, simple_values=False, rewrite_bait=False):
     rng = random.Random(seed)
     n_ops = n_ops if n_ops is not None else rng.randint(3, 40)
     nodes = []
@@ -34,6 +34,17 @@ def random_spec(seed: int, n_ops=None, allow_updates=True, simple_values=False):
         nodes.append({"id": len(nodes), "op": "CONST", "preds": [], "attrs": {}, "name": f"c{k}",
                       "shape": shp, "data": {"kind": "uniform", "tag": f"r{seed}c{k}", "lo": 0.5, "hi": 1.5}})
         g.add_leaf("CONST", shp)
+    if rewrite_bait:  # exact 0 / 1 Consts and scalar Consts: identity / AdaGrad pattern material
+        for k, (val, shp) in enumerate([(0.0, []), (1.0, []), (0.0, [4, 8]), (1.0, [1, 8])]):
+            nodes.append({"id": len(nodes), "op": "CONST", "preds": [], "attrs": {}, "name": f"b{k}",
+                          "shape": shp, "data": {"kind": "full", "value": val}})
+            g.add_leaf("CONST", shp)
+        nodes.append({"id": len(nodes), "op": "CONST", "preds": [], "attrs": {}, "name": "lr",
+                      "shape": [], "data": {"kind": "literal", "values": [0.1]}})
+        g.add_leaf("CONST", [])
+        nodes.append({"id": len(nodes), "op": "CONST", "preds": [], "attrs": {}, "name": "eps",
+                      "shape": [], "data": {"kind": "literal", "values": [1e-3]}})
+        g.add_leaf("CONST", [])
     tries = 0
     made = 0
     while made < n_ops and tries < 50 * n_ops:
@@ -62,6 +73,24 @@ def random_spec(seed: int, n_ops=None, allow_updates=True, simple_values=False):
             a1 = rng.randint(a0 + 1, rank)
             op, preds, attrs = rng.choice(["SUM", "MAX"]), [x], {"a0": a0, "a1": a1}
         elif r < 0.94:
+            if rewrite_bait and rng.random() < 0.5:  # an AdaGrad adjusted-gradient pattern
+                gv, sv = pick(), pick()
+                lr = next(n["id"] for n in nodes if n.get("name") == "lr")
+                eps = next(n["id"] for n in nodes if n.get("name") == "eps")
+                try:
+                    ids = []
+                    for op_, pr in (("MUL", [lr, gv]), ("SQRT", [sv]), ("ADD", None), ("DIV", None)):
+                        if op_ == "ADD":
+                            pr = [ids[1], eps] if rng.random() < 0.5 else [eps, ids[1]]
+                        if op_ == "DIV":
+                            pr = [ids[0], ids[2]]
+                        g.add_node(op_, pr, {})
+                        nodes.append({"id": len(nodes), "op": op_, "preds": pr, "attrs": {}})
+                        ids.append(len(nodes) - 1)
+                    made += 4
+                except CGError:
+                    pass
+                continue
             op, preds, attrs = "DOT", [pick(), pick()], {"ta": rng.randint(0, 1), "tb": rng.randint(0, 1)}
         else:
             x = pick()

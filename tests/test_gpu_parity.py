@@ -88,7 +88,7 @@ def test_counter_three_rounds():
 def test_c2_small(rows, cols):
     spec = configs.c2(rows, cols)
     g, outs, rep, info = gpu_graph(spec, 0)
-    assert rep == {"cse_merged": 1, "cf_folded": 2, "dce_removed": 2}
+    assert {k: rep[k] for k in ("cse_merged", "cf_folded", "dce_removed")} == {"cse_merged": 1, "cf_folded": 2, "dce_removed": 2}
     assert info["n_groups"] == 1 and info["n_blocks"] == 1
     g.eval(outs)
     ref, _, _ = oracle_outputs(spec)
@@ -476,7 +476,7 @@ def _train_parity(spec, iters, tol):
     print(spec["name"], {k: f"{e:.2e}" for k, e in errs.items()})
 
 
-def _teacher_forced(spec, iters, tol):
+def _teacher_forced(spec, iters, tol, rewrites=0):
     """Each iteration starts from the ORACLE's parameter state (cg_assign of every
     update target), so the comparison measures one evaluation + update_iopair per
     step instead of 10 steps of chaotic amplification.  The pre-activations
@@ -488,7 +488,7 @@ def _teacher_forced(spec, iters, tol):
     spec = dict(spec)
     zs = [n["preds"][0] for n in spec["nodes"] if n["op"] == "RELU"]
     spec["outputs"] = list(spec["outputs"]) + zs
-    g, outs, _, _ = gpu_graph(spec, 0)
+    g, outs, _, _ = gpu_graph(spec, 0, rewrites=rewrites)
     og, oo = from_spec(spec)
     per = {n["name"]: n["data"] for n in spec["nodes"] if n.get("name") in spec["meta"]["per_iteration"]}
     name_to_id = {n["name"]: n["id"] for n in spec["nodes"] if n["op"] == "VAR"}
@@ -575,3 +575,49 @@ def test_in_place_elementwise_group(c):
         g.eval([out], cg.EVAL_FULL)
         ref = np.maximum(np.concatenate([x1, x2], axis=1) * np.float32(2) - np.float32(1), 0)
         assert np.array_equal(g.read(out), ref)
+
+
+# ---------------------------------------------------------------- f1 rewrites on the GPU
+def test_c2_with_rewrites():
+    """C2 with the paper's rewrites (3 FMAs): still the eager result within 1e-5."""
+    spec = configs.c2(300, 1024)
+    g, outs, rep, _ = gpu_graph(spec, 0, rewrites=cg.RW_ALL)
+    assert rep["rw_fma"] == 3
+    g.eval(outs)
+    ref, _, _ = oracle_outputs(spec)
+    assert normwise(g.read(outs[0]), ref[outs[0]]) <= 1e-5
+
+
+def test_fused_adagrad_closed_form():
+    """S:360: FusedAdagrad(lr=0.1, eps=1e-8)(g=1, s=4) = 0.1/(2+1e-8), computed in f64
+    with one rounding on both sides: bit-exact."""
+    g = cg.Graph(0)
+    gv, sv = g.var([3]), g.var([3])
+    lr, eps = g.const(np.float32(0.1)), g.const(np.float32(1e-8))
+    d = g.add_node("DIV", [g.add_node("MUL", [lr, gv]), g.add_node("ADD", [g.add_node("SQRT", [sv]), eps])])
+    g.set_rewrites(cg.RW_ADAGRAD)
+    rep = g.optimise([d])
+    assert rep["rw_adagrad"] == 1
+    g.plan_memory([d])
+    g.assign(gv, np.ones(3, np.float32))
+    g.assign(sv, np.full(3, 4.0, np.float32))
+    g.eval([d])
+    want = np.float32(np.float64(np.float32(0.1)) * 1.0 / (2.0 + np.float64(np.float32(1e-8))))
+    assert np.all(g.read(d) == want) and abs(float(want) - 0.05) < 1e-6
+
+
+@pytest.mark.parametrize("flags", [0, cg.PLAN_NO_FUSION])
+def test_random_graphs_with_rewrites(flags):
+    for seed in range(40):
+        spec = random_spec(seed, allow_updates=False, simple_values=True, rewrite_bait=True)
+        g, outs, _, _ = gpu_graph(spec, flags, rewrites=cg.RW_ALL)
+        g.eval(outs)
+        ref, _, oo = oracle_outputs(spec)
+        for o in oo:
+            assert normwise(g.read(o), ref[o]) <= 2e-5, (seed, o)
+
+
+def test_c3_adagrad_training_with_rewrites():
+    """C3 with AdaGrad and every rewrite on (6 Fused_Adagrad + FMA nodes), teacher-forced."""
+    _teacher_forced(configs.c3(batch=256, widths=(784, 128, 64, 10), optimizer="adagrad"), 10, 1e-4,
+                    rewrites=cg.RW_ALL)

@@ -30,17 +30,19 @@ def _const_data(rec):
     return materialise(rec["data"], rec["shape"]) if rec["op"] == "CONST" else None
 
 
-def host_graph(spec, flags, optimise=True):
+def host_graph(spec, flags, optimise=True, rewrites=0):
     g, outs = cg.build_from_spec(spec, device=-1, data_fn=_const_data)
+    if rewrites:
+        g.set_rewrites(rewrites)
     rep = g.optimise(outs) if optimise else None
     info = g.plan_memory(outs, flags)
     return g, outs, rep, info
 
 
-def check_parity(spec, flags):
-    g, outs, rep, info = host_graph(spec, flags)
+def check_parity(spec, flags, rewrites=0):
+    g, outs, rep, info = host_graph(spec, flags, rewrites=rewrites)
     og, oo = from_spec(spec)
-    c = compile_graph(og, oo, flags, compute_values=False)
+    c = compile_graph(og, oo, flags, compute_values=False, rewrites=rewrites)
     assert rep == c.opt.report
     assert g.dump_json(cg.DUMP_GRAPH) == graph_json(c.opt)
     assert g.dump_json(cg.DUMP_PLAN) == plan_json(c)
@@ -79,6 +81,22 @@ def test_c5_parity_and_memory():
     c = compile_graph(og, oo, 0, compute_values=False)
     assert c.opt.report["cf_folded"] == 94 and c.opt.report["dce_removed"] >= 94
     assert c.plan.pool_bytes < c.unshared_bytes / 10
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C3adagrad"])
+def test_rewrite_parity_configs(name):
+    """f1 rewrites: the C++ host compiler and the oracle rewrite the
+    same nodes, byte for byte (graph and plan dumps, rewrite counts)."""
+    spec = configs.c3(optimizer="adagrad") if name == "C3adagrad" else configs.CONFIGS[name]()
+    g = check_parity(spec, 0, rewrites=cg.RW_ALL)
+    if name == "C3adagrad":
+        assert '"adagrad":[' in g.dump_json(cg.DUMP_GRAPH)
+
+
+@pytest.mark.parametrize("flags", [0, cg.PLAN_NO_FUSION])
+def test_rewrite_parity_random(flags):
+    for seed in range(200):
+        check_parity(random_spec(seed, rewrite_bait=True), flags, rewrites=cg.RW_ALL)
 
 
 @pytest.mark.parametrize("flags", MODES)

@@ -126,7 +126,7 @@ def test_constant_folding_examples():
     m = g.add_node("MUL", [d, x])
     c = compile_graph(g, [m])
     assert c.opt.folded == [d] and c.g.nodes[d].op == "CONST" and float(c.g.nodes[d].value) == 1.0
-    assert c.opt.report == {"cse_merged": 0, "cf_folded": 1, "dce_removed": 2}
+    assert {k: c.opt.report[k] for k in ("cse_merged", "cf_folded", "dce_removed")} == {"cse_merged": 0, "cf_folded": 1, "dce_removed": 2}
     # all-const graph -> a single Const
     g = Graph()
     a = g.add_leaf("CONST", [2], data={"kind": "literal", "values": [1.0, 2.0]})
@@ -139,7 +139,7 @@ def test_constant_folding_examples():
     # Fig. 1 unchanged
     g, outs = _fig1()
     c = compile_graph(g, outs)
-    assert c.opt.report == {"cse_merged": 0, "cf_folded": 0, "dce_removed": 0}
+    assert {k: c.opt.report[k] for k in ("cse_merged", "cf_folded", "dce_removed")} == {"cse_merged": 0, "cf_folded": 0, "dce_removed": 0}
 
 
 def test_cse_rules():
@@ -171,7 +171,7 @@ def test_c2_structure():
     """CSE merges 15->6, CF folds n1, n2, DCE drops kb, kc; 17 ops, 1 group."""
     g, outs = from_spec(configs.c2(rows=8, cols=16))
     c = compile_graph(g, outs)
-    assert c.opt.report == {"cse_merged": 1, "cf_folded": 2, "dce_removed": 2}
+    assert {k: c.opt.report[k] for k in ("cse_merged", "cf_folded", "dce_removed")} == {"cse_merged": 1, "cf_folded": 2, "dce_removed": 2}
     assert c.opt.rep == {23: 14} and c.opt.folded == [9, 10] and sorted(c.opt.dead) == [6, 7, 23]
     assert float(c.g.nodes[9].value) == 1.0 and c.g.nodes[10].value == np.float32(0.044715)
     assert len(c.groups) == 1 and len(c.groups[0].members) == 17

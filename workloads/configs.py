@@ -60,6 +60,10 @@ class Spec:
         return {"name": self.name, "nodes": self.nodes, "outputs": list(self.outputs),
                 "updates": [list(p) for p in self.updates], "meta": dict(self.meta)}
 
+    def shape_of(self, i):
+        """Shape of a leaf (accumulators copy their parameter's shape)."""
+        return list(self.nodes[i]["shape"])
+
     def leaf_ids(self, op=None):
         return [n["id"] for n in self.nodes if n["op"] in ("VAR", "CONST") and (op is None or n["op"] == op)]
 
@@ -173,6 +177,23 @@ def _softmax_xent(s: Spec, L, Y, batch_global: int):
     return loss, P, dL
 
 
+def _adagrad(s: Spec, params_and_grads, lr: float, allreduce: bool, eps: float = 1e-8):
+    """AdaGrad [adagrad]: s <- s + g*g; W <- W - lr*g / (sqrt(s) + eps), with an
+    accumulator Var per parameter and two update edges per parameter.  The
+    adjusted-gradient subgraph is the pattern the paper fuses into
+    Fused_Adagrad (P:273-277)."""
+    klr = s.scalar("lr", lr)
+    keps = s.scalar("eps", eps)
+    for W, g in params_and_grads:
+        if allreduce:
+            g = s.op("ALLREDUCE_SUM", g)
+        acc = s.var(f"acc_{s.nodes[W]['name']}", s.shape_of(W), ZEROS)
+        acc_new = s.op("ADD", acc, s.op("MUL", g, g))
+        step = s.op("DIV", s.op("MUL", klr, g), s.op("ADD", s.op("SQRT", acc_new), keps))
+        s.update(s.op("SUB", W, step), W)
+        s.update(acc_new, acc)
+
+
 def _sgd(s: Spec, params_and_grads, lr: float, allreduce: bool):
     klr = s.scalar("lr", lr)
     for W, g in params_and_grads:
@@ -189,7 +210,7 @@ def _sgd(s: Spec, params_and_grads, lr: float, allreduce: bool):
 
 
 def c3(batch: int = 4096, widths=(784, 1024, 1024, 10), batch_global: int | None = None,
-       lr: float = 0.05, allreduce: bool = True) -> dict:
+       lr: float = 0.05, allreduce: bool = True, optimizer: str = "sgd") -> dict:
     """Forward DOT->+b->RELU (x2), DOT->+b; softmax-xent; hand-written backward; SGD.
 
     ``batch`` is the local (per-rank) batch; ``batch_global`` scales the loss
@@ -230,7 +251,10 @@ def c3(batch: int = 4096, widths=(784, 1024, 1024, 10), batch_global: int | None
     for li in range(nl):
         pg.append((Ws[li], grads[li][0]))
         pg.append((bs[li], grads[li][1]))
-    _sgd(s, pg, lr, allreduce)
+    if optimizer == "adagrad":
+        _adagrad(s, pg, lr, allreduce)
+    else:
+        _sgd(s, pg, lr, allreduce)
     s.output(loss, L)
     s.meta["per_iteration"] = ["X", "Y"]
     return s.to_dict()
