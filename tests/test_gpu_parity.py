@@ -486,7 +486,10 @@ def _teacher_forced(spec, iters, tol, rewrites=0):
     a value within rounding of the kink (observed: C3 batch 256, iteration 9,
     |Z| = 2.3e-7 of max|Z|) is taken identically on both sides."""
     spec = dict(spec)
+    # pinned: pre-activations (ReLU decisions) and the gradients entering the
+    # optimiser (AdaGrad's lr*g/(sqrt(s)+eps) is a sign-like map of tiny g)
     zs = [n["preds"][0] for n in spec["nodes"] if n["op"] == "RELU"]
+    zs += [n["id"] for n in spec["nodes"] if n["op"] == "ALLREDUCE_SUM"]
     spec["outputs"] = list(spec["outputs"]) + zs
     g, outs, _, _ = gpu_graph(spec, 0, rewrites=rewrites)
     og, oo = from_spec(spec)
