@@ -68,17 +68,27 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Blocking wait on an mbarrier phase.  The suspend-time hint lets the hardware
+// park the warp until the phase flips instead of spinning (spinning waiters of
+// the idle roles were eating the issue slots of the split/gather warps).
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
-  long long spins = 0;
+  uint64_t t0 = 0;
   while (true) {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(1000000u)
         : "memory");
     if (done) return;
-    if (++spins > (1LL << 28)) __trap();  // watchdog: a lost arrival must fail the launch, not hang the GPU
+    // watchdog: a lost arrival must fail the launch (10 s), not hang the GPU
+    if (t0 == 0) t0 = globaltimer();
+    else if (globaltimer() - t0 > 10000000000ull) __trap();
   }
 }
 
