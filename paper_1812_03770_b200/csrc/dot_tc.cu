@@ -359,7 +359,10 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       if (lane == 0) mbar_arrive(tempty(b));
     }
   } else if (GATHER) {
-    // ---------------- warps 10..13: im2col gather of A, one tile row (output pixel) per thread
+    // ---------------- warps 10..13: im2col gather of A, one tile row (output pixel) per thread.
+    // The (kh, kw, ci) position of the k-slab is advanced incrementally (no
+    // per-chunk divisions); with Ci % 32 == 0 a whole slab is one tap: one
+    // contiguous 128-byte run of channels per row.
     const int r = threadIdx.x - 320;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -375,35 +378,49 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         wo = q - ho * cv.Wo;
       }
       const int hb = ho * cv.sh - cv.pt, wb = wo * cv.sw - cv.pl;
+      const float* img = cv.x + (size_t)n * cv.H * cv.W * cv.Ci;
+      // slab start k0 = kb0 * BK  ->  (kh, kw, ci)
+      int k0 = kb0 * BK;
+      int tap = k0 / cv.Ci, ci = k0 - tap * cv.Ci;
+      int kh = tap / cv.KW, kw = tap - kh * cv.KW;
+      const bool row_ok = m < M;
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = it % STAGES;
         const uint32_t ph = (it / STAGES) & 1;
         mbar_wait(empty(s), ph ^ 1);
         const uint32_t row = sbase + s * STAGE_BYTES + r * 128;
-        if ((cv.Ci & 3) == 0) {  // 4 consecutive k = 4 channels of one tap: one 16-byte async copy
+        if ((cv.Ci & 31) == 0) {  // the slab is 32 channels of one tap
+          const int hi = hb + kh, wi = wb + kw;
+          const bool ok = row_ok && k0 < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
+          const float* src = ok ? img + ((size_t)hi * cv.W + wi) * cv.Ci + ci : cv.x;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) cp_async16(row + ((jj ^ (r & 7)) << 4), src + (ok ? 4 * jj : 0), ok ? 16u : 0u);
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
+          ci += BK;
+          if (ci >= cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
+          k0 += BK;
+        } else if ((cv.Ci & 3) == 0) {  // 4 consecutive k = 4 channels of one tap: one 16-byte async copy
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
-            const int k = (kb0 + kb) * BK + 4 * jj;
-            const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
-            const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
             const int hi = hb + kh, wi = wb + kw;
-            const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
-            const float* src = ok ? cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci : cv.x;
+            const bool ok = row_ok && k0 < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
+            const float* src = ok ? img + ((size_t)hi * cv.W + wi) * cv.Ci + ci : cv.x;
             cp_async16(row + ((jj ^ (r & 7)) << 4), src, ok ? 16u : 0u);
+            ci += 4;
+            if (ci >= cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
+            k0 += 4;
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
         } else {  // few input channels (e.g. RGB): element-wise gather, 16-byte shared stores
-#pragma unroll 2
           for (int jj = 0; jj < 8; ++jj) {
             float e[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const int k = (kb0 + kb) * BK + 4 * jj + q;
-              const int tap = k / cv.Ci, ci = k - tap * cv.Ci;
-              const int kh = tap / cv.KW, kw = tap - kh * cv.KW;
               const int hi = hb + kh, wi = wb + kw;
-              const bool ok = m < M && k < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
-              e[q] = ok ? __ldg(cv.x + (((size_t)n * cv.H + hi) * cv.W + wi) * cv.Ci + ci) : 0.f;
+              const bool ok = row_ok && k0 < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
+              e[q] = ok ? __ldg(img + ((size_t)hi * cv.W + wi) * cv.Ci + ci) : 0.f;
+              if (++ci == cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
+              ++k0;
             }
             sts128(row + ((jj ^ (r & 7)) << 4), make_float4(e[0], e[1], e[2], e[3]));
           }
