@@ -42,10 +42,18 @@ namespace cg {
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 32;
-constexpr int STAGES = 3;
+// Decoupled rings: the raw operand tiles (TMA / gather destinations, also the hi
+// operands) live in a deep ring so loads run far ahead of the MMAs; the lo tiles
+// written by the split warps only live from the split to the MMA (short ring).
+constexpr int STAGES = 5;   // raw ring: A raw + B raw
+constexpr int LSTAGES = 2;  // lo ring: A lo + B lo
 constexpr int TILE_BYTES = BM * BK * 4;             // 16 KiB: one operand tile (BN == BM)
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;          // A hi, B hi, A lo, B lo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+constexpr int STAGE_BYTES = 2 * TILE_BYTES;          // raw slot: A, B
+constexpr int LO_BYTES = 2 * TILE_BYTES;             // lo slot: A lo, B lo
+constexpr int LO_BASE = STAGES * STAGE_BYTES;
+constexpr int BAR_BASE = LO_BASE + LSTAGES * LO_BYTES;
+constexpr int SMEM_BYTES = BAR_BASE + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 constexpr int THREADS = 320;         // TMA, MMA, 4 split warps, 4 epilogue warps
 constexpr int THREADS_GATHER = 448;  // + 4 warps gathering the im2col A tile
 
@@ -158,14 +166,15 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
+  uint64_t* bars = (uint64_t*)(smem + BAR_BASE);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int s) { return bar0 + 8u * s; };
-  auto conv = [&](int s) { return bar0 + 8u * (STAGES + s); };
-  auto empty = [&](int s) { return bar0 + 8u * (2 * STAGES + s); };
-  auto tfull = [&](int b) { return bar0 + 8u * (3 * STAGES + b); };
-  auto tempty = [&](int b) { return bar0 + 8u * (3 * STAGES + 2 + b); };
-  uint32_t* tmem_slot = (uint32_t*)(smem + STAGES * STAGE_BYTES + 512);
+  auto empty = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto conv = [&](int l) { return bar0 + 8u * (2 * STAGES + l); };
+  auto lofree = [&](int l) { return bar0 + 8u * (2 * STAGES + LSTAGES + l); };
+  auto tfull = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 * LSTAGES + b); };
+  auto tempty = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 * LSTAGES + 2 + b); };
+  uint32_t* tmem_slot = (uint32_t*)(smem + BAR_BASE + 512);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
@@ -185,8 +194,11 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full(s), GATHER ? 1 + 128 : 1);
-      mbar_init(conv(s), 4);
       mbar_init(empty(s), 1);
+    }
+    for (int l = 0; l < LSTAGES; ++l) {
+      mbar_init(conv(l), 4);
+      mbar_init(lofree(l), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull(b), 1);
@@ -247,12 +259,11 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(b * BN);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(conv(s), ph);
+          const int s = it % STAGES, l = it % LSTAGES;
+          mbar_wait(conv(l), (it / LSTAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = sbase + s * STAGE_BYTES;
-          const uint32_t ahi = st, bhi = st + TILE_BYTES, alo = st + 2 * TILE_BYTES, blo = st + 3 * TILE_BYTES;
+          const uint32_t st = sbase + s * STAGE_BYTES, lo = sbase + LO_BASE + l * LO_BYTES;
+          const uint32_t ahi = st, bhi = st + TILE_BYTES, alo = lo, blo = lo + TILE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
@@ -261,7 +272,8 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
             mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
             mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, 1u);
           }
-          mma_commit(empty(s));  // frees the stage once these MMAs have read it
+          mma_commit(empty(s));   // frees the raw slot once these MMAs have read it
+          mma_commit(lofree(l));  // and the lo slot
         }
         mma_commit(tfull(b));
       }
@@ -274,15 +286,15 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       int z, m0, n0, kb0, nk;
       unit(u, z, m0, n0, kb0, nk);
       for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(full(s), ph);
+        const int s = it % STAGES, l = it % LSTAGES;
+        mbar_wait(full(s), (it / STAGES) & 1);
+        mbar_wait(lofree(l), ((it / LSTAGES) & 1) ^ 1);
         if (dbg && u == 0 && kb == 0 && t < 8) {
           dbg[t] = reinterpret_cast<float*>(smem)[t];                   // A raw
           dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_BYTES)[t];  // B raw
         }
         // 16 float4 per thread: all loads first (ILP), explicit shared-space ops
-        const uint32_t hb = sbase + s * STAGE_BYTES + t * 16, lb = hb + 2 * TILE_BYTES;
+        const uint32_t hb = sbase + s * STAGE_BYTES + t * 16, lb = sbase + LO_BASE + l * LO_BYTES + t * 16;
         constexpr int PER = 2 * TILE_BYTES / 16 / 128;
         float4 v[PER];
 #pragma unroll
@@ -308,7 +320,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(conv(s));
+        if (lane == 0) mbar_arrive(conv(l));
       }
     }
   } else if (warp < 10) {
