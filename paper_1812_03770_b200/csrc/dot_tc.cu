@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -41,19 +42,25 @@ namespace cg {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 32;
-// Decoupled rings: the raw operand tiles (TMA / gather destinations, also the hi
-// operands) live in a deep ring so loads run far ahead of the MMAs; the lo tiles
-// written by the split warps only live from the split to the MMA (short ring).
-constexpr int STAGES = 5;   // raw ring: A raw + B raw
-constexpr int LSTAGES = 2;  // lo ring: A lo + B lo
-constexpr int TILE_BYTES = BM * BK * 4;             // 16 KiB: one operand tile (BN == BM)
-constexpr int STAGE_BYTES = 2 * TILE_BYTES;          // raw slot: A, B
-constexpr int LO_BYTES = 2 * TILE_BYTES;             // lo slot: A lo, B lo
-constexpr int LO_BASE = STAGES * STAGE_BYTES;
-constexpr int BAR_BASE = LO_BASE + LSTAGES * LO_BYTES;
-constexpr int SMEM_BYTES = BAR_BASE + 1024 /*barriers*/ + 1024 /*alignment slack*/;
-static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+constexpr int BM = 128, BK = 32;
+// Tile configurations (N = 128 or 256 columns per unit).  Decoupled rings: the
+// raw operand tiles (TMA / gather destinations, also the hi operands) live in a
+// ring that runs ahead of the MMAs; the lo tiles written by the split warps only
+// live from the split to the MMA.
+template <int BNT>
+struct TC {
+  static constexpr int BN = BNT;
+  static constexpr int TILE_A = BM * BK * 4;      // 16 KiB
+  static constexpr int TILE_B = BNT * BK * 4;     // 16 / 32 KiB
+  static constexpr int STAGES = BNT == 256 ? 2 : 5;   // raw ring
+  static constexpr int LSTAGES = 2;                   // lo ring
+  static constexpr int STAGE_BYTES = TILE_A + TILE_B;
+  static constexpr int LO_BYTES = TILE_A + TILE_B;
+  static constexpr int LO_BASE = STAGES * STAGE_BYTES;
+  static constexpr int BAR_BASE = LO_BASE + LSTAGES * LO_BYTES;
+  static constexpr int SMEM_BYTES = BAR_BASE + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+};
 constexpr int THREADS = 320;         // TMA, MMA, 4 split warps, 4 epilogue warps
 constexpr int THREADS_GATHER = 448;  // + 4 warps gathering the im2col A tile
 
@@ -158,11 +165,15 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 // and tfull/tempty per accumulator (MMA -> epilogue -> MMA); the stage index and
 // phase run on a k-block counter that continues across units, so the producers
 // prefetch the next unit while the current one finishes.
-template <bool GATHER>
+template <bool GATHER, int BNT>
 __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                    int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
                    float* __restrict__ dbg) {
+  using T = TC<BNT>;
+  constexpr int BN = T::BN, STAGES = T::STAGES, LSTAGES = T::LSTAGES;
+  constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, STAGE_BYTES = T::STAGE_BYTES, LO_BYTES = T::LO_BYTES;
+  constexpr int LO_BASE = T::LO_BASE, BAR_BASE = T::BAR_BASE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
@@ -229,7 +240,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(empty(s), ph ^ 1);
           const uint32_t st = sbase + s * STAGE_BYTES;
-          mbar_expect_tx(full(s), GATHER ? TILE_BYTES : 2 * TILE_BYTES);
+          mbar_expect_tx(full(s), GATHER ? TILE_B : TILE_A + TILE_B);
           const int k0 = (kb0 + kb) * BK;
           if (GATHER) {
           } else if (a_mn) {
@@ -238,9 +249,9 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
             tma_load_2d(st, &mapA, k0, m0, full(s));
           }
           if (b_mn) {
-            for (int j = 0; j < BN / 32; ++j) tma_load_2d(st + TILE_BYTES + j * 4096, &mapB, n0 + 32 * j, k0, full(s));
+            for (int j = 0; j < BN / 32; ++j) tma_load_2d(st + TILE_A + j * 4096, &mapB, n0 + 32 * j, k0, full(s));
           } else {
-            tma_load_2d(st + TILE_BYTES, &mapB, k0, n0, full(s));
+            tma_load_2d(st + TILE_A, &mapB, k0, n0, full(s));
           }
         }
       }
@@ -263,14 +274,16 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           mbar_wait(conv(l), (it / LSTAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t st = sbase + s * STAGE_BYTES, lo = sbase + LO_BASE + l * LO_BYTES;
-          const uint32_t ahi = st, bhi = st + TILE_BYTES, alo = lo, blo = lo + TILE_BYTES;
+          const uint32_t ahi = st, bhi = st + TILE_A, alo = lo, blo = lo + TILE_A;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
             // small terms first, then the leading hi.hi product
-            mma_tf32(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
-            mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
-            mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, 1u);
+            if (raw_hi != 2) {
+              mma_tf32(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
+              mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
+            }
+            mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, raw_hi != 2 ? 1u : acc0);
           }
           mma_commit(empty(s));   // frees the raw slot once these MMAs have read it
           mma_commit(lofree(l));  // and the lo slot
@@ -291,11 +304,17 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         mbar_wait(lofree(l), ((it / LSTAGES) & 1) ^ 1);
         if (dbg && u == 0 && kb == 0 && t < 8) {
           dbg[t] = reinterpret_cast<float*>(smem)[t];                   // A raw
-          dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_BYTES)[t];  // B raw
+          dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_A)[t];  // B raw
+        }
+        if (raw_hi == 2) {  // probe only: 1xTF32 (no split) to measure what the split costs
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(conv(l));
+          continue;
         }
         // 16 float4 per thread: all loads first (ILP), explicit shared-space ops
         const uint32_t hb = sbase + s * STAGE_BYTES + t * 16, lb = sbase + LO_BASE + l * LO_BYTES + t * 16;
-        constexpr int PER = 2 * TILE_BYTES / 16 / 128;
+        constexpr int PER = STAGE_BYTES / 16 / 128;
         float4 v[PER];
 #pragma unroll
         for (int q = 0; q < PER; ++q) v[q] = lds128(hb + q * 2048);
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           // threads (generic proxy); rewriting it here, followed by this thread's
           // proxy fence, is what makes it visible to the tensor core.  TMA tiles are
           // async-proxy writes already, so with raw_hi they are read as they are.
-          if (!raw_hi || (GATHER && q < PER / 2)) sts128(hb + q * 2048, h);
+          if (!raw_hi || (GATHER && q < TILE_A / 2048)) sts128(hb + q * 2048, h);
           sts128(lb + q * 2048, l);
         }
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
@@ -492,8 +511,16 @@ bool dot_tc_supported(int M, int N, int K, int ta, int tb) {
   return M >= 64 && N >= 32 && K >= 8;
 }
 
+// N tile: 256 columns when that wastes no more padding than 128 (halves the
+// operand traffic per FLOP: A is re-read per N tile), else 128.
+int pick_bn(int N) {
+  const int w128 = (N + 127) / 128 * 128 - N, w256 = (N + 255) / 256 * 256 - N;
+  return (N >= 256 && w256 <= w128 && !getenv("CG_TC_BN128")) ? 256 : 128;
+}
+
 void dot_tc_split(int M, int N, int K, int num_sms, int* splits, int* kb_per_split) {
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int bn = pick_bn(N);
+  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int nk = (K + BK - 1) / BK;
   int S = 1;
   if (tiles < num_sms) S = std::max(1, std::min((num_sms + tiles - 1) / tiles, nk / 4));
@@ -515,6 +542,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   p->M = M; p->N = N; p->K = K;
   p->num_sms = num_sms;
   p->raw_hi = 1;  // tcgen05 kind::tf32 truncates fp32 operands (tests: test_tf32_truncation_probe)
+  if (getenv("CG_PROBE_1XTF32")) p->raw_hi = 2;  // measurement probe only (lower accuracy)
   dot_tc_split(M, N, K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
   if (p->splits > 1 && !ws) return -3;
@@ -524,31 +552,35 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   bool ok = ta ? make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, K, M, 32, true)
                : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM, false);
   // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x 128 n)
-  ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, BN, false)
+  p->bn = pick_bn(N);
+  ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, p->bn, false)
                  : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32, true));
   return ok ? 0 : -2;
 }
 
-cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
+template <bool G, int BNT>
+cudaError_t launch_tc(const DotTcPlan& p, float* out, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(gemm_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<G, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC<BNT>::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const int units = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.splits;
+  const int units = ((p.M + BM - 1) / BM) * ((p.N + BNT - 1) / BNT) * p.splits;
   const int grid = std::max(1, std::min(units, p.num_sms));
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
+  gemm_tc_kernel<G, BNT><<<grid, G ? THREADS_GATHER : THREADS, TC<BNT>::SMEM_BYTES, s>>>(
+      a, b, out, p.M, p.N, p.K, G ? 0 : p.a_mn, G ? 1 : p.b_mn, p.kb_per_split, p.splits, p.conv, p.raw_hi, p.dbg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   float* out = p.splits > 1 ? p.ws : p.C;
-  if (p.conv.x)
-    gemm_tc_kernel<true><<<grid, THREADS_GATHER, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, 0, 1, p.kb_per_split, p.splits,
-                                                                   p.conv, p.raw_hi, p.dbg);
-  else
-    gemm_tc_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(a, b, out, p.M, p.N, p.K, p.a_mn, p.b_mn, p.kb_per_split,
-                                                             p.splits, p.conv, p.raw_hi, p.dbg);
+  cudaError_t e0;
+  if (p.conv.x) e0 = p.bn == 256 ? launch_tc<true, 256>(p, out, s) : launch_tc<true, 128>(p, out, s);
+  else e0 = p.bn == 256 ? launch_tc<false, 256>(p, out, s) : launch_tc<false, 128>(p, out, s);
+  if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_reduce_finalize(p.ws, p.C, (long long)p.M * p.N, p.splits, 0, s);
@@ -563,13 +595,14 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   std::memset(p, 0, sizeof(*p));
   p->M = (int)M; p->N = co; p->K = kh * kw * ci;
   p->num_sms = num_sms;
-  p->raw_hi = 1;
+  p->raw_hi = getenv("CG_PROBE_1XTF32") ? 2 : 1;
   dot_tc_split(p->M, p->N, p->K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
   if (p->splits > 1 && !ws) return -3;
   p->a_mn = 0; p->b_mn = 1;
   p->C = y;
   p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl};
+  p->bn = pick_bn(co);
   // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0
   return make_map(reinterpret_cast<CUtensorMap*>(p->mapB), w, p->K, co, 32, true) ? 0 : -2;
 }
