@@ -513,13 +513,15 @@ bool dot_tc_supported(int M, int N, int K, int ta, int tb) {
 
 // N tile: 256 columns when that wastes no more padding than 128 (halves the
 // operand traffic per FLOP: A is re-read per N tile), else 128.
-int pick_bn(int N) {
+int pick_bn(int M, int N, int num_sms) {
   const int w128 = (N + 127) / 128 * 128 - N, w256 = (N + 255) / 256 * 256 - N;
-  return (N >= 256 && w256 <= w128 && !getenv("CG_TC_BN128")) ? 256 : 128;
+  const long long units256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
+  // only with enough units for two waves: otherwise the wider tile just idles SMs
+  return (N >= 256 && w256 <= w128 && units256 >= 2LL * num_sms) ? 256 : 128;
 }
 
 void dot_tc_split(int M, int N, int K, int num_sms, int* splits, int* kb_per_split) {
-  const int bn = pick_bn(N);
+  const int bn = pick_bn(M, N, num_sms);
   const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int nk = (K + BK - 1) / BK;
   int S = 1;
@@ -552,7 +554,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   bool ok = ta ? make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, K, M, 32, true)
                : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM, false);
   // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x 128 n)
-  p->bn = pick_bn(N);
+  p->bn = pick_bn(M, N, num_sms);
   ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, p->bn, false)
                  : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32, true));
   return ok ? 0 : -2;
@@ -602,7 +604,7 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   p->a_mn = 0; p->b_mn = 1;
   p->C = y;
   p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl};
-  p->bn = pick_bn(co);
+  p->bn = pick_bn(p->M, co, num_sms);
   // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0
   return make_map(reinterpret_cast<CUtensorMap*>(p->mapB), w, p->K, co, 32, true) ? 0 : -2;
 }

@@ -185,7 +185,8 @@ def test_dot_integer_exact(m, n, k, ta, tb):
 
 
 # shapes the tcgen05 path takes (16-byte row pitches), with ragged M / N / K tails
-TC_SHAPES = [(128, 128, 32), (300, 136, 100), (129, 260, 36), (784, 1024, 512), (4096, 1024, 784)]
+TC_SHAPES = [(128, 128, 32), (300, 136, 100), (129, 260, 36), (784, 1024, 512), (4096, 1024, 784),
+             (40000, 512, 36)]  # the last one takes 128x256 tiles
 
 
 @pytest.mark.parametrize("m,n,k", TC_SHAPES)
@@ -285,7 +286,7 @@ TC_CONV_CASES = [((2, 35, 35, 64), (3, 3, 64, 96), 1, 1), ((2, 35, 35, 32), (3, 
                  ((4, 17, 17, 48), (7, 1, 48, 64), 1, 1), ((2, 17, 17, 80), (1, 7, 80, 48), 1, 1),
                  ((2, 8, 8, 1280), (1, 1, 1280, 320), 1, 1), ((3, 15, 13, 12), (5, 5, 12, 20), 1, 1),
                  ((2, 31, 29, 3), (3, 3, 3, 32), 2, 0), ((2, 20, 20, 6), (5, 5, 6, 16), 1, 1),
-                 ((2, 8, 8, 64), (3, 3, 64, 448), 1, 1), ((1, 17, 17, 32), (1, 1, 32, 512), 1, 1)]
+                 ((2, 8, 8, 64), (3, 3, 64, 448), 1, 1), ((16, 35, 35, 32), (1, 1, 32, 512), 1, 1)]
 
 
 @pytest.mark.parametrize("xs,ws,st,pad", TC_CONV_CASES)
