@@ -19,6 +19,7 @@
 #include "codegen.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <functional>
 #include <sstream>
@@ -248,7 +249,12 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
     }
     row = true;
   }
-  const int U = 2;
+  // rows (row mode) / vectors (flat mode) in flight per thread per iteration;
+  // CG_EW_UNROLL overrides for measurement sweeps
+  // (measured on C2, tools/ew_sweep.sh: row mode 1 row -> 6.68 TB/s, 2 -> 6.09, 4 -> 6.60)
+  static const int U_env = getenv("CG_EW_UNROLL") ? atoi(getenv("CG_EW_UNROLL")) : 0;
+  const int U_row = U_env > 0 ? U_env : 1;
+  const int U = U_env > 0 ? U_env : 2;
   if (row) {
     ks.mode = "row";
     const int64_t WV = W / V;
@@ -276,17 +282,17 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
         }
       }
     }
-    b << "  const long long step = (long long)gridDim.x * " << TY * U << ";\n";
-    b << "  for (long long rb = (long long)blockIdx.x * " << TY * U << " + ty; rb < " << R << "LL; rb += step) {\n";
+    b << "  const long long step = (long long)gridDim.x * " << TY * U_row << ";\n";
+    b << "  for (long long rb = (long long)blockIdx.x * " << TY * U_row << " + ty; rb < " << R << "LL; rb += step) {\n";
     for (int j = 0; j < KC; ++j) {
       b << "   {\n    const int c = tx + " << j * TX << ";\n";
       b << "    if (c < " << WV << ") {\n";
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U_row; ++u) {
         b << "     const long long r" << u << " = rb + " << u * TY << ";\n";
         b << "     const bool ok" << u << " = r" << u << " < " << R << "LL;\n";
       }
-      // loads for all U rows first (memory-level parallelism)
-      for (int u = 0; u < U; ++u) {
+      // loads for all U_row rows first (memory-level parallelism)
+      for (int u = 0; u < U_row; ++u) {
         for (size_t q = 0; q < nin; ++q) {
           std::string rv = "r" + std::to_string(u);
           if (so[q] == 0 && (si[q] == 0 || hoist)) continue;
@@ -301,7 +307,7 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
           }
         }
       }
-      for (int u = 0; u < U; ++u) {
+      for (int u = 0; u < U_row; ++u) {
         b << "     {\n";
         for (int l = 0; l < V; ++l)
           for (size_t q = 0; q < nin; ++q) {
@@ -328,7 +334,7 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
       b << "    }\n   }\n";
     }
     b << "  }\n}\n";
-    int64_t work = (R + TY * U - 1) / (TY * U);
+    int64_t work = (R + TY * U_row - 1) / (TY * U_row);
     ks.work_blocks = work;
     ks.grid[0] = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)num_sms * 8));
     ks.source = finish("ew", b.str(), &ks.name);

@@ -277,8 +277,11 @@ static int build_launches(cg_graph* g) {
       unsigned block = ks.block;
       if (ks.mode != "red") {  // grid-stride kernels: exactly one full wave of resident blocks
         int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k, (int)block, 0) == cudaSuccess && occ > 0)
+        static const int occ_cap = getenv("CG_EW_BLOCKS_PER_SM") ? atoi(getenv("CG_EW_BLOCKS_PER_SM")) : 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k, (int)block, 0) == cudaSuccess && occ > 0) {
+          if (occ_cap > 0) occ = std::min(occ, occ_cap);
           grid.x = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ks.work_blocks, (int64_t)g->num_sms * occ));
+        }
         cudaGetLastError();
       }
       auto st = std::make_shared<std::vector<void*>>(argv);
