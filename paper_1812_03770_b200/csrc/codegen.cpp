@@ -516,7 +516,30 @@ KernelSpec gen_red(const HostGraph& hg, const Group& G, int num_sms) {
       b << "    const float x" << q << "_0 = in" << q << "[" << seg_off(sO[q], "o") << " + " << seg_off(sI[q], "i") << "];\n";
     }
   }
-  b << "    for (long long rr = r_lo + ty; rr < r_hi; rr += " << TY << ") {\n";
+  // main loop: RU consecutive rows of this thread per iteration, all loads first
+  // (memory-level parallelism), then the prologue ops and the accumulation in
+  // row order -- the same summation order as one row at a time
+  const int RU = 4;
+  b << "    long long rr = r_lo + ty;\n";
+  b << "    for (; rr + " << (RU - 1) * TY << " < r_hi; rr += " << RU * TY << ") {\n";
+  for (size_t q = 0; q < nin; ++q)
+    for (int l = 0; l < RU; ++l) {
+      if (hoisted[q]) {
+        if (l) b << "     const float x" << q << "_" << l << " = x" << q << "_0;\n";
+        continue;
+      }
+      b << "     const float x" << q << "_" << l << " = in" << q << "[" << seg_off(sO[q], "o") << " + "
+        << seg_off(sR[q], "rr + " + std::to_string(l * TY)) << " + " << seg_off(sI[q], "i") << "];\n";
+    }
+  b << me.emit(RU);
+  for (int l = 0; l < RU; ++l) {
+    for (size_t j = 0; j < interior.size(); ++j)
+      b << "     out" << j << "[(o * " << Rn << "LL + rr + " << l * TY << ") * " << I << "LL + i] = v" << interior[j] << "_" << l
+        << ";\n";
+    b << "     acc = " << comb("acc", me.name(red_in, l)) << ";\n";
+  }
+  b << "    }\n";
+  b << "    for (; rr < r_hi; rr += " << TY << ") {\n";
   for (size_t q = 0; q < nin; ++q) {
     if (hoisted[q]) continue;
     b << "     const float x" << q << "_0 = in" << q << "[" << seg_off(sO[q], "o") << " + " << seg_off(sR[q], "rr") << " + "

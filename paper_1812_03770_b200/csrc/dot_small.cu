@@ -18,6 +18,7 @@
 #include <algorithm>
 
 #include "dot_small.h"
+#include "kernels.h"
 
 namespace cg {
 
@@ -119,7 +120,17 @@ __global__ void __launch_bounds__(256) dot_smalln_cols(const float* __restrict__
     }
     __syncthreads();
     if (m < M) {
-      for (int k = 0; k < kn; ++k) {
+      int k = 0;
+      for (; k + 8 <= kn; k += 8) {  // 8 independent loads in flight, then the FMAs in k order
+        float a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = __ldg(A + (size_t)(k0 + k + q) * M + m);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) acc[j] = fmaf(a[q], bs[k + q][j], acc[j]);
+      }
+      for (; k < kn; ++k) {
         const float a = __ldg(A + (size_t)(k0 + k) * M + m);
 #pragma unroll
         for (int j = 0; j < NT; ++j) acc[j] = fmaf(a, bs[k][j], acc[j]);
@@ -131,15 +142,6 @@ __global__ void __launch_bounds__(256) dot_smalln_cols(const float* __restrict__
 #pragma unroll
     for (int j = 0; j < NT; ++j)
       if (j < N) o[j] = acc[j];
-  }
-}
-
-// fixed-order sum of S partial [M*N] planes
-__global__ void sum_partials(const float* __restrict__ ws, float* __restrict__ C, long long n, int S) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    float acc = ws[i];
-    for (int s = 1; s < S; ++s) acc = __fadd_rn(acc, ws[(long long)s * n + i]);
-    C[i] = acc;
   }
 }
 
@@ -159,29 +161,41 @@ __global__ void __launch_bounds__(256) dot_smallk(const float* __restrict__ A, c
   const int q = threadIdx.x % 64, r = threadIdx.x / 64;
   const int n = n0 + q * 4;
   const bool vec = (N % 4) == 0;
-  for (int m = blockIdx.y * 4 + r; m < M; m += gridDim.y * 4) {
-    float a[32];
+  // RPT rows per thread per iteration: all A loads of those rows first (ILP)
+  constexpr int RPT = 4;
+  for (int mb = (blockIdx.y * 4 + r) * RPT; mb < M; mb += gridDim.y * 4 * RPT) {
+    float a[RPT][32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) a[k] = (k < K) ? __ldg(ta ? A + (size_t)k * M + m : A + (size_t)m * K + k) : 0.f;
-    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+    for (int i = 0; i < RPT; ++i) {
+      const int m = mb + i;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      if (k < K) {
-        const float4 b = *reinterpret_cast<const float4*>(&bs[k][q * 4]);
-        c0 = fmaf(a[k], b.x, c0);
-        c1 = fmaf(a[k], b.y, c1);
-        c2 = fmaf(a[k], b.z, c2);
-        c3 = fmaf(a[k], b.w, c3);
-      }
+      for (int k = 0; k < 32; ++k)
+        a[i][k] = (k < K && m < M) ? __ldg(ta ? A + (size_t)k * M + m : A + (size_t)m * K + k) : 0.f;
     }
-    float* crow = C + (size_t)m * N;
-    if (vec && n + 4 <= N) {
-      *reinterpret_cast<float4*>(crow + n) = make_float4(c0, c1, c2, c3);
-    } else {
-      if (n < N) crow[n] = c0;
-      if (n + 1 < N) crow[n + 1] = c1;
-      if (n + 2 < N) crow[n + 2] = c2;
-      if (n + 3 < N) crow[n + 3] = c3;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int m = mb + i;
+      if (m >= M) break;
+      float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k < K) {
+          const float4 b = *reinterpret_cast<const float4*>(&bs[k][q * 4]);
+          c0 = fmaf(a[i][k], b.x, c0);
+          c1 = fmaf(a[i][k], b.y, c1);
+          c2 = fmaf(a[i][k], b.z, c2);
+          c3 = fmaf(a[i][k], b.w, c3);
+        }
+      }
+      float* crow = C + (size_t)m * N;
+      if (vec && n + 4 <= N) {
+        *reinterpret_cast<float4*>(crow + n) = make_float4(c0, c1, c2, c3);
+      } else {
+        if (n < N) crow[n] = c0;
+        if (n + 1 < N) crow[n + 1] = c1;
+        if (n + 2 < N) crow[n + 2] = c2;
+        if (n + 3 < N) crow[n + 3] = c3;
+      }
     }
   }
 }
@@ -208,7 +222,9 @@ cudaError_t launch_rows(const float* A, const float* B, float* C, int M, int N, 
     attr = true;
   }
   const int warps = 8;
-  int grid = std::min((M + warps - 1) / warps, num_sms * 4);
+  // few blocks, many rows each: op(B)^T is staged once per block and reused
+  const int blocks_per_sm = std::max(1, std::min(4, (int)(227 * 1024 / std::max<size_t>(smem, 1))));
+  int grid = std::min((M + warps - 1) / warps, num_sms * blocks_per_sm);
   dot_smalln_rows<NT><<<grid, warps * 32, smem, s>>>(A, B, C, M, N, K, tb, kc);
   return cudaGetLastError();
 }
@@ -222,9 +238,7 @@ cudaError_t launch_cols(const float* A, const float* B, float* C, float* ws, int
   dot_smalln_cols<NT><<<grid, 256, 0, s>>>(A, B, S > 1 ? ws : C, M, N, K, tb, kchunk);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
-  long long n = (long long)M * N;
-  sum_partials<<<(int)std::min<long long>((n + 255) / 256, num_sms * 8LL), 256, 0, s>>>(ws, C, n, S);
-  return cudaGetLastError();
+  return launch_reduce_finalize(ws, C, (long long)M * N, S, 0, s);
 }
 
 }  // namespace
@@ -246,7 +260,7 @@ cudaError_t launch_dot_small(const float* A, const float* B, float* C, float* ws
                              int num_sms, cudaStream_t s) {
   const int kind = dot_small_kind(M, N, K);
   if (kind == DOT_SMALL_K) {
-    dim3 grid((N + SK_TN - 1) / SK_TN, std::min((M + 3) / 4, std::max(1, num_sms * 8 / ((N + SK_TN - 1) / SK_TN))));
+    dim3 grid((N + SK_TN - 1) / SK_TN, std::min((M + 15) / 16, std::max(1, num_sms * 8 / ((N + SK_TN - 1) / SK_TN))));
     dot_smallk<<<grid, 256, 0, s>>>(A, B, C, M, N, K, ta, tb);
     return cudaGetLastError();
   }
