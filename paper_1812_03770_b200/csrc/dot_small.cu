@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) dot_smallk(const float* __restrict__ A, c
   const int n = n0 + q * 4;
   const bool vec = (N % 4) == 0;
   // RPT rows per thread per iteration: all A loads of those rows first (ILP)
-  constexpr int RPT = 4;
+  constexpr int RPT = 1;
   for (int mb = (blockIdx.y * 4 + r) * RPT; mb < M; mb += gridDim.y * 4 * RPT) {
     float a[RPT][32];
 #pragma unroll
@@ -260,7 +260,8 @@ cudaError_t launch_dot_small(const float* A, const float* B, float* C, float* ws
                              int num_sms, cudaStream_t s) {
   const int kind = dot_small_kind(M, N, K);
   if (kind == DOT_SMALL_K) {
-    dim3 grid((N + SK_TN - 1) / SK_TN, std::min((M + 15) / 16, std::max(1, num_sms * 8 / ((N + SK_TN - 1) / SK_TN))));
+    const int gx = (N + SK_TN - 1) / SK_TN;
+    dim3 grid(gx, std::min((M + 3) / 4, std::max(1, num_sms * 6 / gx)));  // one full wave (32 KB smem / block)
     dot_smallk<<<grid, 256, 0, s>>>(A, B, C, M, N, K, ta, tb);
     return cudaGetLastError();
   }
