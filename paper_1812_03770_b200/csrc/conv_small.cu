@@ -214,6 +214,166 @@ __global__ void __launch_bounds__(256) conv_bwdk_img(const float* __restrict__ x
   }
 }
 
+// ---------------------------------------------------------------- register-tiled, stride 1
+// Forward correlation of a zero-padded, channel-planar image with a KS x KS
+// kernel; each thread computes PX horizontally adjacent output pixels x all
+// (padded) output channels, sliding a window of PX+KS-1 input values along the
+// row so every shared-memory load feeds PX*COP FMAs.  FLIP = 1 runs the
+// backward-input pass as this same correlation: input = dy (channels Co),
+// weights flipped in both taps and transposed (ci <-> co), padding KS-1-p.
+// Accumulation order per output: ci, kh, kw ascending (deterministic).
+struct RtGeom {
+  int n, hin, win, cin;     // image fed to the correlation (x, or dy for FLIP)
+  int hout, wout, cout;     // result (y, or dx for FLIP)
+  int pt, pl;               // zero padding in front
+  int wcin, wcout;          // weight tensor [KS][KS][wcin][wcout] as stored (HWIO)
+  int Hp, Wp;               // padded image dims in shared memory
+};
+
+template <int COP, int KS, int PX, bool FLIP>
+__global__ void __launch_bounds__(256) conv_rt_kernel(const float* __restrict__ x, const float* __restrict__ w,
+                                                      float* __restrict__ y, RtGeom g) {
+  extern __shared__ float sm[];
+  float* ws = sm;                                  // [KS*KS*cin][COP]
+  float* xs = sm + KS * KS * g.cin * COP;          // [cin][Hp][Wp]
+  for (int e = threadIdx.x; e < KS * KS * g.cin * COP; e += blockDim.x) {
+    const int co = e % COP, r = e / COP, ci = r % g.cin, tap = r / g.cin;
+    float v = 0.f;
+    if (co < g.cout) {
+      if (!FLIP) {
+        v = w[((size_t)tap * g.cin + ci) * g.cout + co];
+      } else {  // wf[kh][kw][ci'=co_orig][co'=ci_orig] = w[KS-1-kh][KS-1-kw][ci_orig][co_orig]
+        const int kh = tap / KS, kw = tap % KS;
+        const int ftap = (KS - 1 - kh) * KS + (KS - 1 - kw);
+        v = w[((size_t)ftap * g.wcin + co) * g.wcout + ci];
+      }
+    }
+    ws[e] = v;
+  }
+  const int WQ = (g.wout + PX - 1) / PX, items = g.hout * WQ;
+  const int img = g.hin * g.win * g.cin;
+  for (int n = blockIdx.x; n < g.n; n += gridDim.x) {
+    __syncthreads();
+    const float* xi = x + (size_t)n * img;
+    for (int e = threadIdx.x; e < g.cin * g.Hp * g.Wp; e += blockDim.x) {
+      const int wp = e % g.Wp, q = e / g.Wp, hp = q % g.Hp, c = q / g.Hp;
+      const int h = hp - g.pt, ww = wp - g.pl;
+      xs[e] = (h >= 0 && h < g.hin && ww >= 0 && ww < g.win) ? __ldg(xi + ((size_t)h * g.win + ww) * g.cin + c) : 0.f;
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+      const int ho = it / WQ, wo0 = (it - ho * WQ) * PX;
+      float acc[PX][COP];
+#pragma unroll
+      for (int p = 0; p < PX; ++p)
+#pragma unroll
+        for (int c = 0; c < COP; ++c) acc[p][c] = 0.f;
+      for (int ci = 0; ci < g.cin; ++ci) {
+#pragma unroll
+        for (int kh = 0; kh < KS; ++kh) {
+          const float* xr = xs + ((size_t)ci * g.Hp + ho + kh) * g.Wp + wo0;
+          float xv[PX + KS - 1];
+#pragma unroll
+          for (int q = 0; q < PX + KS - 1; ++q) xv[q] = xr[q];
+#pragma unroll
+          for (int kw = 0; kw < KS; ++kw) {
+            const float* wp = ws + ((kh * KS + kw) * g.cin + ci) * COP;
+#pragma unroll
+            for (int c = 0; c < COP; c += 4) {
+              const float4 b = *reinterpret_cast<const float4*>(wp + c);
+#pragma unroll
+              for (int p = 0; p < PX; ++p) {
+                const float a = xv[p + kw];
+                acc[p][c] = fmaf(a, b.x, acc[p][c]);
+                acc[p][c + 1] = fmaf(a, b.y, acc[p][c + 1]);
+                acc[p][c + 2] = fmaf(a, b.z, acc[p][c + 2]);
+                acc[p][c + 3] = fmaf(a, b.w, acc[p][c + 3]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < PX; ++p) {
+        if (wo0 + p >= g.wout) break;
+        float* yp = y + (((size_t)n * g.hout + ho) * g.wout + wo0 + p) * g.cout;
+#pragma unroll
+        for (int c = 0; c < COP; ++c)
+          if (c < g.cout) yp[c] = acc[p][c];
+      }
+    }
+  }
+}
+
+// bwd-kernel, stride 1: thread = (kh, ci, co quad, row phase); the KS kw taps of
+// one (kh, ci) slide along a row (one new x value per pixel) -> 4*KS FMAs per
+// dy float4; per-block partials over a chunk of images, fixed-order reductions.
+template <int KS>
+__global__ void __launch_bounds__(256) conv_bwdk_rt_kernel(const float* __restrict__ x, const float* __restrict__ dy,
+                                                           float* __restrict__ part, ConvGeom g, int Hp, int Wp, int PH,
+                                                           int chunk) {
+  extern __shared__ float sm[];
+  const int CQ = (g.co + 3) / 4, co4 = CQ * 4;
+  const int units = KS * g.ci * CQ;
+  float* xs = sm;                                   // [ci][Hp][Wp]
+  float* ds = sm + (g.ci * Hp * Wp + 3) / 4 * 4;    // [P][co4]
+  const int t = threadIdx.x % units, ph = threadIdx.x / units;
+  const bool active = ph < PH;
+  const int q = t % CQ, r = t / CQ, ci = r % g.ci, kh = r / g.ci;
+  float acc[KS][4];
+#pragma unroll
+  for (int kw = 0; kw < KS; ++kw) acc[kw][0] = acc[kw][1] = acc[kw][2] = acc[kw][3] = 0.f;
+  const int P = g.ho * g.wo;
+  const int n0 = blockIdx.x * chunk, n1 = min(g.n, n0 + chunk);
+  for (int n = n0; n < n1; ++n) {
+    __syncthreads();
+    load_padded(xs, x, n, g.h, g.w, g.ci, Hp, Wp, g.pt, g.pl);
+    const float* dyi = dy + (size_t)n * P * g.co;
+    for (int e = threadIdx.x; e < P * co4; e += blockDim.x) {
+      const int c = e % co4, p = e / co4;
+      ds[e] = c < g.co ? __ldg(dyi + (size_t)p * g.co + c) : 0.f;
+    }
+    __syncthreads();
+    if (active) {
+      for (int ho = ph; ho < g.ho; ho += PH) {
+        const float* xr = xs + ((size_t)ci * Hp + ho + kh) * Wp;
+        float xv[KS];
+#pragma unroll
+        for (int kw = 0; kw < KS - 1; ++kw) xv[kw + 1] = xr[kw];
+        for (int wo = 0; wo < g.wo; ++wo) {
+#pragma unroll
+          for (int kw = 0; kw < KS - 1; ++kw) xv[kw] = xv[kw + 1];
+          xv[KS - 1] = xr[wo + KS - 1];
+          const float4 d = *reinterpret_cast<const float4*>(ds + (ho * g.wo + wo) * co4 + q * 4);
+#pragma unroll
+          for (int kw = 0; kw < KS; ++kw) {
+            acc[kw][0] = fmaf(xv[kw], d.x, acc[kw][0]);
+            acc[kw][1] = fmaf(xv[kw], d.y, acc[kw][1]);
+            acc[kw][2] = fmaf(xv[kw], d.z, acc[kw][2]);
+            acc[kw][3] = fmaf(xv[kw], d.w, acc[kw][3]);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  float* red = sm;  // [PH][KS*KS*ci*co4]
+  const int O = KS * KS * g.ci * co4;
+  if (active) {
+#pragma unroll
+    for (int kw = 0; kw < KS; ++kw)
+      for (int j = 0; j < 4; ++j) red[ph * O + ((kh * KS + kw) * g.ci + ci) * co4 + q * 4 + j] = acc[kw][j];
+  }
+  __syncthreads();
+  const int OO = KS * KS * g.ci * g.co;
+  for (int o = threadIdx.x; o < OO; o += blockDim.x) {
+    const int co = o % g.co, rr = o / g.co;
+    float s_ = red[rr * co4 + co];
+    for (int h = 1; h < PH; ++h) s_ = __fadd_rn(s_, red[h * O + rr * co4 + co]);
+    part[(size_t)blockIdx.x * OO + o] = s_;
+  }
+}
+
 struct Pads {
   int Hp, Wp;
 };
@@ -253,11 +413,72 @@ void set_smem(F f) {
   cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
 }
 
+constexpr int RT_PX = 4;
+
+RtGeom rt_geom_fwd(const ConvGeom& g) {
+  RtGeom r{};
+  r.n = g.n; r.hin = g.h; r.win = g.w; r.cin = g.ci;
+  r.hout = g.ho; r.wout = g.wo; r.cout = g.co;
+  r.pt = g.pt; r.pl = g.pl; r.wcin = g.ci; r.wcout = g.co;
+  r.Hp = g.ho + g.kh - 1;
+  r.Wp = (g.wo + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1;
+  return r;
+}
+RtGeom rt_geom_bwdin(const ConvGeom& g) {
+  RtGeom r{};
+  r.n = g.n; r.hin = g.ho; r.win = g.wo; r.cin = g.co;
+  r.hout = g.h; r.wout = g.w; r.cout = g.ci;
+  r.pt = g.kh - 1 - g.pt; r.pl = g.kw - 1 - g.pl; r.wcin = g.ci; r.wcout = g.co;
+  r.Hp = g.h + g.kh - 1;
+  r.Wp = (g.w + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1;
+  return r;
+}
+size_t rt_smem(const RtGeom& r, int cop, int ks) {
+  return ((size_t)ks * ks * r.cin * cop + (size_t)r.cin * r.Hp * r.Wp) * 4;
+}
+bool rt_ok(const ConvGeom& g) {  // stride 1, square 5x5 or 3x3 taps
+  return g.sh == 1 && g.sw == 1 && g.kh == g.kw && (g.kh == 5 || g.kh == 3);
+}
+
+template <int COP, bool FLIP>
+cudaError_t launch_rt(const float* x, const float* w, float* y, const RtGeom& r, int ks, int num_sms, cudaStream_t s) {
+  const size_t smem = rt_smem(r, COP, ks);
+  const int grid = std::min(r.n, num_sms * 4);
+  if (ks == 5) {
+    set_smem(conv_rt_kernel<COP, 5, RT_PX, FLIP>);
+    conv_rt_kernel<COP, 5, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r);
+  } else {
+    set_smem(conv_rt_kernel<COP, 3, RT_PX, FLIP>);
+    conv_rt_kernel<COP, 3, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r);
+  }
+  return cudaGetLastError();
+}
+
+void bwdk_rt_geom(const ConvGeom& g, int* PH, int* units) {
+  *units = g.kh * g.ci * ((g.co + 3) / 4);
+  *PH = std::max(1, std::min(g.ho, 256 / std::max(1, *units)));
+}
+size_t bwdk_rt_smem(const ConvGeom& g) {
+  int PH, units;
+  bwdk_rt_geom(g, &PH, &units);
+  const int co4 = (g.co + 3) / 4 * 4;
+  const int Hp = g.ho + g.kh - 1, Wp = g.wo + g.kw - 1;
+  size_t img = ((size_t)g.ci * Hp * Wp + 3) / 4 * 4 + (size_t)g.ho * g.wo * co4;
+  size_t red = (size_t)PH * g.kh * g.kw * g.ci * co4;
+  return std::max(img, red) * 4;
+}
+bool bwdk_rt_ok(const ConvGeom& g) {
+  int PH, units;
+  bwdk_rt_geom(g, &PH, &units);
+  return rt_ok(g) && units <= 256 && bwdk_rt_smem(g) <= SMEM_LIMIT;
+}
+
 }  // namespace
 
 bool conv_small_fwd_ok(const ConvGeom& g) { return co_pad(g.co) && fwd_smem(g) <= SMEM_LIMIT; }
 bool conv_small_bwdin_ok(const ConvGeom& g) { return co_pad(g.ci) && bwdin_smem(g) <= SMEM_LIMIT; }
 bool conv_small_bwdk_ok(const ConvGeom& g) {
+  if (bwdk_rt_ok(g)) return true;
   int PH, units;
   bwdk_geom(g, &PH, &units);
   return g.ci <= 8 && units <= 256 && bwdk_smem(g) <= SMEM_LIMIT;
@@ -268,6 +489,12 @@ size_t conv_small_bwdk_ws(const ConvGeom& g, int num_sms) {
 
 cudaError_t launch_conv_small_fwd(const float* x, const float* w, float* y, const ConvGeom& g, int num_sms,
                                   cudaStream_t s) {
+  if (rt_ok(g) && co_pad(g.co) <= 16) {
+    const RtGeom r = rt_geom_fwd(g);
+    if (rt_smem(r, co_pad(g.co), g.kh) <= SMEM_LIMIT)
+      return co_pad(g.co) == 8 ? launch_rt<8, false>(x, w, y, r, g.kh, num_sms, s)
+                               : launch_rt<16, false>(x, w, y, r, g.kh, num_sms, s);
+  }
   Pads p = pads(g);
   const int Hp = std::max(p.Hp, g.h + g.pt), Wp = std::max(p.Wp, g.w + g.pl);
   const size_t smem = fwd_smem(g);
@@ -287,6 +514,12 @@ cudaError_t launch_conv_small_fwd(const float* x, const float* w, float* y, cons
 
 cudaError_t launch_conv_small_bwdin(const float* dy, const float* w, float* dx, const ConvGeom& g, int num_sms,
                                     cudaStream_t s) {
+  if (rt_ok(g) && co_pad(g.ci) <= 16) {  // the transposed correlation of dy with the flipped kernel
+    const RtGeom r = rt_geom_bwdin(g);
+    if (rt_smem(r, co_pad(g.ci), g.kh) <= SMEM_LIMIT)
+      return co_pad(g.ci) == 8 ? launch_rt<8, true>(dy, w, dx, r, g.kh, num_sms, s)
+                               : launch_rt<16, true>(dy, w, dx, r, g.kh, num_sms, s);
+  }
   const size_t smem = bwdin_smem(g);
   const int grid = std::min(g.n, num_sms * 8);
   const bool k5 = g.kh == 5 && g.kw == 5;
@@ -304,6 +537,25 @@ cudaError_t launch_conv_small_bwdin(const float* dy, const float* w, float* dx, 
 
 cudaError_t launch_conv_small_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g,
                                    int num_sms, cudaStream_t s) {
+  if (bwdk_rt_ok(g)) {
+    int PH, units;
+    bwdk_rt_geom(g, &PH, &units);
+    const int blocks = bwdk_blocks(g, num_sms);
+    const int chunk = (g.n + blocks - 1) / blocks;
+    const int nb = (g.n + chunk - 1) / chunk;
+    const size_t smem = bwdk_rt_smem(g);
+    const int Hp = g.ho + g.kh - 1, Wp = g.wo + g.kw - 1;
+    if (g.kh == 5) {
+      set_smem(conv_bwdk_rt_kernel<5>);
+      conv_bwdk_rt_kernel<5><<<nb, 256, smem, s>>>(x, dy, ws, g, Hp, Wp, PH, chunk);
+    } else {
+      set_smem(conv_bwdk_rt_kernel<3>);
+      conv_bwdk_rt_kernel<3><<<nb, 256, smem, s>>>(x, dy, ws, g, Hp, Wp, PH, chunk);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_reduce_finalize(ws, dw, (long long)g.kh * g.kw * g.ci * g.co, nb, 0, s);
+  }
   Pads p = pads(g);
   const int Hp = std::max(p.Hp, g.h + g.pt), Wp = std::max(p.Wp, g.w + g.pl);
   int PH, units;
