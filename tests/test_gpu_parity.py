@@ -280,7 +280,8 @@ def test_conv_family_integer_exact(sh, pad):
 CONV_CASES = [((8, 28, 28, 1), (5, 5, 1, 6), 1, 1), ((8, 14, 14, 6), (5, 5, 6, 16), 1, 0),
               ((4, 13, 11, 3), (3, 3, 3, 8), 2, 1), ((4, 12, 12, 5), (5, 3, 5, 20), 2, 0),
               ((4, 13, 11, 3), (3, 3, 3, 8), 1, 1), ((3, 9, 10, 12), (3, 3, 12, 16), 1, 0),
-              ((2, 17, 15, 2), (5, 5, 2, 10), 1, 1),
+              ((2, 17, 15, 2), (5, 5, 2, 10), 1, 1), ((2, 15, 13, 6), (5, 5, 6, 8), 1, 1),
+              ((2, 11, 12, 5), (3, 3, 5, 7), 1, 0),
               ((2, 9, 9, 40), (3, 3, 40, 48), 1, 1), ((2, 9, 9, 40), (3, 3, 40, 48), 2, 0)]
 
 # geometries of C5's InceptionV3 convolutions (tcgen05 implicit GEMM, forward)
