@@ -65,7 +65,7 @@ class cg_report(ctypes.Structure):
 
 class cg_plan_info(ctypes.Structure):
     _fields_ = [("n_groups", ctypes.c_int32), ("n_blocks", ctypes.c_int32), ("n_kernels", ctypes.c_int32),
-                ("pad_", ctypes.c_int32), ("pool_bytes", ctypes.c_uint64), ("plan_bytes", ctypes.c_uint64),
+                ("n_fused", ctypes.c_int32), ("pool_bytes", ctypes.c_uint64), ("plan_bytes", ctypes.c_uint64),
                 ("external_bytes", ctypes.c_uint64), ("workspace_bytes", ctypes.c_uint64),
                 ("unshared_bytes", ctypes.c_uint64)]
 
@@ -205,7 +205,7 @@ class Graph:
     def plan_memory(self, outputs, flags: int = 0) -> dict:
         info = cg_plan_info()
         self._check(lib().cg_plan_memory(self.h, _ids(outputs), len(outputs), int(flags), ctypes.byref(info)))
-        return {f: getattr(info, f) for f, _ in cg_plan_info._fields_ if f != "pad_"}
+        return {f: getattr(info, f) for f, _ in cg_plan_info._fields_}
 
     # ---- run
     def assign(self, var: int, value):

@@ -169,7 +169,7 @@ template <bool GATHER, int BNT>
 __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                    int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
-                   float* __restrict__ dbg) {
+                   const __grid_constant__ EpiProg epi, float* __restrict__ dbg) {
   using T = TC<BNT>;
   constexpr int BN = T::BN, STAGES = T::STAGES, LSTAGES = T::LSTAGES;
   constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, STAGE_BYTES = T::STAGE_BYTES, LO_BYTES = T::LO_BYTES;
@@ -369,6 +369,27 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
               "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (epi.n) {  // fused elementwise epilogue, IEEE-rounded per op like the unfused kernel
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int col = min(n0 + c0 + q, N - 1);
+            float v = __uint_as_float(r[q]);
+            for (int e = 0; e < epi.n; ++e) {
+              const float xv = epi.op[e] == EPI_RELU ? 0.f : __ldg(epi.x[e] + (epi.scalar[e] ? 0 : col));
+              const float a = epi.swap[e] ? xv : v, bb = epi.swap[e] ? v : xv;
+              switch (epi.op[e]) {
+                case EPI_ADD: v = __fadd_rn(a, bb); break;
+                case EPI_SUB: v = __fsub_rn(a, bb); break;
+                case EPI_MUL: v = __fmul_rn(a, bb); break;
+                case EPI_DIV: v = __fdiv_rn(a, bb); break;
+                case EPI_RELU: v = v > 0.f ? v : 0.f; break;
+                case EPI_MAX: asm("max.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(bb)); break;
+                case EPI_MIN: asm("min.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(bb)); break;
+              }
+            }
+            r[q] = __float_as_uint(v);
+          }
+        }
         if (row < M && n0 + c0 < N) {
           float* crow = Cz + (size_t)row * N;
           const int n = n0 + c0;
@@ -573,7 +594,7 @@ cudaError_t launch_tc(const DotTcPlan& p, float* out, cudaStream_t s) {
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
   gemm_tc_kernel<G, BNT><<<grid, G ? THREADS_GATHER : THREADS, TC<BNT>::SMEM_BYTES, s>>>(
-      a, b, out, p.M, p.N, p.K, G ? 0 : p.a_mn, G ? 1 : p.b_mn, p.kb_per_split, p.splits, p.conv, p.raw_hi, p.dbg);
+      a, b, out, p.M, p.N, p.K, G ? 0 : p.a_mn, G ? 1 : p.b_mn, p.kb_per_split, p.splits, p.conv, p.raw_hi, p.epi, p.dbg);
   return cudaGetLastError();
 }
 

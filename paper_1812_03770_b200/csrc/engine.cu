@@ -161,6 +161,13 @@ struct cg_graph {
   int full_kernels = 0;
   int64_t launches = 0;
   int n_kernels = 0;
+  // f2 epilogue fusion: tensor-core plan per group; partner[g] = the fused elementwise
+  // group of a DOT/CONV group and vice versa (-1: none); fused_away[d] = the DOT/CONV
+  // value is never materialised (its consumer group is computed in the epilogue)
+  std::vector<std::shared_ptr<DotTcPlan>> tcplan;
+  std::vector<int> partner;
+  std::vector<char> fused_away;
+  int n_fused = 0;
   cg_plan_info info{};
 
   int fail(int code, const std::string& m) {
@@ -215,6 +222,82 @@ static ConvGeom geom(const Node& nd, const Shape& x, const Shape& y, int kh, int
   return g;
 }
 
+// ---------------------------------------------------------------- f2: epilogue fusion
+// A tensor-core DOT/CONV group whose value d feeds exactly one group, an
+// elementwise chain d -> op(., x1) -> op(., x2) ... with per-column vectors or
+// scalars as the other operands, runs that chain in its epilogue and writes the
+// chain's sink directly; d is never materialised.  The Alg. 1 plan is unchanged
+// (d's block is simply not written).  Readings: DESIGN.md "f2 epilogue fusion".
+static void fuse_epilogues(cg_graph* g) {
+  HostGraph& hg = g->hg;
+  const size_t NG = hg.groups.size();
+  g->partner.assign(NG, -1);
+  g->fused_away.assign(hg.nodes.size(), 0);
+  g->n_fused = 0;
+  if (getenv("CG_NO_EPILOGUE_FUSION")) return;
+  std::vector<int> consumers(hg.nodes.size(), 0), consumer_group(hg.nodes.size(), -1);
+  for (size_t gi = 0; gi < NG; ++gi)
+    for (int p : hg.groups[gi].inputs) {
+      consumers[p]++;
+      consumer_group[p] = (int)gi;
+    }
+  for (size_t gd = 0; gd < NG; ++gd) {
+    auto plan = g->tcplan[gd];
+    if (!plan || plan->splits != 1) continue;
+    const int d = hg.groups[gd].sink;
+    if (hg.keep[d] || consumers[d] != 1) continue;
+    const int ge = consumer_group[d];
+    const Group& E = hg.groups[ge];
+    if (E.kind != G_EW || E.materialised.size() != 1 || E.domain != hg.nodes[d].shape) continue;
+    const Shape& D = hg.nodes[d].shape;
+    const int64_t ncol = D.back();
+    EpiProg prog{};
+    int prev = d;
+    bool ok = true;
+    for (int m : E.members) {
+      const Node& nd = hg.nodes[m];
+      int op = 0;
+      switch (nd.op) {
+        case CG_ADD: op = EPI_ADD; break;
+        case CG_SUB: op = EPI_SUB; break;
+        case CG_MUL: op = EPI_MUL; break;
+        case CG_DIV: op = EPI_DIV; break;
+        case CG_RELU: op = EPI_RELU; break;
+        case CG_MAX2: op = EPI_MAX; break;
+        case CG_MIN2: op = EPI_MIN; break;
+        default: ok = false;
+      }
+      if (!ok || prog.n == kEpiMax) { ok = false; break; }
+      const int e = prog.n++;
+      prog.op[e] = op;
+      if (op == EPI_RELU) {
+        ok = nd.preds.size() == 1 && nd.preds[0] == prev;
+      } else {
+        const int a = nd.preds[0], b = nd.preds[1];
+        if ((a == prev) == (b == prev)) { ok = false; break; }  // exactly one chain operand
+        const int x = a == prev ? b : a;
+        prog.swap[e] = a == prev ? 0 : 1;
+        const Shape& xs = hg.nodes[x].shape;
+        const int64_t nx = numel(xs);
+        bool col = nx == ncol && !xs.empty() && xs.back() == ncol;
+        if (!hg.is_external(x) || !(nx == 1 || col)) { ok = false; break; }
+        prog.scalar[e] = nx == 1 ? 1 : 0;
+        prog.x[e] = g->ptr[x];
+      }
+      if (!ok) break;
+      prev = m;
+    }
+    if (!ok || prev != E.sink) continue;
+    plan->epi = prog;
+    plan->C = g->ptr[E.sink];
+    g->glaunch[ge].clear();
+    g->partner[gd] = ge;
+    g->partner[ge] = (int)gd;
+    g->fused_away[d] = 1;
+    g->n_fused++;
+  }
+}
+
 // ---------------------------------------------------------------- plan: allocate + build launches
 static int build_launches(cg_graph* g) {
   HostGraph& hg = g->hg;
@@ -254,6 +337,7 @@ static int build_launches(cg_graph* g) {
     g->ws_floats = ws_need;
   }
   // 2) compile + closures
+  g->tcplan.assign(hg.groups.size(), nullptr);
   std::vector<std::string> seen;
   for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
     const Group& G = hg.groups[gi];
@@ -340,6 +424,7 @@ static int build_launches(cg_graph* g) {
           auto plan = std::make_shared<DotTcPlan>();
           if (dot_tc_prepare(plan.get(), A, B, out, M, N, K, ta, tb, g->ws, g->num_sms) != 0)
             return g->fail(CG_E_CUDA, "DOT node " + std::to_string(G.sink) + ": cuTensorMapEncodeTiled failed");
+          g->tcplan[gi] = plan;
           L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, plan->splits > 1 ? 2 : 1});
           break;
         }
@@ -359,6 +444,7 @@ static int build_launches(cg_graph* g) {
           if (conv_tc_prepare(plan.get(), x, w, out, cgm.n, cgm.h, cgm.w, cgm.ci, cgm.kh, cgm.kw, cgm.co, cgm.ho, cgm.wo,
                               cgm.sh, cgm.sw, cgm.pt, cgm.pl, g->ws, sms) != 0)
             return g->fail(CG_E_CUDA, "CONV2D node " + std::to_string(G.sink) + ": tensor-core plan failed");
+          g->tcplan[gi] = plan;
           L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, plan->splits > 1 ? 2 : 1});
         } else if (conv_small_fwd_ok(cgm))  // whole images in shared memory (few channels)
           L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
@@ -431,6 +517,7 @@ static int build_launches(cg_graph* g) {
     }
   }
   (void)n;
+  fuse_epilogues(g);
   return 0;
 }
 
@@ -732,6 +819,7 @@ int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint3
   g->info.n_groups = (int)hg.groups.size();
   g->info.n_blocks = (int)hg.pl.size.size();
   g->info.n_kernels = g->n_kernels;
+  g->info.n_fused = g->n_fused;
   g->info.pool_bytes = hg.pl.pool_bytes;
   g->info.plan_bytes = hg.pl.plan_bytes;
   g->info.workspace_bytes = g->ws_floats * sizeof(float);
@@ -793,6 +881,9 @@ int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float*
     if (!force && !(flags & CG_EVAL_FULL) && valid(g, v)) return;
     R[gi] = 1;
     for (int p : hg.groups[gi].inputs) demand(p, false);
+    // an epilogue-fused pair only runs as one kernel
+    const int pg = g->partner.empty() ? -1 : g->partner[gi];
+    if (pg >= 0 && !R[pg]) demand(hg.groups[pg].sink, true);
   };
   for (int r : roots) demand(r, false);
   for (;;) {  // clobber fix-point: a group may not read a block another launched group overwrote
@@ -818,7 +909,14 @@ int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float*
   if (rc < 0) return rc;
   for (size_t gi = 0; gi < NG; ++gi) {
     if (!R[gi]) continue;
-    for (int m : hg.groups[gi].materialised) g->owner[hg.pl.block_of[m]] = m;
+    for (int m : hg.groups[gi].materialised) {
+      const int b = hg.pl.block_of[m];
+      if (!g->fused_away.empty() && g->fused_away[m]) {  // never written: its block holds no value of m
+        if (g->owner[b] == m) g->owner[b] = -1;
+        continue;
+      }
+      g->owner[b] = m;
+    }
     for (int m : hg.groups[gi].members) {
       g->dirty[m] = 0;
       g->count[m]++;

@@ -629,3 +629,64 @@ def test_c3_adagrad_training_with_rewrites():
     """C3 with AdaGrad and every rewrite on (6 Fused_Adagrad + FMA nodes), teacher-forced."""
     _teacher_forced(configs.c3(batch=256, widths=(784, 128, 64, 10), optimizer="adagrad"), 10, 1e-4,
                     rewrites=cg.RW_ALL)
+
+
+# ---------------------------------------------------------------- f2: epilogue fusion
+def test_dot_bias_relu_epilogue_fusion_and_incremental():
+    """DOT -> ADD(bias) -> SUB(scalar) -> RELU runs in the tensor-core epilogue
+    (n_fused == 1) with the unfused kernels' exact per-op rounding; re-assigning
+    only the bias still recomputes the pair (the DOT value is never materialised)."""
+    rng = np.random.default_rng(21)
+    M, N, K = 1000, 384, 200
+    a = rng.integers(-3, 4, (M, K)).astype(np.float32)
+    b = rng.integers(-3, 4, (K, N)).astype(np.float32)
+    bias = rng.standard_normal((1, N)).astype(np.float32)
+    g = cg.Graph(0)
+    va, vb, vbias = g.var(a.shape), g.var(b.shape), g.var(bias.shape)
+    half = g.const(np.float32(0.5))
+    d = g.add_node("DOT", [va, vb], ta=0, tb=0)
+    out = g.add_node("RELU", [g.add_node("SUB", [g.add_node("ADD", [d, vbias]), half])])
+    info = g.plan_memory([out], cg.PLAN_INCREMENTAL)
+    assert info["n_fused"] == 1
+    for x, v in ((va, a), (vb, b), (vbias, bias)):
+        g.assign(x, v)
+    g.eval([out])
+
+    def ref(bias_):
+        z = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
+        return np.maximum((z + bias_) - np.float32(0.5), np.float32(0))
+    assert np.array_equal(g.read(out), ref(bias))
+    bias2 = rng.standard_normal((1, N)).astype(np.float32)
+    g.assign(vbias, bias2)
+    g.eval([out])
+    assert np.array_equal(g.read(out), ref(bias2))
+    assert g.eval_count(d) == 2
+
+
+@pytest.mark.parametrize("xs,ws", [((4, 17, 17, 48), (3, 3, 48, 64)), ((2, 35, 35, 32), (1, 1, 32, 96))])
+def test_conv_bn_relu_epilogue_fusion(xs, ws):
+    """C5's conv -> BN (SUB mean, DIV sd, MUL gamma, ADD beta) -> RELU chain fused."""
+    rng = np.random.default_rng(22)
+    co = ws[3]
+    spec_vals = {"x": rng.uniform(-1, 1, xs).astype(np.float32), "w": rng.uniform(-0.2, 0.2, ws).astype(np.float32)}
+    mean = rng.uniform(-0.1, 0.1, (co,)).astype(np.float32)
+    sd = rng.uniform(0.7, 1.2, (co,)).astype(np.float32)
+    gamma = rng.uniform(0.5, 1.5, (co,)).astype(np.float32)
+    beta = rng.uniform(-0.1, 0.1, (co,)).astype(np.float32)
+    g = cg.Graph(0)
+    vx, vw = g.var(xs), g.var(ws)
+    cm, cs, cgm, cb = g.const(mean), g.const(sd), g.const(gamma), g.const(beta)
+    y = g.add_node("CONV2D", [vx, vw], sh=1, sw=1, pad=1)
+    t = g.add_node("ADD", [g.add_node("MUL", [g.add_node("DIV", [g.add_node("SUB", [y, cm]), cs]), cgm]), cb])
+    out = g.add_node("RELU", [t])
+    info = g.plan_memory([out])
+    assert info["n_fused"] == 1
+    g.assign(vx, spec_vals["x"])
+    g.assign(vw, spec_vals["w"])
+    g.eval([out])
+    og = OGraph()
+    ox, ow = og.add_leaf("VAR", xs), og.add_leaf("VAR", ws)
+    oy = og.add_node("CONV2D", [ox, ow], {"sh": 1, "sw": 1, "pad": 1})
+    yv = evaluate(og, {ox: spec_vals["x"], ow: spec_vals["w"]})[oy]
+    want = np.maximum(((((yv - mean) / sd) * gamma) + beta).astype(np.float32), 0)
+    assert normwise(g.read(out), want) <= 5e-5
