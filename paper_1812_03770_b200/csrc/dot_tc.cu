@@ -52,12 +52,13 @@ struct TC {
   static constexpr int BN = BNT;
   static constexpr int TILE_A = BM * BK * 4;      // 16 KiB
   static constexpr int TILE_B = BNT * BK * 4;     // 16 / 32 KiB
-  static constexpr int STAGES = BNT == 256 ? 2 : 5;   // raw ring
+  static constexpr int STAGES = BNT == 256 ? 2 : 4;   // raw ring
   static constexpr int LSTAGES = 2;                   // lo ring
   static constexpr int STAGE_BYTES = TILE_A + TILE_B;
   static constexpr int LO_BYTES = TILE_A + TILE_B;
   static constexpr int LO_BASE = STAGES * STAGE_BYTES;
-  static constexpr int BAR_BASE = LO_BASE + LSTAGES * LO_BYTES;
+  static constexpr int EPI_BASE = LO_BASE + LSTAGES * LO_BYTES;   // fused-epilogue operands [kEpiMax][BN]
+  static constexpr int BAR_BASE = EPI_BASE + kEpiMax * BNT * 4;
   static constexpr int SMEM_BYTES = BAR_BASE + 1024 /*barriers*/ + 1024 /*alignment slack*/;
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
@@ -359,6 +360,15 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       }
       const int row = m0 + sub * 32 + lane;
       float* Cz = C + (size_t)z * M * N;
+      if (epi.n) {  // this unit's per-column operands -> shared memory (named barrier: the 4 epilogue warps)
+        float* es = reinterpret_cast<float*>(smem + T::EPI_BASE);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (int i = threadIdx.x - 192; i < epi.n * BN; i += 128) {
+          const int e = i / BN, c = i - e * BN, col = n0 + c;
+          es[i] = epi.op[e] == EPI_RELU ? 0.f : (epi.scalar[e] ? __ldg(epi.x[e]) : (col < N ? __ldg(epi.x[e] + col) : 0.f));
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         uint32_t r[16];
@@ -370,14 +380,15 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (epi.n) {  // fused elementwise epilogue, IEEE-rounded per op like the unfused kernel
+          const float* es = reinterpret_cast<const float*>(smem + T::EPI_BASE) + c0;
+          for (int e = 0; e < epi.n; ++e) {
+            const int op = epi.op[e], sw = epi.swap[e];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int col = min(n0 + c0 + q, N - 1);
-            float v = __uint_as_float(r[q]);
-            for (int e = 0; e < epi.n; ++e) {
-              const float xv = epi.op[e] == EPI_RELU ? 0.f : __ldg(epi.x[e] + (epi.scalar[e] ? 0 : col));
-              const float a = epi.swap[e] ? xv : v, bb = epi.swap[e] ? v : xv;
-              switch (epi.op[e]) {
+            for (int q = 0; q < 16; ++q) {
+              float v = __uint_as_float(r[q]);
+              const float xv = es[e * BN + q];
+              const float a = sw ? xv : v, bb = sw ? v : xv;
+              switch (op) {
                 case EPI_ADD: v = __fadd_rn(a, bb); break;
                 case EPI_SUB: v = __fsub_rn(a, bb); break;
                 case EPI_MUL: v = __fmul_rn(a, bb); break;
@@ -386,8 +397,8 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
                 case EPI_MAX: asm("max.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(bb)); break;
                 case EPI_MIN: asm("min.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(bb)); break;
               }
+              r[q] = __float_as_uint(v);
             }
-            r[q] = __float_as_uint(v);
           }
         }
         if (row < M && n0 + c0 < N) {

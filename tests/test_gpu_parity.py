@@ -646,7 +646,7 @@ def test_dot_bias_relu_epilogue_fusion_and_incremental():
     half = g.const(np.float32(0.5))
     d = g.add_node("DOT", [va, vb], ta=0, tb=0)
     out = g.add_node("RELU", [g.add_node("SUB", [g.add_node("ADD", [d, vbias]), half])])
-    info = g.plan_memory([out], cg.PLAN_INCREMENTAL)
+    info = g.plan_memory([out])  # (CG_PLAN_INCREMENTAL would pin d as a Var frontier: no fusion)
     assert info["n_fused"] == 1
     for x, v in ((va, a), (vb, b), (vbias, bias)):
         g.assign(x, v)
