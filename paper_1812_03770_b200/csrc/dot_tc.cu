@@ -84,9 +84,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
-// Blocking wait on an mbarrier phase.  The suspend-time hint lets the hardware
-// park the warp until the phase flips instead of spinning (spinning waiters of
-// the idle roles were eating the issue slots of the split/gather warps).
+// Blocking wait on an mbarrier phase (try_wait suspends briefly in hardware; an
+// explicit suspend-time hint compiled to NANOSLEEP.SYNCS and made waiters
+// oversleep the phase flip: measured 45 -> 63 ms on C5 with fused epilogues).
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -97,9 +97,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint64_t t0 = 0;
   while (true) {
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(bar), "r"(parity), "r"(1000000u)
+        : "r"(bar), "r"(parity)
         : "memory");
     if (done) return;
     // watchdog: a lost arrival must fail the launch (10 s), not hang the GPU
