@@ -369,8 +369,8 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
-#pragma unroll 1
       const int cend = min(BN, N - n0);  // columns of this unit that exist (padding chunks skipped)
+#pragma unroll 1
       for (int c0 = 0; c0 < cend; c0 += 16) {
         uint32_t r[16];
         const uint32_t taddr = tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)(b * BN + c0);
