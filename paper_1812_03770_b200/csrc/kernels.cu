@@ -344,7 +344,9 @@ __device__ __forceinline__ float nanmax(float a, float b) {
   return a;
 }
 
-template <bool MAXP>
+// KS > 0: square KS x KS window known at compile time: the KS*KS loads are issued
+// together (predicated) before the fixed-order combine -> same results, more MLP
+template <bool MAXP, int KS>
 __global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ y, ConvGeom g, int total4) {
   const int C4 = g.co / 4;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total4; t += gridDim.x * blockDim.x) {
@@ -356,6 +358,29 @@ __global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ 
     const float ninf = -__int_as_float(0x7f800000);
     float4 acc = MAXP ? make_float4(ninf, ninf, ninf, ninf) : make_float4(0.f, 0.f, 0.f, 0.f);
     int cnt = 0;
+    if (KS > 0) {
+      float4 v[KS * KS];
+      bool ok[KS * KS];
+#pragma unroll
+      for (int kh = 0; kh < KS; ++kh)
+#pragma unroll
+        for (int kw = 0; kw < KS; ++kw) {
+          const int hi = ho * g.sh + kh - g.pt, wi = wo * g.sw + kw - g.pl;
+          ok[kh * KS + kw] = hi >= 0 && hi < g.h && wi >= 0 && wi < g.w;
+          v[kh * KS + kw] = ok[kh * KS + kw] ? __ldg(x + (((size_t)n * g.h + hi) * g.w + wi) * C4 + c) : acc;
+        }
+#pragma unroll
+      for (int i = 0; i < KS * KS; ++i) {
+        if (!ok[i]) continue;
+        if (MAXP) {
+          acc.x = nanmax(acc.x, v[i].x); acc.y = nanmax(acc.y, v[i].y); acc.z = nanmax(acc.z, v[i].z); acc.w = nanmax(acc.w, v[i].w);
+        } else {
+          acc.x = __fadd_rn(acc.x, v[i].x); acc.y = __fadd_rn(acc.y, v[i].y);
+          acc.z = __fadd_rn(acc.z, v[i].z); acc.w = __fadd_rn(acc.w, v[i].w);
+        }
+        ++cnt;
+      }
+    } else
     for (int kh = 0; kh < g.kh; ++kh) {
       const int hi = ho * g.sh + kh - g.pt;
       if (hi < 0 || hi >= g.h) continue;
@@ -482,7 +507,9 @@ cudaError_t launch_conv2d_bwd_kernel(const float* x, const float* dy, float* dw,
 cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
   if (g.co % 4 == 0 && total < INT32_MAX) {
-    pool4_kernel<true><<<grid_for(total / 4), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
+    const int blocks = (int)std::min<long long>((total / 4 + 255) / 256, 65535LL * 8);
+    if (g.kh == 3 && g.kw == 3) pool4_kernel<true, 3><<<blocks, 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
+    else pool4_kernel<true, 0><<<grid_for(total / 4), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
     return cudaGetLastError();
   }
   if (total < INT32_MAX) maxpool_kernel<int><<<grid_for(total), 256, 0, s>>>(x, y, g, (int)total);
@@ -506,7 +533,9 @@ cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const
 cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
   if (g.co % 4 == 0 && total < INT32_MAX) {
-    pool4_kernel<false><<<grid_for(total / 4), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
+    const int blocks = (int)std::min<long long>((total / 4 + 255) / 256, 65535LL * 8);
+    if (g.kh == 3 && g.kw == 3) pool4_kernel<false, 3><<<blocks, 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
+    else pool4_kernel<false, 0><<<grid_for(total / 4), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
     return cudaGetLastError();
   }
   if (total < INT32_MAX) avgpool_kernel<int><<<grid_for(total), 256, 0, s>>>(x, y, g, (int)total);
