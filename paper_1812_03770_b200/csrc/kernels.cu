@@ -359,8 +359,9 @@ __global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ 
     float4 acc = MAXP ? make_float4(ninf, ninf, ninf, ninf) : make_float4(0.f, 0.f, 0.f, 0.f);
     int cnt = 0;
     if (KS > 0) {
-      float4 v[KS * KS];
-      bool ok[KS * KS];
+      constexpr int KK = KS > 0 ? KS * KS : 1;
+      float4 v[KK];
+      bool ok[KK];
 #pragma unroll
       for (int kh = 0; kh < KS; ++kh)
 #pragma unroll
