@@ -52,7 +52,7 @@ struct TC {
   static constexpr int BN = BNT;
   static constexpr int TILE_A = BM * BK * 4;      // 16 KiB
   static constexpr int TILE_B = BNT * BK * 4;     // 16 / 32 KiB
-  static constexpr int STAGES = BNT == 256 ? 2 : 4;   // raw ring
+  static constexpr int STAGES = BNT == 256 ? 2 : BNT == 128 ? 4 : 6;   // raw ring
   static constexpr int LSTAGES = 2;                   // lo ring
   static constexpr int STAGE_BYTES = TILE_A + TILE_B;
   static constexpr int LO_BYTES = TILE_A + TILE_B;
@@ -547,6 +547,9 @@ bool dot_tc_supported(int M, int N, int K, int ta, int tb) {
 // N tile: 256 columns when that wastes no more padding than 128 (halves the
 // operand traffic per FLOP: A is re-read per N tile), else 128.
 int pick_bn(int M, int N, int num_sms) {
+  // narrow outputs (convs with 32 / 64 channels): a matching MMA N instead of padding to 128
+  if (N <= 32) return 32;
+  if (N <= 64) return 64;
   const int w128 = (N + 127) / 128 * 128 - N, w256 = (N + 255) / 256 * 256 - N;
   const long long units256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
   // only with enough units for two waves: otherwise the wider tile just idles SMs
@@ -613,8 +616,12 @@ cudaError_t launch_tc(const DotTcPlan& p, float* out, cudaStream_t s) {
 cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   float* out = p.splits > 1 ? p.ws : p.C;
   cudaError_t e0;
-  if (p.conv.x) e0 = p.bn == 256 ? launch_tc<true, 256>(p, out, s) : launch_tc<true, 128>(p, out, s);
-  else e0 = p.bn == 256 ? launch_tc<false, 256>(p, out, s) : launch_tc<false, 128>(p, out, s);
+  switch (p.bn) {
+    case 256: e0 = p.conv.x ? launch_tc<true, 256>(p, out, s) : launch_tc<false, 256>(p, out, s); break;
+    case 64: e0 = p.conv.x ? launch_tc<true, 64>(p, out, s) : launch_tc<false, 64>(p, out, s); break;
+    case 32: e0 = p.conv.x ? launch_tc<true, 32>(p, out, s) : launch_tc<false, 32>(p, out, s); break;
+    default: e0 = p.conv.x ? launch_tc<true, 128>(p, out, s) : launch_tc<false, 128>(p, out, s); break;
+  }
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || p.splits == 1) return e;

@@ -186,7 +186,8 @@ def test_dot_integer_exact(m, n, k, ta, tb):
 
 # shapes the tcgen05 path takes (16-byte row pitches), with ragged M / N / K tails
 TC_SHAPES = [(128, 128, 32), (300, 136, 100), (129, 260, 36), (784, 1024, 512), (4096, 1024, 784),
-             (40000, 512, 36)]  # the last one takes 128x256 tiles
+             (40000, 512, 36),  # 128x256 tiles
+             (1000, 48, 100), (500, 64, 64)]  # 128x64 tiles
 
 
 @pytest.mark.parametrize("m,n,k", TC_SHAPES)
