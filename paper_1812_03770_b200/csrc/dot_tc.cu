@@ -47,19 +47,22 @@ constexpr int BM = 128, BK = 32;
 // raw operand tiles (TMA / gather destinations, also the hi operands) live in a
 // ring that runs ahead of the MMAs; the lo tiles written by the split warps only
 // live from the split to the MMA.
-template <int BNT>
+template <int BNT, int CG = 1>
 struct TC {
   static constexpr int BN = BNT;
-  static constexpr int TILE_A = BM * BK * 4;      // 16 KiB
-  static constexpr int TILE_B = BNT * BK * 4;     // 16 / 32 KiB
-  static constexpr int STAGES = BNT == 256 ? 2 : BNT == 128 ? 4 : 6;   // raw ring
-  static constexpr int LSTAGES = 2;                   // lo ring
+  static constexpr int TILE_A = BM * BK * 4;           // 16 KiB
+  static constexpr int TILE_B = BNT / CG * BK * 4;     // this CTA's share of the B tile
   static constexpr int STAGE_BYTES = TILE_A + TILE_B;
   static constexpr int LO_BYTES = TILE_A + TILE_B;
+  static constexpr int LSTAGES = 2;                    // lo ring
+  static constexpr int EPI_BYTES = kEpiMax * BNT * 4;
+  static constexpr int STAGES_FIT = (220 * 1024 - LSTAGES * LO_BYTES - EPI_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;   // raw ring
   static constexpr int LO_BASE = STAGES * STAGE_BYTES;
   static constexpr int EPI_BASE = LO_BASE + LSTAGES * LO_BYTES;   // fused-epilogue operands [kEpiMax][BN]
-  static constexpr int BAR_BASE = EPI_BASE + kEpiMax * BNT * 4;
+  static constexpr int BAR_BASE = EPI_BASE + EPI_BYTES;
   static constexpr int SMEM_BYTES = BAR_BASE + 1024 /*barriers*/ + 1024 /*alignment slack*/;
+  static_assert(STAGES >= 2, "pipeline depth");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 constexpr int THREADS = 320;         // TMA, MMA, 4 split warps, 4 epilogue warps
@@ -134,6 +137,27 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accum));
 }
 
+// arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cta(uint32_t bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+}
+// commit of a CTA-pair MMA: arrive on the barrier at this offset in both CTAs
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+               "h"((uint16_t)3)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -166,13 +190,18 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 // and tfull/tempty per accumulator (MMA -> epilogue -> MMA); the stage index and
 // phase run on a k-block counter that continues across units, so the producers
 // prefetch the next unit while the current one finishes.
-template <bool GATHER, int BNT>
+// CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 issued by the leader: each CTA holds its 128 rows of A
+// and half of the B columns, so per-SM operand traffic and split work drop by a
+// third; the follower's split and epilogue warps arrive on the leader's barriers,
+// the MMA commits multicast to both CTAs.
+template <bool GATHER, int BNT, int CG>
 __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                    int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
                    const __grid_constant__ EpiProg epi, float* __restrict__ dbg) {
-  using T = TC<BNT>;
-  constexpr int BN = T::BN, STAGES = T::STAGES, LSTAGES = T::LSTAGES;
+  using T = TC<BNT, CG>;
+  constexpr int BN = T::BN, STAGES = T::STAGES, LSTAGES = T::LSTAGES, BNH = BNT / CG;
   constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, STAGE_BYTES = T::STAGE_BYTES, LO_BYTES = T::LO_BYTES;
   constexpr int LO_BASE = T::LO_BASE, BAR_BASE = T::BAR_BASE;
   extern __shared__ uint8_t smem_raw[];
@@ -189,15 +218,19 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(smem + BAR_BASE + 512);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  uint32_t rank = 0;
+  if (CG == 2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const bool leader = rank == 0;
+  const int tiles_m = (M + BM * CG - 1) / (BM * CG), tiles_n = (N + BN - 1) / BN;
   const int units = tiles_m * tiles_n * splits;
   const int nkt = (K + BK - 1) / BK;
-  // unit -> (z, m0, n0, kb0, nk)
+  const int u_first = blockIdx.x / CG, u_step = gridDim.x / CG;
+  // unit -> (z, m0 (this CTA's rows), n0, kb0, nk)
   auto unit = [&](int u, int& z, int& m0, int& n0, int& kb0, int& nk) {
     const int per = tiles_m * tiles_n;
     z = u / per;
     const int rem = u - z * per;
-    m0 = (rem / tiles_n) * BM;
+    m0 = (rem / tiles_n) * BM * CG + (int)rank * BM;
     n0 = (rem % tiles_n) * BN;
     kb0 = z * kb_per_split;
     nk = min(nkt - kb0, kb_per_split);
@@ -209,31 +242,38 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       mbar_init(empty(s), 1);
     }
     for (int l = 0; l < LSTAGES; ++l) {
-      mbar_init(conv(l), 4);
+      mbar_init(conv(l), 4 * CG);
       mbar_init(lofree(l), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), 4);
+      mbar_init(tempty(b), 4 * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (!GATHER) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(2 * BN));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (CG == 2) cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+  else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       int it = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = u_first; u < units; u += u_step) {
         int z, m0, n0, kb0, nk;
         unit(u, z, m0, n0, kb0, nk);
         for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -241,7 +281,8 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           const uint32_t ph = (it / STAGES) & 1;
           mbar_wait(empty(s), ph ^ 1);
           const uint32_t st = sbase + s * STAGE_BYTES;
-          mbar_expect_tx(full(s), GATHER ? TILE_B : TILE_A + TILE_B);
+          mbar_expect_tx(full(s), GATHER ? TILE_B : TILE_A + TILE_B);  // (this CTA's B share)
+          const int nb = n0 + (int)rank * BNH;
           const int k0 = (kb0 + kb) * BK;
           if (GATHER) {
           } else if (a_mn) {
@@ -250,20 +291,20 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
             tma_load_2d(st, &mapA, k0, m0, full(s));
           }
           if (b_mn) {
-            for (int j = 0; j < BN / 32; ++j) tma_load_2d(st + TILE_A + j * 4096, &mapB, n0 + 32 * j, k0, full(s));
+            for (int j = 0; j < BNH / 32; ++j) tma_load_2d(st + TILE_A + j * 4096, &mapB, nb + 32 * j, k0, full(s));
           } else {
-            tma_load_2d(st + TILE_A, &mapB, k0, n0, full(s));
+            tma_load_2d(st + TILE_A, &mapB, k0, nb, full(s));
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (the leader CTA of a pair)
       // instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
       int it = 0, j = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      for (int u = u_first; u < units; u += u_step, ++j) {
         int z, m0, n0, kb0, nk;
         unit(u, z, m0, n0, kb0, nk);
         const int b = j & 1;
@@ -280,23 +321,37 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           for (int kk = 0; kk < BK / 8; ++kk) {
             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
             // small terms first, then the leading hi.hi product
-            if (raw_hi != 2) {
-              mma_tf32(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
-              mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
+            if (CG == 1) {
+              if (raw_hi != 2) {
+                mma_tf32(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
+                mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
+              }
+              mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, raw_hi != 2 ? 1u : acc0);
+            } else {
+              if (raw_hi != 2) {
+                mma_tf32_pair(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
+                mma_tf32_pair(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
+              }
+              mma_tf32_pair(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, raw_hi != 2 ? 1u : acc0);
             }
-            mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, raw_hi != 2 ? 1u : acc0);
           }
-          mma_commit(empty(s));   // frees the raw slot once these MMAs have read it
-          mma_commit(lofree(l));  // and the lo slot
+          if (CG == 1) {
+            mma_commit(empty(s));   // frees the raw slot once these MMAs have read it
+            mma_commit(lofree(l));  // and the lo slot
+          } else {
+            mma_commit_pair(empty(s));
+            mma_commit_pair(lofree(l));
+          }
         }
-        mma_commit(tfull(b));
+        if (CG == 1) mma_commit(tfull(b));
+        else mma_commit_pair(tfull(b));
       }
     }
   } else if (warp < 6) {
     // ---------------- warps 2..5: hi/lo split of each stage
     const int t = threadIdx.x - 64;  // 0..127
     int it = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = u_first; u < units; u += u_step) {
       int z, m0, n0, kb0, nk;
       unit(u, z, m0, n0, kb0, nk);
       for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -310,7 +365,10 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         if (raw_hi == 2) {  // probe only: 1xTF32 (no split) to measure what the split costs
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0) mbar_arrive(conv(l));
+          if (lane == 0) {
+            if (CG == 1 || leader) mbar_arrive(conv(l));
+            else mbar_arrive_cta(conv(l), 0);
+          }
           continue;
         }
         // 16 float4 per thread: all loads first (ILP), explicit shared-space ops
@@ -340,7 +398,10 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         // generic-proxy smem writes -> visible to the tensor core (async proxy)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(conv(l));
+        if (lane == 0) {
+          if (CG == 1 || leader) mbar_arrive(conv(l));
+          else mbar_arrive_cta(conv(l), 0);
+        }
       }
     }
   } else if (warp < 10) {
@@ -348,7 +409,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     const int sub = warp % 4;
     const bool vec = (N % 4) == 0;
     int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+    for (int u = u_first; u < units; u += u_step, ++j) {
       int z, m0, n0, kb0, nk;
       unit(u, z, m0, n0, kb0, nk);
       const int b = j & 1;
@@ -420,7 +481,10 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty(b));
+      if (lane == 0) {
+        if (CG == 1 || leader) mbar_arrive(tempty(b));
+        else mbar_arrive_cta(tempty(b), 0);
+      }
     }
   } else if (GATHER) {
     // ---------------- warps 10..13: im2col gather of A, one tile row (output pixel) per thread.
@@ -429,7 +493,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     // contiguous 128-byte run of channels per row.
     const int r = threadIdx.x - 320;
     int it = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = u_first; u < units; u += u_step) {
       int z, m0, n0, kb0, nk;
       unit(u, z, m0, n0, kb0, nk);
       const int m = m0 + r;
@@ -494,10 +558,12 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if (CG == 2) cluster_sync();  // the pair's MMAs (which write both TMEMs) are all complete
+  else __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    if (CG == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -556,6 +622,14 @@ int pick_bn(int M, int N, int num_sms) {
   return (N >= 256 && w256 <= w128 && units256 >= 2LL * num_sms) ? 256 : 128;
 }
 
+// CTA pairs (cta_group::2, 256-row tiles) when the problem has at least two waves
+// of pair units and no split-K; BN >= 64 so each CTA's half of B is >= 32 columns.
+int pick_cg(int M, int N, int bn, int splits, int num_sms) {
+  if (getenv("CG_TC_NO_PAIRS") || splits != 1 || bn < 64 || M < 256) return 1;
+  const long long units2 = (long long)((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn);
+  return units2 >= num_sms ? 2 : 1;
+}
+
 void dot_tc_split(int M, int N, int K, int num_sms, int* splits, int* kb_per_split) {
   const int bn = pick_bn(M, N, num_sms);
   const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
@@ -589,38 +663,59 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   // A: ta = 0 -> [M, K] (K-major, box 32 k x 128 m); ta = 1 -> [K, M] (M-major, box 32 m x 32 k)
   bool ok = ta ? make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, K, M, 32, true)
                : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM, false);
-  // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x 128 n)
+  // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x BN/CG n)
   p->bn = pick_bn(M, N, num_sms);
-  ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, p->bn, false)
+  p->cg = pick_cg(M, N, p->bn, p->splits, num_sms);
+  ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, p->bn / p->cg, false)
                  : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32, true));
   return ok ? 0 : -2;
 }
 
-template <bool G, int BNT>
+template <bool G, int BNT, int CG>
 cudaError_t launch_tc(const DotTcPlan& p, float* out, cudaStream_t s) {
+  using T = TC<BNT, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<G, BNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC<BNT>::SMEM_BYTES);
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<G, BNT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM_BYTES);
   });
   if (attr_err != cudaSuccess) return attr_err;
-  const int units = ((p.M + BM - 1) / BM) * ((p.N + BNT - 1) / BNT) * p.splits;
-  const int grid = std::max(1, std::min(units, p.num_sms));
+  const int units = ((p.M + BM * CG - 1) / (BM * CG)) * ((p.N + BNT - 1) / BNT) * p.splits;
+  const int grid = std::max(1, std::min(units, p.num_sms / CG)) * CG;
   const CUtensorMap& a = *reinterpret_cast<const CUtensorMap*>(p.mapA);
   const CUtensorMap& b = *reinterpret_cast<const CUtensorMap*>(p.mapB);
-  gemm_tc_kernel<G, BNT><<<grid, G ? THREADS_GATHER : THREADS, TC<BNT>::SMEM_BYTES, s>>>(
-      a, b, out, p.M, p.N, p.K, G ? 0 : p.a_mn, G ? 1 : p.b_mn, p.kb_per_split, p.splits, p.conv, p.raw_hi, p.epi, p.dbg);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(G ? THREADS_GATHER : THREADS);
+  cfg.dynamicSmemBytes = T::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<G, BNT, CG>, a, b, out, p.M, p.N, p.K, G ? 0 : p.a_mn, G ? 1 : p.b_mn,
+                            p.kb_per_split, p.splits, p.conv, p.raw_hi, p.epi, p.dbg);
+}
+
+template <bool G, int BNT>
+cudaError_t launch_tc_cg(const DotTcPlan& p, float* out, cudaStream_t s) {
+  if constexpr (BNT >= 64) {
+    if (p.cg == 2) return launch_tc<G, BNT, 2>(p, out, s);
+  }
+  return launch_tc<G, BNT, 1>(p, out, s);
 }
 
 cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   float* out = p.splits > 1 ? p.ws : p.C;
   cudaError_t e0;
   switch (p.bn) {
-    case 256: e0 = p.conv.x ? launch_tc<true, 256>(p, out, s) : launch_tc<false, 256>(p, out, s); break;
-    case 64: e0 = p.conv.x ? launch_tc<true, 64>(p, out, s) : launch_tc<false, 64>(p, out, s); break;
-    case 32: e0 = p.conv.x ? launch_tc<true, 32>(p, out, s) : launch_tc<false, 32>(p, out, s); break;
-    default: e0 = p.conv.x ? launch_tc<true, 128>(p, out, s) : launch_tc<false, 128>(p, out, s); break;
+    case 256: e0 = p.conv.x ? launch_tc_cg<true, 256>(p, out, s) : launch_tc_cg<false, 256>(p, out, s); break;
+    case 64: e0 = p.conv.x ? launch_tc_cg<true, 64>(p, out, s) : launch_tc_cg<false, 64>(p, out, s); break;
+    case 32: e0 = p.conv.x ? launch_tc_cg<true, 32>(p, out, s) : launch_tc_cg<false, 32>(p, out, s); break;
+    default: e0 = p.conv.x ? launch_tc_cg<true, 128>(p, out, s) : launch_tc_cg<false, 128>(p, out, s); break;
   }
   if (e0 != cudaSuccess) return e0;
   cudaError_t e = cudaGetLastError();
@@ -645,6 +740,7 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   p->C = y;
   p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl};
   p->bn = pick_bn(p->M, co, num_sms);
+  p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms);
   // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0
   return make_map(reinterpret_cast<CUtensorMap*>(p->mapB), w, p->K, co, 32, true) ? 0 : -2;
 }
