@@ -622,10 +622,13 @@ int pick_bn(int M, int N, int num_sms) {
   return (N >= 256 && w256 <= w128 && units256 >= 2LL * num_sms) ? 256 : 128;
 }
 
-// CTA pairs (cta_group::2, 256-row tiles) when the problem has at least two waves
+// CTA pairs (cta_group::2, 256-row tiles) when the problem has at least a wave
 // of pair units and no split-K; BN >= 64 so each CTA's half of B is >= 32 columns.
-int pick_cg(int M, int N, int bn, int splits, int num_sms) {
-  if (getenv("CG_TC_NO_PAIRS") || splits != 1 || bn < 64 || M < 256) return 1;
+// Measured: 8192^3 DOT 200 -> 220 TFLOP/s; C5's gathered convs 43 -> 48 ms (their
+// cost is the per-CTA A side, and the pair couples two CTAs' splits), so
+// implicit-GEMM convs stay on single CTAs.
+int pick_cg(int M, int N, int bn, int splits, int num_sms, bool gather) {
+  if (gather || getenv("CG_TC_NO_PAIRS") || splits != 1 || bn < 64 || M < 256) return 1;
   const long long units2 = (long long)((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn);
   return units2 >= num_sms ? 2 : 1;
 }
@@ -665,7 +668,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
                : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM, false);
   // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x BN/CG n)
   p->bn = pick_bn(M, N, num_sms);
-  p->cg = pick_cg(M, N, p->bn, p->splits, num_sms);
+  p->cg = pick_cg(M, N, p->bn, p->splits, num_sms, false);
   ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, p->bn / p->cg, false)
                  : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32, true));
   return ok ? 0 : -2;
@@ -740,7 +743,7 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   p->C = y;
   p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl};
   p->bn = pick_bn(p->M, co, num_sms);
-  p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms);
+  p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms, true);
   // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0
   return make_map(reinterpret_cast<CUtensorMap*>(p->mapB), w, p->K, co, 32, true) ? 0 : -2;
 }
