@@ -436,7 +436,8 @@ static int build_launches(cg_graph* g) {
                             (int)hg.nodes[nd.preds[1]].shape[1]);
         const float *x = in[0], *w = in[1];
         int sms = g->num_sms;
-        if (conv_small_fwd_ok(cgm) && cgm.co <= 16) {  // few channels: whole images in shared memory (HBM-bound)
+        static const bool prefer_tc = getenv("CG_CONV_PREFER_TC") != nullptr;  // A/B measurement switch
+        if (conv_small_fwd_ok(cgm) && cgm.co <= 16 && !prefer_tc) {  // few channels: whole images in shared memory
           L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
         } else if (conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo) &&
                    !getenv("CG_DEBUG_CONV_SIMT")) {  // tcgen05 implicit GEMM
