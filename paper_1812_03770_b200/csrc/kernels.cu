@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdint>
 
 namespace cg {
 
@@ -48,10 +49,44 @@ __global__ void reduce_finalize_kernel(const float* __restrict__ ws, float* __re
   long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= oi) return;
   float acc = ws[j];
-  for (long long s = 1; s < S; ++s) {
+  long long s = 1;
+  for (; s + 4 <= S; s += 4) {  // four partials in flight, combined in s order
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ws[(s + u) * oi + j];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (op == 0) acc = __fadd_rn(acc, v[u]);
+      else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v[u]));  // NaN-propagating, as numpy max
+    }
+  }
+  for (; s < S; ++s) {
     float v = ws[s * oi + j];
     if (op == 0) acc = __fadd_rn(acc, v);
-    else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v));  // NaN-propagating, as numpy max
+    else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v));
+  }
+  out[j] = acc;
+}
+
+// reduce_finalize_kernel on 4 consecutive outputs per thread (oi % 4 == 0).
+__global__ void reduce_finalize4_kernel(const float4* __restrict__ ws, float4* __restrict__ out, long long oi4,
+                                        long long S, int op) {
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= oi4) return;
+  float4 acc = ws[j];
+  auto comb = [&](float& a, float v) {
+    if (op == 0) a = __fadd_rn(a, v);
+    else asm("max.NaN.f32 %0, %0, %1;" : "+f"(a) : "f"(v));
+  };
+  long long s = 1;
+  for (; s + 2 <= S; s += 2) {
+    const float4 v0 = ws[s * oi4 + j], v1 = ws[(s + 1) * oi4 + j];
+    comb(acc.x, v0.x), comb(acc.y, v0.y), comb(acc.z, v0.z), comb(acc.w, v0.w);
+    comb(acc.x, v1.x), comb(acc.y, v1.y), comb(acc.z, v1.z), comb(acc.w, v1.w);
+  }
+  if (s < S) {
+    const float4 v = ws[s * oi4 + j];
+    comb(acc.x, v.x), comb(acc.y, v.y), comb(acc.z, v.z), comb(acc.w, v.w);
   }
   out[j] = acc;
 }
@@ -80,6 +115,38 @@ __global__ void __launch_bounds__(256) reduce_finalize_tree_kernel(const float* 
     __syncthreads();
   }
   if (threadIdx.x == 0) out[j] = sm[0];
+}
+
+// One warp per output: lanes take strided partials, fixed-order shuffle tree.
+__global__ void __launch_bounds__(256) reduce_finalize_warp_kernel(const float* __restrict__ ws, float* __restrict__ out,
+                                                                   long long oi, long long S, int op) {
+  const long long j = (long long)blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (j >= oi) return;
+  float acc = op == 0 ? 0.f : -__int_as_float(0x7f800000);
+  long long s = lane;
+  for (; s + 96 < S; s += 128) {  // four strided partials in flight, combined in s order
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ws[(s + 32 * u) * oi + j];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (op == 0) acc = __fadd_rn(acc, v[u]);
+      else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v[u]));
+    }
+  }
+  for (; s < S; s += 32) {
+    const float v = ws[s * oi + j];
+    if (op == 0) acc = __fadd_rn(acc, v);
+    else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v));
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o /= 2) {
+    const float v = __shfl_xor_sync(0xffffffffu, acc, o);
+    if (op == 0) acc = __fadd_rn(acc, v);
+    else asm("max.NaN.f32 %0, %0, %1;" : "+f"(acc) : "f"(v));
+  }
+  if (lane == 0) out[j] = acc;
 }
 
 // 64x64 output tile, 16-deep k slab, 256 threads x (4x4) outputs, fp32 FFMA
@@ -446,8 +513,16 @@ cudaError_t launch_copy(const float* src, float* dst, long long n, cudaStream_t 
 }
 
 cudaError_t launch_reduce_finalize(const float* ws, float* out, long long oi, long long S, int op, cudaStream_t s) {
-  if (S >= 64 && oi <= 16384) {
+  if (S >= 512 && oi <= 4096) {  // very many partials: a block per output
     reduce_finalize_tree_kernel<<<(unsigned)oi, 256, 0, s>>>(ws, out, oi, S, op);
+    return cudaGetLastError();
+  }
+  if (S >= 8 && oi <= 262144) {  // a warp per output
+    reduce_finalize_warp_kernel<<<(unsigned)((oi + 7) / 8), 256, 0, s>>>(ws, out, oi, S, op);
+    return cudaGetLastError();
+  }
+  if (oi % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    reduce_finalize4_kernel<<<(unsigned)((oi / 4 + 255) / 256), 256, 0, s>>>((const float4*)ws, (float4*)out, oi / 4, S, op);
     return cudaGetLastError();
   }
   reduce_finalize_kernel<<<(unsigned)((oi + 255) / 256), 256, 0, s>>>(ws, out, oi, S, op);

@@ -203,7 +203,8 @@ def test_dot_tc_integer_exact(m, n, k, ta, tb):
 
 # small-extent (HBM-bound SIMT) kernels and split-K tensor-core shapes of C3 / C4
 SMALL_SHAPES = [(4096, 10, 1024), (1024, 10, 4096), (4096, 1024, 10), (84, 10, 8192), (8192, 84, 10),
-                (300, 17, 33), (33, 300, 17), (120, 84, 8192), (400, 120, 8192), (7, 5, 3)]
+                (300, 17, 33), (33, 300, 17), (120, 84, 8192), (400, 120, 8192), (7, 5, 3),
+                (4097, 12, 1024), (513, 11, 130), (2049, 10, 20)]
 
 
 @pytest.mark.parametrize("m,n,k", SMALL_SHAPES)
