@@ -12,19 +12,19 @@
 // < 2^-20 relative, so the result has fp32-GEMM accuracy.
 // Integer-valued operands with |x| < 2^11 have lo == 0 and are multiplied exactly.
 //
-// One CTA computes a BM x BN = 128 x 128 output tile:
-//   warp 0      TMA producer: loads the raw fp32 A/B k-slab (BK = 32, one 128-byte
-//               swizzle row) of stage s with cp.async.bulk.tensor (OOB -> 0, so
-//               ragged M/N/K need no masking on the load side)
-//   warp 1      TMEM allocator + MMA issuer (one elected thread): 3 x 4
-//               tcgen05.mma.kind::tf32 per stage, tcgen05.commit -> empty[s]
-//   warps 2-5   split hi/lo in shared memory (elementwise, layout-preserving, so
-//               the swizzle of the TMA tile is the swizzle of the hi and lo
-//               tiles), then the epilogue: tcgen05.ld TMEM -> registers -> C.
-// Operand majorness comes from the transposes: A is K-major when ta = 0 and
-// M-major when ta = 1; B is N-major when tb = 0 and K-major when tb = 1.  Both
-// are native UMMA smem layouts for TF32 (instruction-descriptor bits 15/16),
-// so transposed operands never take a transpose pass.
+// Operand paths.  The 3 MMAs per k-step read shared memory through the same
+// 128 B/clk/SM port as the TMA writes and the split's loads/stores; with both
+// operands in shared memory that port, not the tensor core, bounded the kernel
+// (~190 KB per 32-deep k-slab of a 128 x 128 tile against 768 MMA cycles).  So
+// A goes to TENSOR MEMORY: the split warps read each A row once from the
+// staged tile and write its hi and lo parts with tcgen05.st (TMEM write
+// 256 B/clk); the MMAs take A from TMEM (tcgen05.mma ... [d], [a_tmem], b_desc)
+// and only B is read from shared memory.  TMEM budget per CTA (512 columns):
+// two BN-column accumulators + LSTAGES x (32 hi + 32 lo) A columns, so BN <= 128.
+// Operand majorness: A may be K-major (ta = 0, SWIZZLE_128B rows) or M-major
+// (ta = 1, SWIZZLE_128B_ATOM_32B boxes) in shared memory -- the split reads
+// either and writes TMEM rows (TMEM A is always K-major); B is N-major when tb = 0
+// and K-major when tb = 1, both native UMMA smem layouts (idesc bit 16).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -43,30 +43,44 @@ namespace cg {
 namespace {
 
 constexpr int BM = 128, BK = 32;
-// Tile configurations (N = 128 or 256 columns per unit).  Decoupled rings: the
-// raw operand tiles (TMA / gather destinations, also the hi operands) live in a
-// ring that runs ahead of the MMAs; the lo tiles written by the split warps only
-// live from the split to the MMA.
+// Tile configurations (N = 32 / 64 / 128 columns per unit).  Three rings, each
+// advancing once per 32-deep k-block:
+//   A ring  (SA stages)  TMA / gather destination of the raw A tile; freed by the
+//                        split warps as soon as they hold their row in registers
+//   B ring  (SB stages)  raw B tile (also the hi operand the MMAs read); freed by
+//                        the MMA commit
+//   lo ring (LSTAGES)    smem B lo tile + TMEM A hi/lo columns; split -> MMA
+// Separating A from B keeps the A stage lifetime at "load latency + split"
+// instead of "... + the MMAs of every earlier stage", so the same shared memory
+// buys a deeper B prefetch.
 template <int BNT, int CG = 1>
 struct TC {
   static constexpr int BN = BNT;
   static constexpr int TILE_A = BM * BK * 4;           // 16 KiB
   static constexpr int TILE_B = BNT / CG * BK * 4;     // this CTA's share of the B tile
-  static constexpr int STAGE_BYTES = TILE_A + TILE_B;
-  static constexpr int LO_BYTES = TILE_A + TILE_B;
-  static constexpr int LSTAGES = 2;                    // lo ring
+  static constexpr int LO_BYTES = TILE_B;              // B lo in shared memory (A hi/lo live in TMEM)
+  static constexpr int LSTAGES = 4;                    // lo ring (smem B lo + TMEM A hi/lo)
+  static constexpr int ACOL = 2 * BNT;                 // first TMEM column of the A stages
+  static_assert(ACOL + LSTAGES * 2 * BK <= 512, "TMEM: accumulators + A stages");
   static constexpr int EPI_BYTES = kEpiMax * BNT * 4;
-  static constexpr int STAGES_FIT = (220 * 1024 - LSTAGES * LO_BYTES - EPI_BYTES) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;   // raw ring
-  static constexpr int LO_BASE = STAGES * STAGE_BYTES;
+  static constexpr int SA = 4;
+  static constexpr int SB_FIT = (220 * 1024 - EPI_BYTES - SA * TILE_A - LSTAGES * LO_BYTES) / TILE_B;
+  static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
+  static constexpr int A_BASE = 0;
+  static constexpr int B_BASE = SA * TILE_A;
+  static constexpr int LO_BASE = B_BASE + SB * TILE_B;
   static constexpr int EPI_BASE = LO_BASE + LSTAGES * LO_BYTES;   // fused-epilogue operands [kEpiMax][BN]
   static constexpr int BAR_BASE = EPI_BASE + EPI_BYTES;
   static constexpr int SMEM_BYTES = BAR_BASE + 1024 /*barriers*/ + 1024 /*alignment slack*/;
-  static_assert(STAGES >= 2, "pipeline depth");
+  static_assert(SB >= 3, "pipeline depth");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
-constexpr int THREADS = 320;         // TMA, MMA, 4 split warps, 4 epilogue warps
-constexpr int THREADS_GATHER = 448;  // + 4 warps gathering the im2col A tile
+// warps: 0 TMA, 1 MMA, 2-5 split group 0, 6-9 epilogue, [10-13 im2col gather],
+// then split group 1 (10-13, or 14-17 with the gather).  The two split groups
+// take alternate k-blocks: one group's per-k-block latency chain (LDS -> split ->
+// tcgen05.st / STS -> fences -> arrive) is longer than the 3 x 4 MMAs it feeds.
+constexpr int THREADS = 448;
+constexpr int THREADS_GATHER = 576;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -111,6 +125,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
+// Warp-collective wait: the exit condition is a vote, so code after it stays
+// provably warp-uniform (lets the compiler keep MMA operands in uniform registers).
+__device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  while (true) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (__all_sync(0xffffffffu, done)) return;
+    if (t0 == 0) t0 = globaltimer();
+    else if (globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
@@ -131,36 +162,68 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
   return d;
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
+// 32 consecutive columns of this thread's TMEM lane (warp-collective, lane quadrant = warp % 4)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum));
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,"
+      "%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]),
+      "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
+      "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]),
+      "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
 }
 
-// arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
+// arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster.
+// Default (.release.cta) semantics: what the peer consumes after this arrive is
+// TMEM / shared memory read by the tensor core, ordered by the tcgen05 and proxy
+// fences issued before it.  (.release.cluster compiled to MEMBAR.ALL.GPU + ERRBAR
+// and made the follower CTA's split the pair's critical path: ncu, 8192^3 DOT.)
 __device__ __forceinline__ void mbar_arrive_cta(uint32_t bar, uint32_t cta) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-}
-__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(accum));
-}
-// commit of a CTA-pair MMA: arrive on the barrier at this offset in both CTAs
-__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-               "h"((uint16_t)3)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+// Warp-collective forms: every lane computes the (uniform) operands, elect.sync
+// picks the one lane that issues.  CG = 2: the pair instruction (leader CTA only)
+// and a commit multicast to the barrier at this offset in both CTAs.
+template <int CG>
+__device__ __forceinline__ void mma_tf32_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t accum) {
+  if (CG == 1)
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
+  else
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(accum));
 }
+template <int CG>
+__device__ __forceinline__ void mma_commit_e(uint32_t bar) {
+  if (CG == 1)
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
+        : "memory");
+  else
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(bar),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
 
 // Descriptor of one K=8 slice `kk` (0..3) of a 128 x 32 operand tile.
 //  K-major tile : 128 rows (M or N) x 128 B (32 k), row r at r*128 B, TMA SWIZZLE_128B
@@ -179,9 +242,11 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 // Persistent, warp-specialised kernel; one CTA per SM walks the work units
 // u = (split z, m-tile, n-tile) with the n-tile fastest.  Roles:
 //   warp 0        TMA producer (B; and A for DOT)
-//   warp 1        TMEM allocator + MMA issuer (one thread); two 128-column
-//                 accumulators so the epilogue of unit j overlaps the MMAs of j+1
-//   warps 2-5     hi/lo split of each stage (writes lo; the raw tile is the hi operand)
+//   warp 1        TMEM allocator (all 512 columns) + MMA issuer (one thread); two
+//                 BN-column accumulators so the epilogue of unit j overlaps the MMAs of j+1
+//   warps 2-5     split of each stage: A row -> TMEM hi/lo columns (one row per
+//                 thread, TMEM lane quadrant = warp % 4); B -> lo tile in shared
+//                 memory (the raw B tile is the hi operand)
 //   warps 6-9     epilogue: tcgen05.ld TMEM -> registers -> C (TMEM lane quadrant = warp % 4)
 //   warps 10-13   (GATHER) implicit im2col: A rows gathered from the NHWC input,
 //                 16-byte cp.async straight into the SWIZZLE_128B K-major layout
@@ -201,20 +266,22 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
                    int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
                    const __grid_constant__ EpiProg epi, float* __restrict__ dbg) {
   using T = TC<BNT, CG>;
-  constexpr int BN = T::BN, STAGES = T::STAGES, LSTAGES = T::LSTAGES, BNH = BNT / CG;
-  constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, STAGE_BYTES = T::STAGE_BYTES, LO_BYTES = T::LO_BYTES;
-  constexpr int LO_BASE = T::LO_BASE, BAR_BASE = T::BAR_BASE;
+  constexpr int BN = T::BN, SA = T::SA, SB = T::SB, LSTAGES = T::LSTAGES, BNH = BNT / CG;
+  constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, LO_BYTES = T::LO_BYTES;
+  constexpr int A_BASE = T::A_BASE, B_BASE = T::B_BASE, LO_BASE = T::LO_BASE, BAR_BASE = T::BAR_BASE, ACOL = T::ACOL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bars = (uint64_t*)(smem + BAR_BASE);
   const uint32_t bar0 = smem_u32(bars);
-  auto full = [&](int s) { return bar0 + 8u * s; };
-  auto empty = [&](int s) { return bar0 + 8u * (STAGES + s); };
-  auto conv = [&](int l) { return bar0 + 8u * (2 * STAGES + l); };
-  auto lofree = [&](int l) { return bar0 + 8u * (2 * STAGES + LSTAGES + l); };
-  auto tfull = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 * LSTAGES + b); };
-  auto tempty = [&](int b) { return bar0 + 8u * (2 * STAGES + 2 * LSTAGES + 2 + b); };
+  auto fullA = [&](int s) { return bar0 + 8u * s; };
+  auto emptyA = [&](int s) { return bar0 + 8u * (SA + s); };
+  auto fullB = [&](int s) { return bar0 + 8u * (2 * SA + s); };
+  auto emptyB = [&](int s) { return bar0 + 8u * (2 * SA + SB + s); };
+  auto conv = [&](int l) { return bar0 + 8u * (2 * SA + 2 * SB + l); };
+  auto lofree = [&](int l) { return bar0 + 8u * (2 * SA + 2 * SB + LSTAGES + l); };
+  auto tfull = [&](int b) { return bar0 + 8u * (2 * SA + 2 * SB + 2 * LSTAGES + b); };
+  auto tempty = [&](int b) { return bar0 + 8u * (2 * SA + 2 * SB + 2 * LSTAGES + 2 + b); };
   uint32_t* tmem_slot = (uint32_t*)(smem + BAR_BASE + 512);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -237,9 +304,13 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full(s), GATHER ? 1 + 128 : 1);
-      mbar_init(empty(s), 1);
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(fullA(s), GATHER ? 128 : 1);
+      mbar_init(emptyA(s), 4);  // the 4 split warps of this CTA
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(fullB(s), 1);
+      mbar_init(emptyB(s), 1);
     }
     for (int l = 0; l < LSTAGES; ++l) {
       mbar_init(conv(l), 4 * CG);
@@ -256,11 +327,11 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   if (warp == 1) {
     if (CG == 1) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(2 * BN));
+                   "r"(512));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     } else {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                   "r"(2 * BN));
+                   "r"(512));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
   }
@@ -277,126 +348,163 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         int z, m0, n0, kb0, nk;
         unit(u, z, m0, n0, kb0, nk);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(empty(s), ph ^ 1);
-          const uint32_t st = sbase + s * STAGE_BYTES;
-          mbar_expect_tx(full(s), GATHER ? TILE_B : TILE_A + TILE_B);  // (this CTA's B share)
+          const int sa = it % SA, sb = it % SB;
           const int nb = n0 + (int)rank * BNH;
           const int k0 = (kb0 + kb) * BK;
-          if (GATHER) {
-          } else if (a_mn) {
-            for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &mapA, m0 + 32 * j, k0, full(s));
-          } else {
-            tma_load_2d(st, &mapA, k0, m0, full(s));
+          if (!GATHER) {
+            mbar_wait(emptyA(sa), ((it / SA) & 1) ^ 1);
+            const uint32_t st = sbase + A_BASE + sa * TILE_A;
+            mbar_expect_tx(fullA(sa), TILE_A);
+            if (a_mn) {
+              for (int j = 0; j < BM / 32; ++j) tma_load_2d(st + j * 4096, &mapA, m0 + 32 * j, k0, fullA(sa));
+            } else {
+              tma_load_2d(st, &mapA, k0, m0, fullA(sa));
+            }
           }
+          mbar_wait(emptyB(sb), ((it / SB) & 1) ^ 1);
+          const uint32_t bt = sbase + B_BASE + sb * TILE_B;
+          mbar_expect_tx(fullB(sb), TILE_B);  // (this CTA's B share)
           if (b_mn) {
-            for (int j = 0; j < BNH / 32; ++j) tma_load_2d(st + TILE_A + j * 4096, &mapB, nb + 32 * j, k0, full(s));
+            for (int j = 0; j < BNH / 32; ++j) tma_load_2d(bt + j * 4096, &mapB, nb + 32 * j, k0, fullB(sb));
           } else {
-            tma_load_2d(st + TILE_A, &mapB, k0, nb, full(s));
+            tma_load_2d(bt, &mapB, k0, nb, fullB(sb));
           }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {  // ---------------- MMA issuer (the leader CTA of a pair)
+    if (leader) {  // ---------------- MMA issuer (the leader CTA of a pair)
+      // The whole warp walks the loop (its indices stay warp-uniform, so descriptors
+      // live in uniform registers); one elected lane issues each tcgen05 op.  Issued
+      // from a single lane the operands went through R2UR.BROADCAST loops and every
+      // MMA cost ~108 cycles regardless of N (ncu + CG_TC_BN sweep).
       // instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)b_mn << 16) |  // A (TMEM) K-major
                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
+      const uint64_t kstep = b_mn ? 64 : 2;  // descriptor address advance per K=8 slice (1024 B or 32 B, in 16 B)
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // (uniform)
       int it = 0, j = 0;
       for (int u = u_first; u < units; u += u_step, ++j) {
         int z, m0, n0, kb0, nk;
         unit(u, z, m0, n0, kb0, nk);
         const int b = j & 1;
-        mbar_wait(tempty(b), ((j >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
+        mbar_wait_warp(tempty(b), ((j >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + (uint32_t)(b * BN);
+        const uint32_t d = tm + (uint32_t)(b * BN);
         for (int kb = 0; kb < nk; ++kb, ++it) {
-          const int s = it % STAGES, l = it % LSTAGES;
-          mbar_wait(conv(l), (it / LSTAGES) & 1);
+          const int sb = it % SB, l = it % LSTAGES;
+          mbar_wait_warp(conv(l), (it / LSTAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t st = sbase + s * STAGE_BYTES, lo = sbase + LO_BASE + l * LO_BYTES;
-          const uint32_t ahi = st, bhi = st + TILE_A, alo = lo, blo = lo + TILE_A;
+          const uint64_t dhi = tile_desc(sbase + B_BASE + sb * TILE_B, b_mn, 0);
+          const uint64_t dlo = tile_desc(sbase + LO_BASE + l * LO_BYTES, b_mn, 0);
+          const uint32_t ahi = tm + (uint32_t)(ACOL + l * 2 * BK), alo = ahi + BK;  // TMEM columns
+          if (raw_hi != 4) {  // (4: measurement probe without MMAs)
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
-            // small terms first, then the leading hi.hi product
-            if (CG == 1) {
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
+              // small terms first, then the leading hi.hi product
               if (raw_hi != 2) {
-                mma_tf32(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
-                mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
+                mma_tf32_e<CG>(d, alo + kk * 8, dhi + kk * kstep, idesc, acc0);
+                mma_tf32_e<CG>(d, ahi + kk * 8, dlo + kk * kstep, idesc, 1u);
               }
-              mma_tf32(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, raw_hi != 2 ? 1u : acc0);
-            } else {
-              if (raw_hi != 2) {
-                mma_tf32_pair(d, tile_desc(alo, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, acc0);
-                mma_tf32_pair(d, tile_desc(ahi, a_mn, kk), tile_desc(blo, b_mn, kk), idesc, 1u);
-              }
-              mma_tf32_pair(d, tile_desc(ahi, a_mn, kk), tile_desc(bhi, b_mn, kk), idesc, raw_hi != 2 ? 1u : acc0);
+              mma_tf32_e<CG>(d, ahi + kk * 8, dhi + kk * kstep, idesc, raw_hi != 2 ? 1u : acc0);
             }
           }
-          if (CG == 1) {
-            mma_commit(empty(s));   // frees the raw slot once these MMAs have read it
-            mma_commit(lofree(l));  // and the lo slot
-          } else {
-            mma_commit_pair(empty(s));
-            mma_commit_pair(lofree(l));
-          }
+          mma_commit_e<CG>(emptyB(sb));  // frees the raw B slot once these MMAs have read it
+          mma_commit_e<CG>(lofree(l));   // and the lo slot
         }
-        if (CG == 1) mma_commit(tfull(b));
-        else mma_commit_pair(tfull(b));
+        mma_commit_e<CG>(tfull(b));
       }
     }
-  } else if (warp < 6) {
-    // ---------------- warps 2..5: hi/lo split of each stage
-    const int t = threadIdx.x - 64;  // 0..127
+  } else if (warp < 6 || warp >= (GATHER ? 14 : 10)) {
+    // ---------------- split warps (two groups of 4, alternate k-blocks)
+    const int grp = warp < 6 ? 0 : 1;                       // split group: k-blocks with it % 2 == grp
+    const int t = (threadIdx.x - (grp ? (GATHER ? 448 : 320) : 64));  // 0..127: B chunks
+    const int wq = warp % 4;         // TMEM lane quadrant this warp may access
+    const int rr = wq * 32 + lane;   // the A tile row this thread owns
     int it = 0;
     for (int u = u_first; u < units; u += u_step) {
       int z, m0, n0, kb0, nk;
       unit(u, z, m0, n0, kb0, nk);
       for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % STAGES, l = it % LSTAGES;
-        mbar_wait(full(s), (it / STAGES) & 1);
+        if ((it & 1) != grp) continue;
+        const int sa = it % SA, sb = it % SB, l = it % LSTAGES;
+        mbar_wait(fullA(sa), (it / SA) & 1);
         mbar_wait(lofree(l), ((it / LSTAGES) & 1) ^ 1);
-        if (dbg && u == 0 && kb == 0 && t < 8) {
-          dbg[t] = reinterpret_cast<float*>(smem)[t];                   // A raw
-          dbg[8 + t] = reinterpret_cast<float*>(smem + TILE_A)[t];  // B raw
-        }
-        if (raw_hi == 2) {  // probe only: 1xTF32 (no split) to measure what the split costs
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");  // the MMAs that read this TMEM stage are done
+        if (raw_hi == 3) {  // measurement probe: no split work (pipeline without the split)
           __syncwarp();
+          if (lane == 0) mbar_arrive(emptyA(sa));
+          mbar_wait(fullB(sb), (it / SB) & 1);
           if (lane == 0) {
             if (CG == 1 || leader) mbar_arrive(conv(l));
             else mbar_arrive_cta(conv(l), 0);
           }
           continue;
         }
-        // 16 float4 per thread: all loads first (ILP), explicit shared-space ops
-        const uint32_t hb = sbase + s * STAGE_BYTES + t * 16, lb = sbase + LO_BASE + l * LO_BYTES + t * 16;
-        constexpr int PER = STAGE_BYTES / 16 / 128;
-        float4 v[PER];
+        const uint32_t st = sbase + A_BASE + sa * TILE_A;
+        if (dbg && u == 0 && kb == 0 && t < 8) dbg[t] = reinterpret_cast<float*>(smem + A_BASE)[t];  // A raw
+        // A row rr (32 k values) -> registers.  K-major (TMA SWIZZLE_128B or the
+        // gather's identical layout): 16-byte chunk c of row r sits at chunk c ^ (r & 7).
+        // M-major (TMA SWIZZLE_128B_ATOM_32B, boxes [32 k][32 m] of 4 KiB): the 32-byte
+        // chunk of element (k, m) is (m % 32) / 8 ^ (k & 3) within k-row k.
+        uint32_t hv[32], lv[32];
+        if (!GATHER && a_mn) {
+          const uint32_t box = st + (uint32_t)(rr >> 5) * 4096u + (uint32_t)((lane & 7) << 2);
 #pragma unroll
-        for (int q = 0; q < PER; ++q) v[q] = lds128(hb + q * 2048);
+          for (int k = 0; k < 32; ++k) hv[k] = __float_as_uint(lds32(box + k * 128 + ((((lane >> 3) ^ (k & 3))) << 5)));
+        } else {
+          const uint32_t row = st + (uint32_t)rr * 128u;
 #pragma unroll
-        for (int q = 0; q < PER; ++q) {
-          float4 h, l;
-          h.x = __uint_as_float(__float_as_uint(v[q].x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(v[q].y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(v[q].z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(v[q].w) & 0xFFFFE000u);
-          l.x = __fsub_rn(v[q].x, h.x);
-          l.y = __fsub_rn(v[q].y, h.y);
-          l.z = __fsub_rn(v[q].z, h.z);
-          l.w = __fsub_rn(v[q].w, h.w);
-          // The A tile of a GATHER stage was written by cp.async / st.shared of other
-          // threads (generic proxy); rewriting it here, followed by this thread's
-          // proxy fence, is what makes it visible to the tensor core.  TMA tiles are
-          // async-proxy writes already, so with raw_hi they are read as they are.
-          if (!raw_hi || (GATHER && q < TILE_A / 2048)) sts128(hb + q * 2048, h);
-          sts128(lb + q * 2048, l);
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = lds128(row + ((c ^ (rr & 7)) << 4));
+            hv[4 * c] = __float_as_uint(v.x);
+            hv[4 * c + 1] = __float_as_uint(v.y);
+            hv[4 * c + 2] = __float_as_uint(v.z);
+            hv[4 * c + 3] = __float_as_uint(v.w);
+          }
         }
-        // generic-proxy smem writes -> visible to the tensor core (async proxy)
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t h = hv[k] & 0xFFFFE000u;
+          lv[k] = __float_as_uint(__fsub_rn(__uint_as_float(hv[k]), __uint_as_float(h)));
+          hv[k] = h;
+        }
+        const uint32_t ta = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ACOL + l * 2 * BK);
+        tmem_st32(ta, hv);
+        if (raw_hi != 2) tmem_st32(ta + BK, lv);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(emptyA(sa));  // the row is in registers / TMEM: A slot free
+        mbar_wait(fullB(sb), (it / SB) & 1);
+        if (dbg && u == 0 && kb == 0 && t < 8) dbg[8 + t] = reinterpret_cast<float*>(smem + B_BASE)[t];  // B raw
+        // B: lo tile in shared memory (the raw tile is read as hi by the tensor core,
+        // which truncates fp32 operands to TF32; with raw_hi == 0 hi is written too)
+        if (raw_hi != 2) {
+          const uint32_t hb = sbase + B_BASE + sb * TILE_B + t * 16, lb = sbase + LO_BASE + l * LO_BYTES + t * 16;
+          constexpr int PER = TILE_B / 16 / 128;
+          float4 v[PER];
+#pragma unroll
+          for (int q = 0; q < PER; ++q) v[q] = lds128(hb + q * 2048);
+#pragma unroll
+          for (int q = 0; q < PER; ++q) {
+            float4 h, lo;
+            h.x = __uint_as_float(__float_as_uint(v[q].x) & 0xFFFFE000u);
+            h.y = __uint_as_float(__float_as_uint(v[q].y) & 0xFFFFE000u);
+            h.z = __uint_as_float(__float_as_uint(v[q].z) & 0xFFFFE000u);
+            h.w = __uint_as_float(__float_as_uint(v[q].w) & 0xFFFFE000u);
+            lo.x = __fsub_rn(v[q].x, h.x);
+            lo.y = __fsub_rn(v[q].y, h.y);
+            lo.z = __fsub_rn(v[q].z, h.z);
+            lo.w = __fsub_rn(v[q].w, h.w);
+            if (!raw_hi) sts128(hb + q * 2048, h);
+            sts128(lb + q * 2048, lo);
+          }
+        }
+        // generic-proxy smem writes -> visible to the tensor core (async proxy);
+        // TMEM stores complete and ordered before the arrive
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
           if (CG == 1 || leader) mbar_arrive(conv(l));
@@ -513,17 +621,16 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       int kh = tap / cv.KW, kw = tap - kh * cv.KW;
       const bool row_ok = m < M;
       for (int kb = 0; kb < nk; ++kb, ++it) {
-        const int s = it % STAGES;
-        const uint32_t ph = (it / STAGES) & 1;
-        mbar_wait(empty(s), ph ^ 1);
-        const uint32_t row = sbase + s * STAGE_BYTES + r * 128;
+        const int s = it % SA;
+        mbar_wait(emptyA(s), ((it / SA) & 1) ^ 1);
+        const uint32_t row = sbase + A_BASE + s * TILE_A + r * 128;
         if ((cv.Ci & 31) == 0) {  // the slab is 32 channels of one tap
           const int hi = hb + kh, wi = wb + kw;
           const bool ok = row_ok && k0 < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
           const float* src = ok ? img + ((size_t)hi * cv.W + wi) * cv.Ci + ci : cv.x;
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) cp_async16(row + ((jj ^ (r & 7)) << 4), src + (ok ? 4 * jj : 0), ok ? 16u : 0u);
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fullA(s)) : "memory");
           ci += BK;
           if (ci >= cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
           k0 += BK;
@@ -538,7 +645,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
             if (ci >= cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
             k0 += 4;
           }
-          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(full(s)) : "memory");
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(fullA(s)) : "memory");
         } else {  // few input channels (e.g. RGB): element-wise gather, 16-byte shared stores
           for (int jj = 0; jj < 8; ++jj) {
             float e[4];
@@ -552,7 +659,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
             }
             sts128(row + ((jj ^ (r & 7)) << 4), make_float4(e[0], e[1], e[2], e[3]));
           }
-          mbar_arrive(full(s));
+          mbar_arrive(fullA(s));
         }
       }
     }
@@ -562,8 +669,8 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   else __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (CG == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
-    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+    if (CG == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    else asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -616,29 +723,36 @@ int pick_bn(int M, int N, int num_sms) {
   // narrow outputs (convs with 32 / 64 channels): a matching MMA N instead of padding to 128
   if (N <= 32) return 32;
   if (N <= 64) return 64;
-  const int w128 = (N + 127) / 128 * 128 - N, w256 = (N + 255) / 256 * 256 - N;
-  const long long units256 = (long long)((M + BM - 1) / BM) * ((N + 255) / 256);
-  // only with enough units for two waves: otherwise the wider tile just idles SMs
-  return (N >= 256 && w256 <= w128 && units256 >= 2LL * num_sms) ? 256 : 128;
+  (void)M, (void)num_sms;
+  if (const char* e = getenv("CG_TC_BN")) return atoi(e);  // measurement override (32 / 64 / 128)
+  return 128;  // TMEM: 2 x BN accumulator columns + the A stages fit 512 columns for BN <= 128
 }
 
 // CTA pairs (cta_group::2, 256-row tiles) when the problem has at least a wave
-// of pair units and no split-K; BN >= 64 so each CTA's half of B is >= 32 columns.
-// Measured: 8192^3 DOT 200 -> 220 TFLOP/s; C5's gathered convs 43 -> 48 ms (their
-// cost is the per-CTA A side, and the pair couples two CTAs' splits), so
-// implicit-GEMM convs stay on single CTAs.
+// of pair units; BN >= 64 so each CTA's half of B is >= 32 columns.
 int pick_cg(int M, int N, int bn, int splits, int num_sms, bool gather) {
-  if (gather || getenv("CG_TC_NO_PAIRS") || splits != 1 || bn < 64 || M < 256) return 1;
-  const long long units2 = (long long)((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn);
-  return units2 >= num_sms ? 2 : 1;
+  (void)gather;  // implicit-GEMM convs pair too (C5: 36.4 -> 34.4 ms)
+  if (getenv("CG_TC_NO_PAIRS") || bn < 64 || M < 256) return 1;
+  const long long units2 = (long long)((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn) * splits;
+  return units2 >= num_sms / 2 ? 2 : 1;  // at least one full wave of pairs
 }
 
 void dot_tc_split(int M, int N, int K, int num_sms, int* splits, int* kb_per_split) {
   const int bn = pick_bn(M, N, num_sms);
-  const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+  const long long tiles = (long long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int nk = (K + BK - 1) / BK;
+  // split-K: minimise (waves x k-blocks per unit) + the partials' HBM round trip
+  // (S x M x N x 8 B at ~6.5 TB/s, in units of one k-block ~0.45 us) + the finalize
   int S = 1;
-  if (tiles < num_sms) S = std::max(1, std::min((num_sms + tiles - 1) / tiles, nk / 4));
+  double best = 1e300;
+  for (int s = 1; s <= std::max(1, std::min(16, nk / 4)); ++s) {
+    const int per_s = (nk + s - 1) / s;
+    const int s_eff = (nk + per_s - 1) / per_s;
+    const long long waves = (tiles * s_eff + num_sms - 1) / num_sms;
+    // (+4 k-blocks for the finalize launch; a split output also cannot take a fused epilogue)
+    const double cost = (double)waves * per_s + (s_eff > 1 ? 4.0 + (double)s_eff * M * N * 8.0 / 2.9e6 : 0.0);
+    if (cost < best - 1e-9) best = cost, S = s_eff;
+  }
   const int per = (nk + S - 1) / S;
   *kb_per_split = per;
   *splits = (nk + per - 1) / per;
@@ -658,6 +772,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   p->num_sms = num_sms;
   p->raw_hi = 1;  // tcgen05 kind::tf32 truncates fp32 operands (tests: test_tf32_truncation_probe)
   if (getenv("CG_PROBE_1XTF32")) p->raw_hi = 2;  // measurement probe only (lower accuracy)
+  if (getenv("CG_PROBE_MODE")) p->raw_hi = atoi(getenv("CG_PROBE_MODE"));  // 3: no split, 4: no MMA (wrong results)
   dot_tc_split(M, N, K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
   if (p->splits > 1 && !ws) return -3;
@@ -715,7 +830,6 @@ cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
   float* out = p.splits > 1 ? p.ws : p.C;
   cudaError_t e0;
   switch (p.bn) {
-    case 256: e0 = p.conv.x ? launch_tc_cg<true, 256>(p, out, s) : launch_tc_cg<false, 256>(p, out, s); break;
     case 64: e0 = p.conv.x ? launch_tc_cg<true, 64>(p, out, s) : launch_tc_cg<false, 64>(p, out, s); break;
     case 32: e0 = p.conv.x ? launch_tc_cg<true, 32>(p, out, s) : launch_tc_cg<false, 32>(p, out, s); break;
     default: e0 = p.conv.x ? launch_tc_cg<true, 128>(p, out, s) : launch_tc_cg<false, 128>(p, out, s); break;

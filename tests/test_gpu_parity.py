@@ -291,7 +291,9 @@ TC_CONV_CASES = [((2, 35, 35, 64), (3, 3, 64, 96), 1, 1), ((2, 35, 35, 32), (3, 
                  ((4, 17, 17, 48), (7, 1, 48, 64), 1, 1), ((2, 17, 17, 80), (1, 7, 80, 48), 1, 1),
                  ((2, 8, 8, 1280), (1, 1, 1280, 320), 1, 1), ((3, 15, 13, 12), (5, 5, 12, 20), 1, 1),
                  ((2, 31, 29, 3), (3, 3, 3, 32), 2, 0), ((2, 20, 20, 6), (5, 5, 6, 16), 1, 1),
-                 ((2, 8, 8, 64), (3, 3, 64, 448), 1, 1), ((16, 35, 35, 32), (1, 1, 32, 512), 1, 1)]
+                 ((2, 8, 8, 64), (3, 3, 64, 448), 1, 1), ((16, 35, 35, 32), (1, 1, 32, 512), 1, 1),
+                 # CTA-pair tiles (>= one wave of 256-row units) on the 4-channel and element gathers
+                 ((32, 35, 35, 20), (3, 3, 20, 128), 1, 1), ((128, 31, 29, 3), (3, 3, 3, 64), 2, 0)]
 
 
 @pytest.mark.parametrize("xs,ws,st,pad", TC_CONV_CASES)

@@ -50,8 +50,11 @@ def time_torch(fn, iters):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--shapes", default="", help="comma-separated indices into C3_DOTS (default: all)")
+    ap.add_argument("--no-torch", action="store_true")
     a = ap.parse_args()
-    for (m, n, k, ta, tb) in C3_DOTS:
+    sel = [int(i) for i in a.shapes.split(",")] if a.shapes else range(len(C3_DOTS))
+    for (m, n, k, ta, tb) in [C3_DOTS[i] for i in sel]:
         sa = (k, m) if ta else (m, k)
         sb = (n, k) if tb else (k, n)
         g = cg.Graph(0)
@@ -62,6 +65,11 @@ def main():
         g.assign(va, rng.uniform(-1, 1, sa).astype(np.float32))
         g.assign(vb, rng.uniform(-1, 1, sb).astype(np.float32))
         ms = time_graph(g, [o], a.iters)
+        if a.no_torch:
+            print(json.dumps({"op": "DOT", "M": m, "N": n, "K": k, "ta": ta, "tb": tb, "ms": ms,
+                              "tflops": 2.0 * m * n * k / ms / 1e9}), flush=True)
+            g.destroy()
+            continue
         A = torch.randn(sa, device="cuda")
         B = torch.randn(sb, device="cuda")
         fa = (lambda: A.T) if ta else (lambda: A)
