@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "conv_small.h"
 #include "kernels.h"
@@ -232,10 +233,11 @@ struct RtGeom {
 
 template <int COP, int KS, int PX, bool FLIP>
 __global__ void __launch_bounds__(256) conv_rt_kernel(const float* __restrict__ x, const float* __restrict__ w,
-                                                      float* __restrict__ y, RtGeom g) {
+                                                      float* __restrict__ y, RtGeom g, int IMG) {
   extern __shared__ float sm[];
   float* ws = sm;                                  // [KS*KS*cin][COP]
-  float* xs = sm + KS * KS * g.cin * COP;          // [cin][Hp][Wp]
+  float* xs = sm + KS * KS * g.cin * COP;          // IMG x [cin][Hp][Wp]
+  const int IS = g.cin * g.Hp * g.Wp;
   for (int e = threadIdx.x; e < KS * KS * g.cin * COP; e += blockDim.x) {
     const int co = e % COP, r = e / COP, ci = r % g.cin, tap = r / g.cin;
     float v = 0.f;
@@ -250,19 +252,38 @@ __global__ void __launch_bounds__(256) conv_rt_kernel(const float* __restrict__ 
     }
     ws[e] = v;
   }
-  const int WQ = (g.wout + PX - 1) / PX, items = g.hout * WQ;
-  const int img = g.hin * g.win * g.cin;
-  for (int n = blockIdx.x; n < g.n; n += gridDim.x) {
+  // the padding of every image buffer stays zero: only interiors are rewritten per batch
+  for (int e = threadIdx.x; e < IMG * IS; e += blockDim.x) xs[e] = 0.f;
+  const int per = g.hout * ((g.wout + PX - 1) / PX);
+  const int isz = g.hin * g.win * g.cin;
+  for (int n0 = blockIdx.x * IMG; n0 < g.n; n0 += gridDim.x * IMG) {
+    const int nimg = min(IMG, g.n - n0);
     __syncthreads();
-    const float* xi = x + (size_t)n * img;
-    for (int e = threadIdx.x; e < g.cin * g.Hp * g.Wp; e += blockDim.x) {
-      const int wp = e % g.Wp, q = e / g.Wp, hp = q % g.Hp, c = q / g.Hp;
-      const int h = hp - g.pt, ww = wp - g.pl;
-      xs[e] = (h >= 0 && h < g.hin && ww >= 0 && ww < g.win) ? __ldg(xi + ((size_t)h * g.win + ww) * g.cin + c) : 0.f;
+    // interiors of nimg consecutive images: one contiguous NHWC run, 8 loads in flight
+    const float* src = x + (size_t)n0 * isz;
+    const int tot = nimg * isz;
+    for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * 256) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 256;
+        v[u] = e < tot ? __ldg(src + e) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + u * 256;
+        if (e < tot) {
+          const int c = e % g.cin, q = e / g.cin, ww = q % g.win, q2 = q / g.win, h = q2 % g.hin, im = q2 / g.hin;
+          xs[im * IS + (c * g.Hp + h + g.pt) * g.Wp + ww + g.pl] = v[u];
+        }
+      }
     }
     __syncthreads();
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
-      const int ho = it / WQ, wo0 = (it - ho * WQ) * PX;
+    // item order: output row fastest, then image, then pixel quad, so a warp's
+    // sliding windows start Wp (odd) words apart: conflict-free shared loads
+    for (int it = threadIdx.x; it < nimg * per; it += blockDim.x) {
+      const int ho = it % g.hout, r2 = it / g.hout, im = r2 % nimg, wo0 = (r2 / nimg) * PX;
+      const float* xi = xs + im * IS;
       float acc[PX][COP];
 #pragma unroll
       for (int p = 0; p < PX; ++p)
@@ -271,7 +292,7 @@ __global__ void __launch_bounds__(256) conv_rt_kernel(const float* __restrict__ 
       for (int ci = 0; ci < g.cin; ++ci) {
 #pragma unroll
         for (int kh = 0; kh < KS; ++kh) {
-          const float* xr = xs + ((size_t)ci * g.Hp + ho + kh) * g.Wp + wo0;
+          const float* xr = xi + ((size_t)ci * g.Hp + ho + kh) * g.Wp + wo0;
           float xv[PX + KS - 1];
 #pragma unroll
           for (int q = 0; q < PX + KS - 1; ++q) xv[q] = xr[q];
@@ -296,7 +317,7 @@ __global__ void __launch_bounds__(256) conv_rt_kernel(const float* __restrict__ 
 #pragma unroll
       for (int p = 0; p < PX; ++p) {
         if (wo0 + p >= g.wout) break;
-        float* yp = y + (((size_t)n * g.hout + ho) * g.wout + wo0 + p) * g.cout;
+        float* yp = y + (((size_t)(n0 + im) * g.hout + ho) * g.wout + wo0 + p) * g.cout;
 #pragma unroll
         for (int c = 0; c < COP; ++c)
           if (c < g.cout) yp[c] = acc[p][c];
@@ -421,7 +442,7 @@ RtGeom rt_geom_fwd(const ConvGeom& g) {
   r.hout = g.ho; r.wout = g.wo; r.cout = g.co;
   r.pt = g.pt; r.pl = g.pl; r.wcin = g.ci; r.wcout = g.co;
   r.Hp = g.ho + g.kh - 1;
-  r.Wp = (g.wo + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1;
+  r.Wp = ((g.wo + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1) | 1;  // odd row pitch (bank spread)
   return r;
 }
 RtGeom rt_geom_bwdin(const ConvGeom& g) {
@@ -430,26 +451,36 @@ RtGeom rt_geom_bwdin(const ConvGeom& g) {
   r.hout = g.h; r.wout = g.w; r.cout = g.ci;
   r.pt = g.kh - 1 - g.pt; r.pl = g.kw - 1 - g.pl; r.wcin = g.ci; r.wcout = g.co;
   r.Hp = g.h + g.kh - 1;
-  r.Wp = (g.w + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1;
+  r.Wp = ((g.w + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1) | 1;
   return r;
-}
-size_t rt_smem(const RtGeom& r, int cop, int ks) {
-  return ((size_t)ks * ks * r.cin * cop + (size_t)r.cin * r.Hp * r.Wp) * 4;
 }
 bool rt_ok(const ConvGeom& g) {  // stride 1, square 5x5 or 3x3 taps
   return g.sh == 1 && g.sw == 1 && g.kh == g.kw && (g.kh == 5 || g.kh == 3);
 }
 
+// images per block iteration: enough work items for the block (>= 2 per thread)
+// within the shared-memory budget
+constexpr size_t RT_SMEM = 110 * 1024;
+int rt_img(const RtGeom& r, int cop, int ks) {
+  const size_t wbytes = (size_t)ks * ks * r.cin * cop * 4, ibytes = (size_t)r.cin * r.Hp * r.Wp * 4;
+  if (wbytes + ibytes > RT_SMEM) return 0;
+  const int per = r.hout * ((r.wout + RT_PX - 1) / RT_PX);
+  const int want = std::max(1, (256 + per - 1) / per);  // one item per thread; several blocks per SM
+  return (int)std::max<size_t>(1, std::min<size_t>(want, (RT_SMEM - wbytes) / ibytes));
+}
+
 template <int COP, bool FLIP>
 cudaError_t launch_rt(const float* x, const float* w, float* y, const RtGeom& r, int ks, int num_sms, cudaStream_t s) {
-  const size_t smem = rt_smem(r, COP, ks);
-  const int grid = std::min(r.n, num_sms * 4);
+  const int IMG = rt_img(r, COP, ks);
+  const size_t smem = ((size_t)ks * ks * r.cin * COP + (size_t)IMG * r.cin * r.Hp * r.Wp) * 4;
+  const int bps = std::max(1, std::min(4, (int)((224 * 1024) / (smem + 1024))));
+  const int grid = std::max(1, std::min((r.n + IMG - 1) / IMG, num_sms * bps));
   if (ks == 5) {
-    set_smem(conv_rt_kernel<COP, 5, RT_PX, FLIP>);
-    conv_rt_kernel<COP, 5, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r);
+    cudaFuncSetAttribute(conv_rt_kernel<COP, 5, RT_PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
+    conv_rt_kernel<COP, 5, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
   } else {
-    set_smem(conv_rt_kernel<COP, 3, RT_PX, FLIP>);
-    conv_rt_kernel<COP, 3, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r);
+    cudaFuncSetAttribute(conv_rt_kernel<COP, 3, RT_PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
+    conv_rt_kernel<COP, 3, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
   }
   return cudaGetLastError();
 }
@@ -489,11 +520,12 @@ size_t conv_small_bwdk_ws(const ConvGeom& g, int num_sms) {
 
 cudaError_t launch_conv_small_fwd(const float* x, const float* w, float* y, const ConvGeom& g, int num_sms,
                                   cudaStream_t s) {
-  // register tiling pays for <= 8 output channels (C4 conv1: 248 vs 319 us); at 16
-  // channels its 128 registers cost more occupancy than it saves (440 vs 293 us)
-  if (rt_ok(g) && co_pad(g.co) == 8) {
+  // register tiling over 4 pixels x all (padded) output channels, several images per block
+  if (rt_ok(g) && !getenv("CG_CONV_NO_RT")) {
     const RtGeom r = rt_geom_fwd(g);
-    if (rt_smem(r, 8, g.kh) <= SMEM_LIMIT) return launch_rt<8, false>(x, w, y, r, g.kh, num_sms, s);
+    // (<= 8 channels only: at 16 the 128 registers per thread cost more occupancy than the
+    // tiling saves -- C4 conv2: 320 us vs 291 us for conv_fwd_img)
+    if (co_pad(g.co) == 8 && rt_img(r, 8, g.kh)) return launch_rt<8, false>(x, w, y, r, g.kh, num_sms, s);
   }
   Pads p = pads(g);
   const int Hp = std::max(p.Hp, g.h + g.pt), Wp = std::max(p.Wp, g.w + g.pl);
@@ -514,12 +546,11 @@ cudaError_t launch_conv_small_fwd(const float* x, const float* w, float* y, cons
 
 cudaError_t launch_conv_small_bwdin(const float* dy, const float* w, float* dx, const ConvGeom& g, int num_sms,
                                     cudaStream_t s) {
-  // (the register-tiled transposed correlation, launch_rt<., true>, measured slower on
-  // C4's 16->6-channel backward-input: 738 vs 429 us; kept for geometries with
-  // at most 8 input-side channels of dy)
-  if (rt_ok(g) && co_pad(g.ci) == 8 && g.co <= 8) {
+  // register-tiled transposed correlation (several images per block): C4's
+  // 16 -> 6-channel backward-input 366 us vs 427 us for conv_bwdin_img
+  if (rt_ok(g) && co_pad(g.ci) == 8 && g.co <= 16 && !getenv("CG_CONV_NO_RT")) {
     const RtGeom r = rt_geom_bwdin(g);
-    if (rt_smem(r, 8, g.kh) <= SMEM_LIMIT) return launch_rt<8, true>(dy, w, dx, r, g.kh, num_sms, s);
+    if (rt_img(r, 8, g.kh)) return launch_rt<8, true>(dy, w, dx, r, g.kh, num_sms, s);
   }
   const size_t smem = bwdin_smem(g);
   const int grid = std::min(g.n, num_sms * 8);

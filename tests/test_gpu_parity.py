@@ -353,13 +353,24 @@ def test_maxpool_bwd_tiled_exact():
 
 
 @pytest.mark.parametrize("k,s,pad", [(2, 2, 0), (3, 2, 0), (3, 1, 1), (3, 2, 1), (8, 8, 0)])
-@pytest.mark.parametrize("c", [4, 12])
+@pytest.mark.parametrize("c", [4, 12, 32, 96])
 def test_pools_channel_vectorised(k, s, pad, c):
     """C % 4 == 0: the float4-over-channels pool kernels (C5's pools)."""
     a = {"kh": k, "kw": k, "sh": s, "sw": s, "pad": pad}
     got, ref = _run_single("MAXPOOL2D", [(2, 17, 16, c)], a, -3, 4)
     assert np.array_equal(got, ref)
     got, ref = _run_single("AVGPOOL2D", [(2, 17, 16, c)], a, -3, 4)
+    assert normwise(got, ref) <= 1e-6
+
+
+@pytest.mark.parametrize("shape,s,pad", [((1, 9, 147, 64), 2, 0), ((3, 35, 35, 288), 1, 1), ((2, 17, 17, 768), 2, 0),
+                                         ((2, 8, 8, 1280), 1, 1)])
+def test_pools_c5_shapes(shape, s, pad):
+    """C5's 3x3 pools (stride 2 VALID max, stride 1 SAME average) at their widths."""
+    a = {"kh": 3, "kw": 3, "sh": s, "sw": s, "pad": pad}
+    got, ref = _run_single("MAXPOOL2D", [shape], a, -3, 4)
+    assert np.array_equal(got, ref)
+    got, ref = _run_single("AVGPOOL2D", [shape], a, -3, 4)
     assert normwise(got, ref) <= 1e-6
 
 
