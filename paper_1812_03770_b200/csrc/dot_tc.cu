@@ -53,7 +53,7 @@ constexpr int BM = 128, BK = 32;
 // Separating A from B keeps the A stage lifetime at "load latency + split"
 // instead of "... + the MMAs of every earlier stage", so the same shared memory
 // buys a deeper B prefetch.
-template <int BNT, int CG = 1>
+template <int BNT, int CG = 1, bool GATHER = false>
 struct TC {
   static constexpr int BN = BNT;
   static constexpr int TILE_A = BM * BK * 4;           // 16 KiB
@@ -63,7 +63,10 @@ struct TC {
   static constexpr int ACOL = 2 * BNT;                 // first TMEM column of the A stages
   static_assert(ACOL + LSTAGES * 2 * BK <= 512, "TMEM: accumulators + A stages");
   static constexpr int EPI_BYTES = kEpiMax * BNT * 4;
-  static constexpr int SA = 4;
+  // im2col-gathered A tiles are cp.async loads with a long L2 latency: a deeper A ring
+  static constexpr int SA_WANT = GATHER ? 8 : 4;
+  static constexpr int SA_FIT = (220 * 1024 - EPI_BYTES - LSTAGES * LO_BYTES - 3 * TILE_B) / TILE_A;
+  static constexpr int SA = SA_FIT < SA_WANT ? SA_FIT : SA_WANT;
   static constexpr int SB_FIT = (220 * 1024 - EPI_BYTES - SA * TILE_A - LSTAGES * LO_BYTES) / TILE_B;
   static constexpr int SB = SB_FIT > 8 ? 8 : SB_FIT;
   static constexpr int A_BASE = 0;
@@ -72,7 +75,7 @@ struct TC {
   static constexpr int EPI_BASE = LO_BASE + LSTAGES * LO_BYTES;   // fused-epilogue operands [kEpiMax][BN]
   static constexpr int BAR_BASE = EPI_BASE + EPI_BYTES;
   static constexpr int SMEM_BYTES = BAR_BASE + 1024 /*barriers*/ + 1024 /*alignment slack*/;
-  static_assert(SB >= 3, "pipeline depth");
+  static_assert(SA >= 4 && SB >= 3, "pipeline depth");
   static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 // warps: 0 TMA, 1 MMA, 2-5 split group 0, 6-9 epilogue, [10-13 im2col gather],
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                    int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
                    const __grid_constant__ EpiProg epi, float* __restrict__ dbg) {
-  using T = TC<BNT, CG>;
+  using T = TC<BNT, CG, GATHER>;
   constexpr int BN = T::BN, SA = T::SA, SB = T::SB, LSTAGES = T::LSTAGES, BNH = BNT / CG;
   constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, LO_BYTES = T::LO_BYTES;
   constexpr int A_BASE = T::A_BASE, B_BASE = T::B_BASE, LO_BASE = T::LO_BASE, BAR_BASE = T::BAR_BASE, ACOL = T::ACOL;
@@ -624,6 +627,10 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         const int s = it % SA;
         mbar_wait(emptyA(s), ((it / SA) & 1) ^ 1);
         const uint32_t row = sbase + A_BASE + s * TILE_A + r * 128;
+        if (raw_hi == 5) {  // measurement probe: no gather (stale A tile)
+          mbar_arrive(fullA(s));
+          continue;
+        }
         if ((cv.Ci & 31) == 0) {  // the slab is 32 channels of one tap
           const int hi = hb + kh, wi = wb + kw;
           const bool ok = row_ok && k0 < K && hi >= 0 && hi < cv.H && wi >= 0 && wi < cv.W;
@@ -791,7 +798,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
 
 template <bool G, int BNT, int CG>
 cudaError_t launch_tc(const DotTcPlan& p, float* out, cudaStream_t s) {
-  using T = TC<BNT, CG>;
+  using T = TC<BNT, CG, G>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -850,6 +857,7 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   p->M = (int)M; p->N = co; p->K = kh * kw * ci;
   p->num_sms = num_sms;
   p->raw_hi = getenv("CG_PROBE_1XTF32") ? 2 : 1;
+  if (getenv("CG_PROBE_MODE")) p->raw_hi = atoi(getenv("CG_PROBE_MODE"));  // 3 no split, 4 no MMA, 5 no gather
   dot_tc_split(p->M, p->N, p->K, num_sms, &p->splits, &p->kb_per_split);
   p->ws = ws;
   if (p->splits > 1 && !ws) return -3;

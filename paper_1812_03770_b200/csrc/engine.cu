@@ -439,6 +439,19 @@ static int build_launches(cg_graph* g) {
         static const bool prefer_tc = getenv("CG_CONV_PREFER_TC") != nullptr;  // A/B measurement switch
         if (conv_small_fwd_ok(cgm) && cgm.co <= 16 && !prefer_tc) {  // few channels: whole images in shared memory
           L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
+        } else if (cgm.kh == 1 && cgm.kw == 1 && cgm.sh == 1 && cgm.sw == 1 && cgm.pt == 0 && cgm.pl == 0 &&
+                   (long long)cgm.n * cgm.h * cgm.w <= INT32_MAX &&
+                   conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo) &&
+                   dot_tc_supported((int)((long long)cgm.n * cgm.h * cgm.w), cgm.co, cgm.ci, 0, 0) &&
+                   !getenv("CG_DEBUG_CONV_SIMT") && !getenv("CG_CONV_1X1_GATHER")) {
+          // pointwise conv = DOT of x viewed as [N*H*W, Ci] with w as [Ci, Co]: plain TMA
+          // tiles, no im2col gather
+          const int M = (int)((long long)cgm.n * cgm.h * cgm.w);
+          auto plan = std::make_shared<DotTcPlan>();
+          if (dot_tc_prepare(plan.get(), x, w, out, M, cgm.co, cgm.ci, 0, 0, g->ws, sms) != 0)
+            return g->fail(CG_E_CUDA, "CONV2D node " + std::to_string(G.sink) + ": tensor-core plan failed");
+          g->tcplan[gi] = plan;
+          L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, plan->splits > 1 ? 2 : 1});
         } else if (conv_tc_supported(cgm.ci, cgm.co, (long long)cgm.n * cgm.ho * cgm.wo) &&
                    !getenv("CG_DEBUG_CONV_SIMT")) {  // tcgen05 implicit GEMM
           auto plan = std::make_shared<DotTcPlan>();

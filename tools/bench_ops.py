@@ -20,6 +20,32 @@ C3_DOTS = [  # (M, N, K, ta, tb) of the C3 training step, batch 4096
     (1024, 1024, 4096, 1, 0), (4096, 1024, 1024, 0, 1), (8192, 8192, 8192, 0, 0)]
 
 
+C5_CONVS = [  # (N, H, W, Ci, KH, KW, Co, stride, pad) of InceptionV3 at batch 256 (pad 1 = SAME)
+    (256, 35, 35, 288, 1, 1, 64, 1, 1), (256, 35, 35, 64, 3, 3, 96, 1, 1), (256, 35, 35, 48, 5, 5, 64, 1, 1),
+    (256, 17, 17, 768, 1, 1, 192, 1, 1), (256, 17, 17, 128, 1, 7, 128, 1, 1), (256, 147, 147, 32, 3, 3, 64, 1, 1),
+    (256, 149, 149, 32, 3, 3, 32, 1, 0), (256, 299, 299, 3, 3, 3, 32, 2, 0)]
+
+
+def conv_main(a):
+    sel = [int(i) for i in a.convs.split(",")] if a.convs != "all" else range(len(C5_CONVS))
+    for i in sel:
+        n, h, w, ci, kh, kw, co, st, pad = C5_CONVS[i]
+        g = cg.Graph(0)
+        vx, vw = g.var((n, h, w, ci)), g.var((kh, kw, ci, co))
+        o = g.add_node("CONV2D", [vx, vw], sh=st, sw=st, pad=pad)
+        g.plan_memory([o])
+        rng = np.random.default_rng(0)
+        g.assign(vx, rng.uniform(-1, 1, (n, h, w, ci)).astype(np.float32))
+        g.assign(vw, rng.uniform(-1, 1, (kh, kw, ci, co)).astype(np.float32))
+        ms = time_graph(g, [o], a.iters)
+        ho = (h - kh) // st + 1 if pad == 0 else (h + st - 1) // st
+        wo = (w - kw) // st + 1 if pad == 0 else (w + st - 1) // st
+        fl = 2.0 * n * ho * wo * co * kh * kw * ci
+        print(json.dumps({"op": "CONV2D", "shape": C5_CONVS[i], "ms": ms, "tflops": fl / ms / 1e9,
+                          "gb_s": 4.0 * (n * h * w * ci + n * ho * wo * co) / ms / 1e6}), flush=True)
+        g.destroy()
+
+
 def time_graph(g, outs, iters):
     ws = torch.cuda.ExternalStream(g.work_stream())
     for _ in range(3):
@@ -52,7 +78,11 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--shapes", default="", help="comma-separated indices into C3_DOTS (default: all)")
     ap.add_argument("--no-torch", action="store_true")
+    ap.add_argument("--convs", default="", help="C5 conv indices or 'all' (instead of the dots)")
     a = ap.parse_args()
+    if a.convs:
+        conv_main(a)
+        return
     sel = [int(i) for i in a.shapes.split(",")] if a.shapes else range(len(C3_DOTS))
     for (m, n, k, ta, tb) in [C3_DOTS[i] for i in sel]:
         sa = (k, m) if ta else (m, k)
