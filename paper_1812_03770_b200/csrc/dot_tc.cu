@@ -152,6 +152,18 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// im2col load of 128 output pixels x 32 channels: TMA walks the pixels from (w, h, n)
+// through the map's bounding box (conv strides = traversal strides) and reads channels
+// [c, c + 32) at pixel + (off_w, off_h); outside the image -> zero.
+__device__ __forceinline__ void tma_load_im2col(uint32_t dst, const CUtensorMap* map, int c, int w, int h, int n,
+                                                uint16_t off_w, uint16_t off_h, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6], "
+      "{%7, %8};" ::"r"(dst),
+      "l"(map), "r"(c), "r"(w), "r"(h), "r"(n), "r"(bar), "h"(off_w), "h"(off_h)
+      : "memory");
+}
+
 // UMMA shared-memory descriptor (version 1 = sm_100).  layout: 2 = SWIZZLE_128B
 // (16-byte chunks), 1 = SWIZZLE_128B_BASE32B (32-byte chunks; the only swizzled
 // MN-major layout TF32 operands have).
@@ -308,7 +320,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SA; ++s) {
-      mbar_init(fullA(s), GATHER ? 128 : 1);
+      mbar_init(fullA(s), GATHER && !cv.tma ? 128 : 1);
       mbar_init(emptyA(s), 4);  // the 4 split warps of this CTA
     }
     for (int s = 0; s < SB; ++s) {
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       mbar_init(tempty(b), 4 * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (!GATHER) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
+    if (!GATHER || cv.tma) asm volatile("prefetch.tensormap [%0];" ::"l"(&mapA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&mapB) : "memory");
   }
   if (warp == 1) {
@@ -350,10 +362,31 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
       for (int u = u_first; u < units; u += u_step) {
         int z, m0, n0, kb0, nk;
         unit(u, z, m0, n0, kb0, nk);
+        // im2col TMA: traversal start = input position of this unit's first output pixel;
+        // k-slab -> (tap (kh, kw) = im2col offsets, 32 channels from ci)
+        int xw = 0, xh = 0, xn = 0, ci = 0, kh = 0, kw = 0;
+        if (GATHER && cv.tma) {
+          const int hw = cv.Ho * cv.Wo;
+          xn = m0 / hw;
+          const int q = m0 - xn * hw, ho = q / cv.Wo, wo = q - ho * cv.Wo;
+          xh = ho * cv.sh - cv.pt;
+          xw = wo * cv.sw - cv.pl;
+          const int k0 = kb0 * BK, tap = k0 / cv.Ci;
+          ci = k0 - tap * cv.Ci;
+          kh = tap / cv.KW;
+          kw = tap - kh * cv.KW;
+        }
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int sa = it % SA, sb = it % SB;
           const int nb = n0 + (int)rank * BNH;
           const int k0 = (kb0 + kb) * BK;
+          if (GATHER && cv.tma) {
+            mbar_wait(emptyA(sa), ((it / SA) & 1) ^ 1);
+            mbar_expect_tx(fullA(sa), TILE_A);
+            tma_load_im2col(sbase + A_BASE + sa * TILE_A, &mapA, ci, xw, xh, xn, (uint16_t)kw, (uint16_t)kh, fullA(sa));
+            ci += BK;
+            if (ci == cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
+          }
           if (!GATHER) {
             mbar_wait(emptyA(sa), ((it / SA) & 1) ^ 1);
             const uint32_t st = sbase + A_BASE + sa * TILE_A;
@@ -597,7 +630,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         else mbar_arrive_cta(tempty(b), 0);
       }
     }
-  } else if (GATHER) {
+  } else if (GATHER && !cv.tma) {
     // ---------------- warps 10..13: im2col gather of A, one tile row (output pixel) per thread.
     // The (kh, kw, ci) position of the k-slab is advanced incrementally (no
     // per-chunk divisions); with Ci % 32 == 0 a whole slab is one tap: one
@@ -711,6 +744,43 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
             mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                    CUtensorMapFloatOOBfill);
+EncodeIm2colFn encode_im2col_fn() {
+  static EncodeIm2colFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeIm2colFn)p;
+  });
+  return fn;
+}
+
+// NHWC input as a rank-4 im2col map {C, W, H, N}: 32 channels x 128 pixels per load,
+// SWIZZLE_128B rows (the K-major A tile layout).  Bounding box per spatial dim:
+// lower = -pad, upper chosen so the strided traversal visits exactly the Wo (Ho)
+// output positions: box = (Wo - 1) * sw + 1.
+bool make_im2col_map(CUtensorMap* m, const float* x, int n, int h, int w, int ci, int ho, int wo, int sh, int sw, int pt,
+                     int pl) {
+  EncodeIm2colFn fn = encode_im2col_fn();
+  if (!fn || ci % 32 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  const int lw = -pl, lh = -pt;
+  const int uw = lw + (wo - 1) * sw + 1 - w, uh = lh + (ho - 1) * sh + 1 - h;
+  if (lw < -128 || lh < -128 || uw < -128 || uw > 127 || uh < -128 || uh > 127) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)ci, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)ci * 4, (cuuint64_t)w * ci * 4, (cuuint64_t)h * w * ci * 4};
+  const int lower[2] = {lw, lh}, upper[2] = {uw, uh};
+  cuuint32_t estr[4] = {1, (cuuint32_t)sw, (cuuint32_t)sh, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, lower, upper, 32, BM, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -863,7 +933,9 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   if (p->splits > 1 && !ws) return -3;
   p->a_mn = 0; p->b_mn = 1;
   p->C = y;
-  p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl};
+  p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl, 0};
+  if (ci % 32 == 0 && !getenv("CG_CONV_NO_IM2COL_TMA") && sh <= 8 && sw <= 8)
+    p->conv.tma = make_im2col_map(reinterpret_cast<CUtensorMap*>(p->mapA), x, n, h, wd, ci, ho, wo, sh, sw, pt, pl) ? 1 : 0;
   p->bn = pick_bn(p->M, co, num_sms);
   p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms, true);
   // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0

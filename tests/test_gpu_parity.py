@@ -293,7 +293,12 @@ TC_CONV_CASES = [((2, 35, 35, 64), (3, 3, 64, 96), 1, 1), ((2, 35, 35, 32), (3, 
                  ((2, 31, 29, 3), (3, 3, 3, 32), 2, 0), ((2, 20, 20, 6), (5, 5, 6, 16), 1, 1),
                  ((2, 8, 8, 64), (3, 3, 64, 448), 1, 1), ((16, 35, 35, 32), (1, 1, 32, 512), 1, 1),
                  # CTA-pair tiles (>= one wave of 256-row units) on the 4-channel and element gathers
-                 ((32, 35, 35, 20), (3, 3, 20, 128), 1, 1), ((128, 31, 29, 3), (3, 3, 3, 64), 2, 0)]
+                 ((32, 35, 35, 20), (3, 3, 20, 128), 1, 1), ((128, 31, 29, 3), (3, 3, 3, 64), 2, 0),
+                 # Ci % 32 == 0: TMA im2col tiles (SAME/VALID, strides 1/2, asymmetric SAME pads, 1xn / nx1 taps)
+                 ((2, 17, 17, 32), (3, 3, 32, 64), 2, 1), ((3, 16, 16, 64), (3, 3, 64, 32), 2, 1),
+                 ((2, 17, 17, 32), (1, 7, 32, 64), 1, 1), ((2, 17, 17, 32), (7, 1, 32, 64), 1, 1),
+                 ((2, 12, 13, 96), (5, 5, 96, 48), 1, 1), ((9, 35, 35, 64), (3, 3, 64, 96), 1, 1),
+                 ((4, 37, 33, 32), (3, 3, 32, 32), 2, 0)]
 
 
 @pytest.mark.parametrize("xs,ws,st,pad", TC_CONV_CASES)
