@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <type_traits>
+#include <cstdlib>
 #include <cstdint>
 
 namespace cg {
@@ -368,6 +370,91 @@ __global__ void maxpool_bwd_tiled_kernel(const float* __restrict__ x, const floa
   }
 }
 
+// 2 x 2 stride-2 VALID max pool with few channels (C4: C = 6, 16).  Thread =
+// (output pixel, V channels) so neighbouring lanes read neighbouring 8- / 16-byte
+// pieces of the same window rows.  Same combine order as maxpool_kernel (bit-identical).
+template <int C, int V>
+__global__ void maxpool2_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, int total) {
+  using VT = typename std::conditional<V == 4, float4, float2>::type;
+  constexpr int Q = C / V;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int p = t / Q, c = (t - p * Q) * V;
+    const int wo = p % g.wo, q = p / g.wo, ho = q % g.ho, n = q / g.ho;
+    const size_t o0 = (((size_t)n * g.h + 2 * ho) * g.w + 2 * wo) * C + c, o1 = o0 + (size_t)g.w * C;
+    VT w4[4];
+    w4[0] = __ldg(reinterpret_cast<const VT*>(x + o0));
+    w4[1] = __ldg(reinterpret_cast<const VT*>(x + o0 + C));
+    w4[2] = __ldg(reinterpret_cast<const VT*>(x + o1));
+    w4[3] = __ldg(reinterpret_cast<const VT*>(x + o1 + C));
+    const float* wf = reinterpret_cast<const float*>(w4);
+    VT o;
+    float* of = reinterpret_cast<float*>(&o);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      float m = -__int_as_float(0x7f800000);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) asm("max.NaN.f32 %0, %0, %1;" : "+f"(m) : "f"(wf[k * V + e]));
+      of[e] = m;
+    }
+    *reinterpret_cast<VT*>(y + (size_t)p * C + c) = o;
+  }
+}
+
+// backward of the above: each window's dy goes to its first maximal element
+// (row-major, as maxpool_bwd_tiled_kernel); rows / columns a VALID pool never
+// reads (odd H or W) get zero gradient.  Thread = (output pixel, V channels):
+// neighbouring lanes touch neighbouring 8- / 16-byte pieces of the same window rows.
+template <int C, int V>
+__global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ dx,
+                                    ConvGeom g, int total) {
+  using VT = typename std::conditional<V == 4, float4, float2>::type;
+  constexpr int Q = C / V;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int p = t / Q, c = (t - p * Q) * V;
+    const int wo = p % g.wo, q = p / g.wo, ho = q % g.ho, n = q / g.ho;
+    const size_t o0 = (((size_t)n * g.h + 2 * ho) * g.w + 2 * wo) * C + c, o1 = o0 + (size_t)g.w * C;
+    VT w4[4];
+    w4[0] = __ldg(reinterpret_cast<const VT*>(x + o0));
+    w4[1] = __ldg(reinterpret_cast<const VT*>(x + o0 + C));
+    w4[2] = __ldg(reinterpret_cast<const VT*>(x + o1));
+    w4[3] = __ldg(reinterpret_cast<const VT*>(x + o1 + C));
+    const VT dv = __ldg(reinterpret_cast<const VT*>(dy + (size_t)p * C + c));
+    VT r4[4];
+    const float* wf = reinterpret_cast<const float*>(w4);
+    const float* df = reinterpret_cast<const float*>(&dv);
+    float* rf = reinterpret_cast<float*>(r4);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      float m = -__int_as_float(0x7f800000);
+      int best = -1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float v = wf[k * V + e];
+        if (v > m || best < 0) { m = v; best = k; }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) rf[k * V + e] = best == k ? df[e] : 0.f;
+    }
+    *reinterpret_cast<VT*>(dx + o0) = r4[0];
+    *reinterpret_cast<VT*>(dx + o0 + C) = r4[1];
+    *reinterpret_cast<VT*>(dx + o1) = r4[2];
+    *reinterpret_cast<VT*>(dx + o1 + C) = r4[3];
+    // zero the column / row a VALID 2x2 pool skips (odd W / H)
+    const bool lastc = wo == g.wo - 1 && g.w > 2 * g.wo;
+    const VT z = {};
+    if (lastc) {
+      *reinterpret_cast<VT*>(dx + o0 + 2 * C) = z;
+      *reinterpret_cast<VT*>(dx + o1 + 2 * C) = z;
+    }
+    if (ho == g.ho - 1 && g.h > 2 * g.ho) {
+      const size_t o2 = o1 + (size_t)g.w * C;
+      *reinterpret_cast<VT*>(dx + o2) = z;
+      *reinterpret_cast<VT*>(dx + o2 + C) = z;
+      if (lastc) *reinterpret_cast<VT*>(dx + o2 + 2 * C) = z;
+    }
+  }
+}
+
 template <typename I>
 __global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, I total) {
   for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
@@ -580,8 +667,20 @@ cudaError_t launch_conv2d_bwd_kernel(const float* x, const float* dy, float* dw,
   return launch_reduce_finalize(ws, dw, outs, S, 0, s);
 }
 
+static bool maxpool2_ok(const ConvGeom& g) {
+  return g.kh == 2 && g.kw == 2 && g.sh == 2 && g.sw == 2 && g.pt == 0 && g.pl == 0 && (g.co == 6 || g.co == 16) &&
+         (long long)g.n * g.h * g.w * g.co < INT32_MAX && g.h >= 2 * g.ho && g.w >= 2 * g.wo && g.h <= 2 * g.ho + 1 &&
+         g.w <= 2 * g.wo + 1 && !getenv("CG_POOL_GENERIC");
+}
+
 cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
+  if (maxpool2_ok(g)) {
+    const int pix = g.n * g.ho * g.wo;
+    if (g.co == 6) maxpool2_fwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, y, g, pix * 3);
+    else maxpool2_fwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, y, g, pix * 4);
+    return cudaGetLastError();
+  }
   if (g.co % 4 == 0 && total < INT32_MAX) {
     const int blocks = (int)std::min<long long>((total / 4 + 255) / 256, 65535LL * 8);
     if (g.kh == 3 && g.kw == 3) pool4_kernel<true, 3><<<blocks, 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
@@ -594,6 +693,12 @@ cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStre
 }
 
 cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s) {
+  if (maxpool2_ok(g)) {
+    const int pix = g.n * g.ho * g.wo;
+    if (g.co == 6) maxpool2_bwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, dy, dx, g, pix * 3);
+    else maxpool2_bwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, dy, dx, g, pix * 4);
+    return cudaGetLastError();
+  }
   if (g.kh == g.sh && g.kw == g.sw && g.pt == 0 && g.pl == 0 && g.h == g.ho * g.sh && g.w == g.wo * g.sw) {
     long long windows = (long long)g.n * g.ho * g.wo * g.co;
     if (windows < INT32_MAX) maxpool_bwd_tiled_kernel<int><<<grid_for(windows), 256, 0, s>>>(x, dy, dx, g, (int)windows);

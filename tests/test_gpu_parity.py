@@ -392,6 +392,32 @@ def test_concat_vectorised():
     assert np.array_equal(g.read(cat), np.concatenate(xs, axis=3))
 
 
+@pytest.mark.parametrize("shape", [(3, 9, 9, 16), (2, 13, 13, 6), (2, 26, 26, 6), (2, 8, 9, 16)])
+def test_maxpool2_few_channels_exact(shape):
+    """C4's 2x2 stride-2 VALID max pools (C = 6, 16; odd sizes drop a row / column):
+    forward and backward bit-identical to the oracle, with tied maxima."""
+    rng = np.random.default_rng(5)
+    a = {"kh": 2, "kw": 2, "sh": 2, "sw": 2, "pad": 0}
+    x = rng.integers(0, 3, shape).astype(np.float32)
+    ho, wo = shape[1] // 2, shape[2] // 2
+    dy = rng.integers(1, 5, (shape[0], ho, wo, shape[3])).astype(np.float32)
+    g = cg.Graph(0)
+    vx, vd = g.var(x.shape), g.var(dy.shape)
+    mp = g.add_node("MAXPOOL2D", [vx], **a)
+    o = g.add_node("MAXPOOL2D_BWD", [vx, vd], **a)
+    g.plan_memory([mp, o])
+    g.assign(vx, x)
+    g.assign(vd, dy)
+    g.eval([mp, o])
+    og = OGraph()
+    ox, od = og.add_leaf("VAR", x.shape), og.add_leaf("VAR", dy.shape)
+    omp = og.add_node("MAXPOOL2D", [ox], a)
+    oo = og.add_node("MAXPOOL2D_BWD", [ox, od], a)
+    vals = evaluate(og, {ox: x, od: dy})
+    assert np.array_equal(g.read(mp), vals[omp])
+    assert np.array_equal(g.read(o), vals[oo])
+
+
 @pytest.mark.parametrize("k,s,pad", [(2, 2, 0), (3, 2, 0), (3, 1, 1), (3, 2, 1)])
 def test_pools_exact(k, s, pad):
     a = {"kh": k, "kw": k, "sh": s, "sw": s, "pad": pad}
