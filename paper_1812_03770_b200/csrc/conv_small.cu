@@ -27,14 +27,45 @@ constexpr int SMEM_LIMIT = 96 * 1024;
 
 // zero-padded image n of x [N,H,W,C] into s, channel-planar [C][Hp][Wp] so that
 // threads on adjacent pixels read adjacent words (no bank conflicts)
+template <int U = 8>  // loads in flight per thread
 __device__ __forceinline__ void load_padded(float* s, const float* __restrict__ x, int n, int H, int W, int C, int Hp,
                                             int Wp, int pt, int pl) {
   const int tot = Hp * Wp * C;
   const float* xi = x + (size_t)n * H * W * C;
-  for (int e = threadIdx.x; e < tot; e += blockDim.x) {  // e walks the NHWC source order (coalesced)
-    const int c = e % C, q = e / C, wp = q % Wp, hp = q / Wp;
-    const int h = hp - pt, w = wp - pl;
-    s[(c * Hp + hp) * Wp + wp] = (h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xi + ((size_t)h * W + w) * C + c) : 0.f;
+  // e walks the NHWC source order (coalesced); U loads in flight per thread
+  for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
+    float v[U];
+    int dst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int c = e % C, q = e / C, wp = q % Wp, hp = q / Wp;
+      const int h = hp - pt, w = wp - pl;
+      dst[u] = e < tot ? (c * Hp + hp) * Wp + wp : -1;
+      v[u] = (e < tot && h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xi + ((size_t)h * W + w) * C + c) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dst[u] >= 0) s[dst[u]] = v[u];
+  }
+}
+
+// dy image [P][C] -> shared [P][C4] (channels zero-padded to C4), 8 loads in flight
+__device__ __forceinline__ void load_dy_padded(float* ds, const float* __restrict__ dyi, int P, int C, int C4) {
+  const int tot = P * C4;
+  for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * blockDim.x) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      const int c = e % C4, p = e / C4;
+      v[u] = (e < tot && c < C) ? __ldg(dyi + (size_t)p * C + c) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < tot) ds[e] = v[u];
+    }
   }
 }
 
@@ -52,7 +83,7 @@ __global__ void __launch_bounds__(256) conv_fwd_img(const float* __restrict__ x,
   const int P = g.ho * g.wo;
   for (int n = blockIdx.x; n < g.n; n += gridDim.x) {
     __syncthreads();
-    load_padded(xs, x, n, g.h, g.w, g.ci, Hp, Wp, g.pt, g.pl);
+    load_padded<1>(xs, x, n, g.h, g.w, g.ci, Hp, Wp, g.pt, g.pl);
     __syncthreads();
     for (int p = threadIdx.x; p < P; p += blockDim.x) {
       const int ho = p / g.wo, wo = p % g.wo;
@@ -167,11 +198,7 @@ __global__ void __launch_bounds__(256) conv_bwdk_img(const float* __restrict__ x
   for (int n = n0; n < n1; ++n) {
     __syncthreads();
     load_padded(xs, x, n, g.h, g.w, g.ci, Hp, Wp, g.pt, g.pl);
-    const float* dyi = dy + (size_t)n * P * g.co;
-    for (int e = threadIdx.x; e < P * co4; e += blockDim.x) {
-      const int c = e % co4, p = e / co4;
-      ds[e] = c < g.co ? __ldg(dyi + (size_t)p * g.co + c) : 0.f;
-    }
+    load_dy_padded(ds, dy + (size_t)n * P * g.co, P, g.co, co4);
     __syncthreads();
     if (active) {
       int ho = ph / g.wo, wo = ph % g.wo;  // (ho, wo) of pixel p, advanced incrementally
@@ -349,11 +376,7 @@ __global__ void __launch_bounds__(256) conv_bwdk_rt_kernel(const float* __restri
   for (int n = n0; n < n1; ++n) {
     __syncthreads();
     load_padded(xs, x, n, g.h, g.w, g.ci, Hp, Wp, g.pt, g.pl);
-    const float* dyi = dy + (size_t)n * P * g.co;
-    for (int e = threadIdx.x; e < P * co4; e += blockDim.x) {
-      const int c = e % co4, p = e / co4;
-      ds[e] = c < g.co ? __ldg(dyi + (size_t)p * g.co + c) : 0.f;
-    }
+    load_dy_padded(ds, dy + (size_t)n * P * g.co, P, g.co, co4);
     __syncthreads();
     if (active) {
       for (int ho = ph; ho < g.ho; ho += PH) {
