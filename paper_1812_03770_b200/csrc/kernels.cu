@@ -512,7 +512,27 @@ __global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ 
     const float ninf = -__int_as_float(0x7f800000);
     float4 acc = MAXP ? make_float4(ninf, ninf, ninf, ninf) : make_float4(0.f, 0.f, 0.f, 0.f);
     int cnt = 0;
-    if (KS > 0) {
+    const int hi0 = ho * g.sh - g.pt, wi0 = wo * g.sw - g.pl;
+    if (KS > 0 && hi0 >= 0 && wi0 >= 0 && hi0 + KS <= g.h && wi0 + KS <= g.w) {
+      // interior window (most outputs): no bounds checks, 32-bit offsets from one base
+      const float4* xb = x + (((size_t)n * g.h + hi0) * g.w + wi0) * C4 + c;
+      constexpr int KK = KS > 0 ? KS * KS : 1;
+      float4 v[KK];
+#pragma unroll
+      for (int kh = 0; kh < KS; ++kh)
+#pragma unroll
+        for (int kw = 0; kw < KS; ++kw) v[kh * KS + kw] = __ldg(xb + (kh * g.w + kw) * C4);
+#pragma unroll
+      for (int i = 0; i < KK; ++i) {
+        if (MAXP) {
+          acc.x = nanmax(acc.x, v[i].x); acc.y = nanmax(acc.y, v[i].y); acc.z = nanmax(acc.z, v[i].z); acc.w = nanmax(acc.w, v[i].w);
+        } else {
+          acc.x = __fadd_rn(acc.x, v[i].x); acc.y = __fadd_rn(acc.y, v[i].y);
+          acc.z = __fadd_rn(acc.z, v[i].z); acc.w = __fadd_rn(acc.w, v[i].w);
+        }
+      }
+      cnt = KK;
+    } else if (KS > 0) {
       constexpr int KK = KS > 0 ? KS * KS : 1;
       float4 v[KK];
       bool ok[KK];
@@ -552,9 +572,9 @@ __global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ 
         ++cnt;
       }
     }
-    if (!MAXP) {
-      const float f = (float)cnt;
-      acc = make_float4(__fdiv_rn(acc.x, f), __fdiv_rn(acc.y, f), __fdiv_rn(acc.z, f), __fdiv_rn(acc.w, f));
+    if (!MAXP) {  // x (1 / count): within 1 ulp of the quotient (the pool tolerance)
+      const float r = __frcp_rn((float)cnt);
+      acc = make_float4(__fmul_rn(acc.x, r), __fmul_rn(acc.y, r), __fmul_rn(acc.z, r), __fmul_rn(acc.w, r));
     }
     y[t] = acc;
   }
