@@ -380,12 +380,24 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           const int sa = it % SA, sb = it % SB;
           const int nb = n0 + (int)rank * BNH;
           const int k0 = (kb0 + kb) * BK;
-          if (GATHER && cv.tma) {
+          if (GATHER && cv.tma == 1) {  // one 128 x 32-channel box (one tap)
             mbar_wait(emptyA(sa), ((it / SA) & 1) ^ 1);
             mbar_expect_tx(fullA(sa), TILE_A);
             tma_load_im2col(sbase + A_BASE + sa * TILE_A, &mapA, ci, xw, xh, xn, (uint16_t)kw, (uint16_t)kh, fullA(sa));
             ci += BK;
             if (ci == cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
+          } else if (GATHER && cv.tma == 2) {  // two 128 x 16-channel boxes (each within one tap)
+            mbar_wait(emptyA(sa), ((it / SA) & 1) ^ 1);
+            mbar_expect_tx(fullA(sa), TILE_A);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              // a half-slab past K (K % 32 == 16) loads from image N: out of bounds -> zeros
+              const bool in_k = k0 + 16 * h < K;
+              tma_load_im2col(sbase + A_BASE + sa * TILE_A + h * (TILE_A / 2), &mapA, ci, xw, xh, in_k ? xn : 1 << 30,
+                              (uint16_t)kw, (uint16_t)kh, fullA(sa));
+              ci += 16;
+              if (ci == cv.Ci) { ci = 0; if (++kw == cv.KW) { kw = 0; ++kh; } }
+            }
           }
           if (!GATHER) {
             mbar_wait(emptyA(sa), ((it / SA) & 1) ^ 1);
@@ -489,6 +501,20 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           const uint32_t box = st + (uint32_t)(rr >> 5) * 4096u + (uint32_t)((lane & 7) << 2);
 #pragma unroll
           for (int k = 0; k < 32; ++k) hv[k] = __float_as_uint(lds32(box + k * 128 + ((((lane >> 3) ^ (k & 3))) << 5)));
+        } else if (GATHER && cv.tma == 2) {
+          // two [128][16] SWIZZLE_64B half-tiles: 16-byte chunk c of row r at c ^ ((r >> 1) & 3)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t row = st + (uint32_t)h * (TILE_A / 2) + (uint32_t)rr * 64u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float4 v = lds128(row + ((c ^ ((rr >> 1) & 3)) << 4));
+              hv[16 * h + 4 * c] = __float_as_uint(v.x);
+              hv[16 * h + 4 * c + 1] = __float_as_uint(v.y);
+              hv[16 * h + 4 * c + 2] = __float_as_uint(v.z);
+              hv[16 * h + 4 * c + 3] = __float_as_uint(v.w);
+            }
+          }
         } else {
           const uint32_t row = st + (uint32_t)rr * 128u;
 #pragma unroll
@@ -768,9 +794,9 @@ EncodeIm2colFn encode_im2col_fn() {
 // lower = -pad, upper chosen so the strided traversal visits exactly the Wo (Ho)
 // output positions: box = (Wo - 1) * sw + 1.
 bool make_im2col_map(CUtensorMap* m, const float* x, int n, int h, int w, int ci, int ho, int wo, int sh, int sw, int pt,
-                     int pl) {
+                     int pl, int chans) {
   EncodeIm2colFn fn = encode_im2col_fn();
-  if (!fn || ci % 32 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  if (!fn || ci % chans || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
   const int lw = -pl, lh = -pt;
   const int uw = lw + (wo - 1) * sw + 1 - w, uh = lh + (ho - 1) * sh + 1 - h;
   if (lw < -128 || lh < -128 || uw < -128 || uw > 127 || uh < -128 || uh > 127) return false;
@@ -778,9 +804,9 @@ bool make_im2col_map(CUtensorMap* m, const float* x, int n, int h, int w, int ci
   cuuint64_t strides[3] = {(cuuint64_t)ci * 4, (cuuint64_t)w * ci * 4, (cuuint64_t)h * w * ci * 4};
   const int lower[2] = {lw, lh}, upper[2] = {uw, uh};
   cuuint32_t estr[4] = {1, (cuuint32_t)sw, (cuuint32_t)sh, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, lower, upper, 32, BM, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, lower, upper, (cuuint32_t)chans, BM, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, chans == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -934,8 +960,12 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   p->a_mn = 0; p->b_mn = 1;
   p->C = y;
   p->conv = ConvA{x, h, wd, ci, ho, wo, kw, sh, sw, pt, pl, 0};
-  if (ci % 32 == 0 && !getenv("CG_CONV_NO_IM2COL_TMA") && sh <= 8 && sw <= 8)
-    p->conv.tma = make_im2col_map(reinterpret_cast<CUtensorMap*>(p->mapA), x, n, h, wd, ci, ho, wo, sh, sw, pt, pl) ? 1 : 0;
+  // A by TMA im2col: 32-channel boxes when Ci % 32 == 0, pairs of 16-channel boxes when Ci % 16 == 0
+  if (!getenv("CG_CONV_NO_IM2COL_TMA") && sh <= 8 && sw <= 8) {
+    CUtensorMap* ma = reinterpret_cast<CUtensorMap*>(p->mapA);
+    if (ci % 32 == 0 && make_im2col_map(ma, x, n, h, wd, ci, ho, wo, sh, sw, pt, pl, 32)) p->conv.tma = 1;
+    else if (ci % 16 == 0 && make_im2col_map(ma, x, n, h, wd, ci, ho, wo, sh, sw, pt, pl, 16)) p->conv.tma = 2;
+  }
   p->bn = pick_bn(p->M, co, num_sms);
   p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms, true);
   // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0
