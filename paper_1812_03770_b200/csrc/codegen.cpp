@@ -461,8 +461,11 @@ KernelSpec gen_red(const HostGraph& hg, const Group& G, int num_sms) {
   int64_t bx = (I + TX - 1) / TX, by = (O + TO - 1) / TO;
   int64_t blocks = bx * by;
   int64_t S = 1;
-  if (blocks < 2LL * num_sms && Rn > 16LL * TY) {
-    S = std::min<int64_t>((2LL * num_sms + blocks - 1) / blocks, Rn / (16LL * TY));
+  // split the reduced extent until ~8 blocks per SM are in flight (each thread then
+  // walks >= 16 rows: a short chain of dependent load batches) -- C3's bias gradients
+  // [4096, 1024] -> [1, 1024]: 4 x 74 blocks -> 4 x 256
+  if (blocks < 8LL * num_sms && Rn > 16LL * TY) {
+    S = std::min<int64_t>((8LL * num_sms + blocks - 1) / blocks, Rn / (16LL * TY));
     S = std::max<int64_t>(1, std::min<int64_t>(S, 65535));
   }
   int64_t CH = (Rn + S - 1) / S;

@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         if (dbg && u == 0 && kb == 0 && t < 8) dbg[8 + t] = reinterpret_cast<float*>(smem + B_BASE)[t];  // B raw
         // B: lo tile in shared memory (the raw tile is read as hi by the tensor core,
         // which truncates fp32 operands to TF32; with raw_hi == 0 hi is written too)
-        if (raw_hi != 2) {
+        if (raw_hi != 2 && raw_hi != 6) {  // (6: measurement probe without the B split)
           const uint32_t hb = sbase + B_BASE + sb * TILE_B + t * 16, lb = sbase + LO_BASE + l * LO_BYTES + t * 16;
           constexpr int PER = TILE_B / 16 / 128;
           float4 v[PER];
