@@ -409,7 +409,8 @@ bool cols4_ok(const float* A, int M) { return M % 4 == 0 && (reinterpret_cast<ui
 
 void cols4_split(int M, int K, int num_sms, int* kchunk, int* S) {
   const int mblocks = (M + 4 * C4_THREADS - 1) / (4 * C4_THREADS);
-  int s = std::max(1, std::min((3 * num_sms + mblocks - 1) / mblocks, (K + 63) / 64));
+  // ~8 blocks (16 warps) per SM, k-chunks of >= 32 rows (partials stay << the A read)
+  int s = std::max(1, std::min((8 * num_sms + mblocks - 1) / mblocks, (K + 31) / 32));
   int ch = (K + s - 1) / s;
   ch = std::min(C4_KMAX, (ch + C4_U - 1) / C4_U * C4_U);
   *kchunk = ch;
