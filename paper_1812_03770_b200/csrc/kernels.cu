@@ -500,6 +500,83 @@ __device__ __forceinline__ float nanmax(float a, float b) {
 
 // KS > 0: square KS x KS window known at compile time: the KS*KS loads are issued
 // together (predicated) before the fixed-order combine -> same results, more MLP
+// 3 x 3 stride-1 average pool (C5): a thread computes RS vertically adjacent outputs
+// of one (column, 4 channels), so the 3 + RS - 1 input rows of its strip are loaded
+// once (3 (RS + 2) loads for RS outputs instead of 9 RS).  Interior strips only
+// (the caller's grid covers strips; border outputs go through the generic path of
+// pool4_kernel); per output the summation order is pool4_kernel's (kh, then kw).
+constexpr int AVG_RS = 4;
+__global__ void avgpool3_strip_kernel(const float4* __restrict__ x, float4* __restrict__ y, ConvGeom g, int total) {
+  const int C4 = g.co / 4, HS = (g.ho + AVG_RS - 1) / AVG_RS;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int c = t % C4;
+    int q = t / C4;
+    const int wo = q % g.wo;
+    q /= g.wo;
+    const int hs = q % HS, n = q / HS;
+    const int ho0 = hs * AVG_RS, nr = min(AVG_RS, g.ho - ho0);
+    const int hi0 = ho0 - g.pt, wi0 = wo - g.pl;
+    const bool interior = hi0 >= 0 && wi0 >= 0 && hi0 + nr + 2 <= g.h && wi0 + 3 <= g.w;
+    if (interior && nr == AVG_RS) {  // the strip's (RS + 2) x 3 window once, in registers
+      const float4* xb = x + (((size_t)n * g.h + hi0) * g.w + wi0) * C4 + c;
+      float4 v[AVG_RS + 2][3];
+#pragma unroll
+      for (int rr = 0; rr < AVG_RS + 2; ++rr)
+#pragma unroll
+        for (int kw = 0; kw < 3; ++kw) v[rr][kw] = __ldg(xb + (rr * g.w + kw) * C4);
+      const float r = 1.f / 9.f;
+#pragma unroll
+      for (int j = 0; j < AVG_RS; ++j) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) {
+            const float4 u = v[j + kh][kw];
+            acc.x = __fadd_rn(acc.x, u.x); acc.y = __fadd_rn(acc.y, u.y);
+            acc.z = __fadd_rn(acc.z, u.z); acc.w = __fadd_rn(acc.w, u.w);
+          }
+        y[(((size_t)n * g.ho + ho0 + j) * g.wo + wo) * C4 + c] =
+            make_float4(__fmul_rn(acc.x, r), __fmul_rn(acc.y, r), __fmul_rn(acc.z, r), __fmul_rn(acc.w, r));
+      }
+      continue;
+    }
+    for (int j = 0; j < nr; ++j) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float r;
+      if (interior) {
+        const float4* xb = x + (((size_t)n * g.h + hi0 + j) * g.w + wi0) * C4 + c;
+#pragma unroll
+        for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+          for (int kw = 0; kw < 3; ++kw) {
+            const float4 v = __ldg(xb + (kh * g.w + kw) * C4);
+            acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
+            acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
+          }
+        r = 1.f / 9.f;
+      } else {
+        int cnt = 0;
+        for (int kh = 0; kh < 3; ++kh) {
+          const int hi = hi0 + j + kh;
+          if (hi < 0 || hi >= g.h) continue;
+          for (int kw = 0; kw < 3; ++kw) {
+            const int wi = wi0 + kw;
+            if (wi < 0 || wi >= g.w) continue;
+            const float4 v = __ldg(x + (((size_t)n * g.h + hi) * g.w + wi) * C4 + c);
+            acc.x = __fadd_rn(acc.x, v.x); acc.y = __fadd_rn(acc.y, v.y);
+            acc.z = __fadd_rn(acc.z, v.z); acc.w = __fadd_rn(acc.w, v.w);
+            ++cnt;
+          }
+        }
+        r = __frcp_rn((float)cnt);
+      }
+      y[(((size_t)n * g.ho + ho0 + j) * g.wo + wo) * C4 + c] =
+          make_float4(__fmul_rn(acc.x, r), __fmul_rn(acc.y, r), __fmul_rn(acc.z, r), __fmul_rn(acc.w, r));
+    }
+  }
+}
+
 template <bool MAXP, int KS>
 __global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ y, ConvGeom g, int total4) {
   const int C4 = g.co / 4;
@@ -735,7 +812,10 @@ cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStre
   long long total = (long long)g.n * g.ho * g.wo * g.co;
   if (g.co % 4 == 0 && total < INT32_MAX) {
     const int blocks = (int)std::min<long long>((total / 4 + 255) / 256, 65535LL * 8);
-    if (g.kh == 3 && g.kw == 3) pool4_kernel<false, 3><<<blocks, 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
+    if (g.kh == 3 && g.kw == 3 && g.sh == 1 && g.sw == 1 && !getenv("CG_POOL_NO_STRIPS")) {
+      const long long strips = (long long)g.n * ((g.ho + AVG_RS - 1) / AVG_RS) * g.wo * (g.co / 4);
+      avgpool3_strip_kernel<<<grid_for(strips), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)strips);
+    } else if (g.kh == 3 && g.kw == 3) pool4_kernel<false, 3><<<blocks, 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
     else pool4_kernel<false, 0><<<grid_for(total / 4), 256, 0, s>>>((const float4*)x, (float4*)y, g, (int)(total / 4));
     return cudaGetLastError();
   }
