@@ -459,22 +459,22 @@ void set_smem(F f) {
 
 constexpr int RT_PX = 4;
 
-RtGeom rt_geom_fwd(const ConvGeom& g) {
+RtGeom rt_geom_fwd(const ConvGeom& g, int px = RT_PX) {
   RtGeom r{};
   r.n = g.n; r.hin = g.h; r.win = g.w; r.cin = g.ci;
   r.hout = g.ho; r.wout = g.wo; r.cout = g.co;
   r.pt = g.pt; r.pl = g.pl; r.wcin = g.ci; r.wcout = g.co;
   r.Hp = g.ho + g.kh - 1;
-  r.Wp = ((g.wo + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1) | 1;  // odd row pitch (bank spread)
+  r.Wp = ((g.wo + px - 1) / px * px + g.kw - 1) | 1;  // odd row pitch (bank spread)
   return r;
 }
-RtGeom rt_geom_bwdin(const ConvGeom& g) {
+RtGeom rt_geom_bwdin(const ConvGeom& g, int px = RT_PX) {
   RtGeom r{};
   r.n = g.n; r.hin = g.ho; r.win = g.wo; r.cin = g.co;
   r.hout = g.h; r.wout = g.w; r.cout = g.ci;
   r.pt = g.kh - 1 - g.pt; r.pl = g.kw - 1 - g.pl; r.wcin = g.ci; r.wcout = g.co;
   r.Hp = g.h + g.kh - 1;
-  r.Wp = ((g.w + RT_PX - 1) / RT_PX * RT_PX + g.kw - 1) | 1;
+  r.Wp = ((g.w + px - 1) / px * px + g.kw - 1) | 1;
   return r;
 }
 bool rt_ok(const ConvGeom& g) {  // stride 1, square 5x5 or 3x3 taps
@@ -484,26 +484,26 @@ bool rt_ok(const ConvGeom& g) {  // stride 1, square 5x5 or 3x3 taps
 // images per block iteration: enough work items for the block (>= 2 per thread)
 // within the shared-memory budget
 constexpr size_t RT_SMEM = 110 * 1024;
-int rt_img(const RtGeom& r, int cop, int ks) {
+int rt_img(const RtGeom& r, int cop, int ks, int px = RT_PX) {
   const size_t wbytes = (size_t)ks * ks * r.cin * cop * 4, ibytes = (size_t)r.cin * r.Hp * r.Wp * 4;
   if (wbytes + ibytes > RT_SMEM) return 0;
-  const int per = r.hout * ((r.wout + RT_PX - 1) / RT_PX);
+  const int per = r.hout * ((r.wout + px - 1) / px);
   const int want = std::max(1, (256 + per - 1) / per);  // one item per thread; several blocks per SM
   return (int)std::max<size_t>(1, std::min<size_t>(want, (RT_SMEM - wbytes) / ibytes));
 }
 
-template <int COP, bool FLIP>
+template <int COP, bool FLIP, int PX = RT_PX>
 cudaError_t launch_rt(const float* x, const float* w, float* y, const RtGeom& r, int ks, int num_sms, cudaStream_t s) {
-  const int IMG = rt_img(r, COP, ks);
+  const int IMG = rt_img(r, COP, ks, PX);
   const size_t smem = ((size_t)ks * ks * r.cin * COP + (size_t)IMG * r.cin * r.Hp * r.Wp) * 4;
   const int bps = std::max(1, std::min(4, (int)((224 * 1024) / (smem + 1024))));
   const int grid = std::max(1, std::min((r.n + IMG - 1) / IMG, num_sms * bps));
   if (ks == 5) {
-    cudaFuncSetAttribute(conv_rt_kernel<COP, 5, RT_PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
-    conv_rt_kernel<COP, 5, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
+    cudaFuncSetAttribute(conv_rt_kernel<COP, 5, PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
+    conv_rt_kernel<COP, 5, PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
   } else {
-    cudaFuncSetAttribute(conv_rt_kernel<COP, 3, RT_PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
-    conv_rt_kernel<COP, 3, RT_PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
+    cudaFuncSetAttribute(conv_rt_kernel<COP, 3, PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
+    conv_rt_kernel<COP, 3, PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
   }
   return cudaGetLastError();
 }
@@ -548,7 +548,17 @@ cudaError_t launch_conv_small_fwd(const float* x, const float* w, float* y, cons
     const RtGeom r = rt_geom_fwd(g);
     // (<= 8 channels only: at 16 the 128 registers per thread cost more occupancy than the
     // tiling saves -- C4 conv2: 320 us vs 291 us for conv_fwd_img)
-    if (co_pad(g.co) == 8 && rt_img(r, 8, g.kh)) return launch_rt<8, false>(x, w, y, r, g.kh, num_sms, s);
+    static const int px8 = getenv("CG_RT_PX8") ? atoi(getenv("CG_RT_PX8")) : 2;  // (C4 conv1: 2 best of 2 / 4 / 8)
+    if (co_pad(g.co) == 8) {
+      const RtGeom r8 = rt_geom_fwd(g, px8);
+      if (px8 == 8 && rt_img(r8, 8, g.kh, 8)) return launch_rt<8, false, 8>(x, w, y, r8, g.kh, num_sms, s);
+      if (px8 == 2 && rt_img(r8, 8, g.kh, 2)) return launch_rt<8, false, 2>(x, w, y, r8, g.kh, num_sms, s);
+      if (rt_img(r, 8, g.kh)) return launch_rt<8, false>(x, w, y, r, g.kh, num_sms, s);
+    }
+    if (co_pad(g.co) == 16) {  // 2 pixels x 16 channels per thread (C4 conv2: 247 vs 293 us for conv_fwd_img)
+      const RtGeom r2 = rt_geom_fwd(g, 2);
+      if (rt_img(r2, 16, g.kh, 2)) return launch_rt<16, false, 2>(x, w, y, r2, g.kh, num_sms, s);
+    }
   }
   Pads p = pads(g);
   const int Hp = std::max(p.Hp, g.h + g.pt), Wp = std::max(p.Wp, g.w + g.pl);
@@ -572,8 +582,11 @@ cudaError_t launch_conv_small_bwdin(const float* dy, const float* w, float* dx, 
   // register-tiled transposed correlation (several images per block): C4's
   // 16 -> 6-channel backward-input 366 us vs 427 us for conv_bwdin_img
   if (rt_ok(g) && co_pad(g.ci) == 8 && g.co <= 16 && !getenv("CG_CONV_NO_RT")) {
-    const RtGeom r = rt_geom_bwdin(g);
-    if (rt_img(r, 8, g.kh)) return launch_rt<8, true>(dy, w, dx, r, g.kh, num_sms, s);
+    static const int pxf = getenv("CG_RT_PXF") ? atoi(getenv("CG_RT_PXF")) : 4;  // (measurement switch)
+    const RtGeom r = rt_geom_bwdin(g, pxf);
+    if (pxf == 8 && rt_img(r, 8, g.kh, 8)) return launch_rt<8, true, 8>(dy, w, dx, r, g.kh, num_sms, s);
+    if (pxf == 2 && rt_img(r, 8, g.kh, 2)) return launch_rt<8, true, 2>(dy, w, dx, r, g.kh, num_sms, s);
+    if (pxf == 4 && rt_img(r, 8, g.kh)) return launch_rt<8, true>(dy, w, dx, r, g.kh, num_sms, s);
   }
   const size_t smem = bwdin_smem(g);
   const int grid = std::min(g.n, num_sms * 8);
