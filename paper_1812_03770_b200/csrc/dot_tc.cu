@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           hv[k] = h;
         }
         const uint32_t ta = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(ACOL + l * 2 * BK);
-        tmem_st32(ta, hv);
+        if (raw_hi != 7) tmem_st32(ta, hv);  // (7: measurement probe without the hi store)
         if (raw_hi != 2) tmem_st32(ta + BK, lv);
         __syncwarp();
         if (lane == 0) mbar_arrive(emptyA(sa));  // the row is in registers / TMEM: A slot free

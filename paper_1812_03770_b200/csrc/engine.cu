@@ -102,6 +102,16 @@ int compile_kernel(const KernelSpec& ks, cudaKernel_t* out, std::string* err, bo
   std::vector<char> cubin(n);
   nvrtcGetCUBIN(prog, cubin.data());
   nvrtcDestroyProgram(&prog);
+  if (const char* dir = getenv("CG_DUMP_KERNELS")) {  // inspection: <dir>/<name>.cu and .cubin
+    if (FILE* f = fopen((std::string(dir) + "/" + ks.name + ".cu").c_str(), "w")) {
+      fwrite(ks.source.data(), 1, ks.source.size(), f);
+      fclose(f);
+    }
+    if (FILE* f = fopen((std::string(dir) + "/" + ks.name + ".cubin").c_str(), "wb")) {
+      fwrite(cubin.data(), 1, cubin.size(), f);
+      fclose(f);
+    }
+  }
   cudaLibrary_t lib;
   cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e != cudaSuccess) { *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e); return CG_E_CUDA; }
