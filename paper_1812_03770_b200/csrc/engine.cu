@@ -300,6 +300,23 @@ static void fuse_epilogues(cg_graph* g) {
       prev = m;
     }
     if (!ok || prev != E.sink) continue;
+    // The fused kernel writes the sink's block at gd's position in Gamma, while the
+    // plan gives that block to the sink only at ge's: unless the sink slid into d's
+    // block, no group strictly between the two may touch the block (its previous
+    // occupant may still be read there).
+    {
+      const int B = hg.pl.block_of[E.sink];
+      bool clash = false;
+      if (B != hg.pl.block_of[d]) {
+        for (int gm = (int)gd + 1; gm < ge && !clash; ++gm) {
+          for (int p : hg.groups[gm].inputs)
+            if (!hg.is_external(p) && hg.pl.block_of[p] == B) clash = true;
+          for (int m : hg.groups[gm].materialised)
+            if (hg.pl.block_of[m] == B) clash = true;
+        }
+      }
+      if (clash) continue;
+    }
     plan->epi = prog;
     plan->C = g->ptr[E.sink];
     g->glaunch[ge].clear();
