@@ -171,6 +171,14 @@ struct cg_graph {
   int full_kernels = 0;
   // CUDA graphs of incremental evaluations, keyed by the set of groups relaunched
   std::map<std::vector<char>, std::pair<cudaGraphExec_t, int>> exec_part;
+  // concurrent capture: per group the pool blocks it reads / writes (fused pairs
+  // folded into the producer), workspace use, collective; side streams + events
+  std::vector<std::vector<int>> rd_blocks, wr_blocks;
+  std::vector<char> uses_ws, is_coll;
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> gev;
+  cudaEvent_t ev_fork = nullptr;
+  int n_streams = 1;
   int64_t launches = 0;
   int n_kernels = 0;
   // f2 epilogue fusion: tensor-core plan per group; partner[g] = the fused elementwise
@@ -335,11 +343,14 @@ static int build_launches(cg_graph* g) {
   size_t ws_need = 0;
   std::vector<KernelSpec> specs(hg.groups.size());
   // 1) specs + workspace sizes
+  g->uses_ws.assign(hg.groups.size(), 0);
   for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
     const Group& G = hg.groups[gi];
+    const size_t ws_before = ws_need;
     if (G.kind == G_EW || G.kind == G_RED) {
       specs[gi] = gen_group(hg, G, g->num_sms);
       ws_need = std::max<size_t>(ws_need, specs[gi].ws_floats);
+      g->uses_ws[gi] = specs[gi].ws_floats > 0;
     } else if (hg.nodes[G.sink].op == CG_DOT) {
       const Node& nd = hg.nodes[G.sink];
       const Shape& as = hg.nodes[nd.preds[0]].shape;
@@ -359,6 +370,12 @@ static int build_launches(cg_graph* g) {
       ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
       ws_need = std::max(ws_need, conv_small_bwdk_ok(cgm) ? conv_small_bwdk_ws(cgm, g->num_sms)
                                                           : conv2d_bwd_kernel_ws(cgm, g->num_sms));
+    }
+    // conservative: any group of a kind that may take partials in the workspace
+    if (G.kind != G_EW && G.kind != G_RED) {
+      const int op = hg.nodes[G.sink].op;
+      g->uses_ws[gi] = op == CG_DOT || op == CG_CONV2D || op == CG_CONV2D_BWD_KERNEL || op == CG_CONV2D_BWD_INPUT ||
+                       ws_need > ws_before;
     }
   }
   if (ws_need) {
@@ -561,6 +578,22 @@ static int build_launches(cg_graph* g) {
   }
   (void)n;
   fuse_epilogues(g);
+  // block access sets for the concurrent capture (values of the fused-away DOT/CONV
+  // output d are never touched; a fused chain's writes happen in its producer group)
+  const size_t NG = hg.groups.size();
+  g->rd_blocks.assign(NG, {});
+  g->wr_blocks.assign(NG, {});
+  g->is_coll.assign(NG, 0);
+  for (size_t gi = 0; gi < NG; ++gi) {
+    const Group& G = hg.groups[gi];
+    if (hg.nodes[G.sink].op == CG_ALLREDUCE_SUM) g->is_coll[gi] = 1;
+    const bool chain_of_fused = g->partner[gi] >= 0 && g->glaunch[gi].empty();
+    const int host = chain_of_fused ? g->partner[gi] : (int)gi;  // where the accesses happen
+    for (int p : G.inputs)
+      if (!hg.is_external(p) && !g->fused_away[p] && hg.pl.block_of[p] >= 0) g->rd_blocks[host].push_back(hg.pl.block_of[p]);
+    for (int m : G.materialised)
+      if (!g->fused_away[m] && hg.pl.block_of[m] >= 0) g->wr_blocks[host].push_back(hg.pl.block_of[m]);
+  }
   return 0;
 }
 
@@ -647,6 +680,90 @@ static void mark_dirty_from_var(cg_graph* g, int var) {
   for (int n : g->hg.desc_of_var[var]) g->dirty[n] = 1;
 }
 
+// Enqueue the groups of R (Gamma order) while a capture is active on g->stream.
+// With n_streams > 1, groups go to several streams: a group waits (event edges in
+// the captured graph) for the last writer of every block it reads, for the last
+// writer and all readers since of every block it writes (Alg. 1 reuses blocks:
+// write-after-read), for the previous workspace user, and collectives are full
+// barriers (every rank issues them in the same order).  Independent branches of
+// the graph then overlap; with one stream this is the sequential Gamma order.
+static bool enqueue_groups(cg_graph* g, const std::vector<char>* R, int* kcount) {
+  HostGraph& hg = g->hg;
+  const size_t NG = hg.groups.size();
+  const int NS = g->n_streams;
+  if (NS <= 1) {
+    for (size_t gi = 0; gi < NG; ++gi) {
+      if (R && !(*R)[gi]) continue;
+      for (auto& L : g->glaunch[gi]) {
+        if (L.fn(g->stream) != cudaSuccess) return false;
+        *kcount += L.kernels;
+      }
+    }
+    return true;
+  }
+  std::vector<cudaStream_t> st(NS);
+  st[0] = g->stream;
+  for (int k = 1; k < NS; ++k) st[k] = g->side[k - 1];
+  if (cudaEventRecord(g->ev_fork, g->stream) != cudaSuccess) return false;
+  for (int k = 1; k < NS; ++k)
+    if (cudaStreamWaitEvent(st[k], g->ev_fork, 0) != cudaSuccess) return false;
+  std::map<int, int> last_writer;                 // block -> group
+  std::map<int, std::vector<int>> readers;        // block -> groups reading it since its last write
+  std::vector<int> on(NG, -1), stream_last(NS, -1);
+  int last_ws = -1, last_coll = -1;
+  std::vector<int> issued;
+  for (size_t gi = 0; gi < NG; ++gi) {
+    if (R && !(*R)[gi]) continue;
+    std::vector<int> deps;
+    for (int b : g->rd_blocks[gi]) {
+      auto it = last_writer.find(b);
+      if (it != last_writer.end()) deps.push_back(it->second);
+    }
+    for (int b : g->wr_blocks[gi]) {
+      auto it = last_writer.find(b);
+      if (it != last_writer.end()) deps.push_back(it->second);
+      auto rt = readers.find(b);
+      if (rt != readers.end()) deps.insert(deps.end(), rt->second.begin(), rt->second.end());
+    }
+    if (g->uses_ws[gi] && last_ws >= 0) deps.push_back(last_ws);
+    if (last_coll >= 0) deps.push_back(last_coll);
+    if (g->is_coll[gi]) deps = issued;  // barrier
+    deps.erase(std::remove(deps.begin(), deps.end(), (int)gi), deps.end());
+    std::sort(deps.begin(), deps.end());
+    deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+    // stream: continue the chain of the latest dependency when it is that stream's tail,
+    // else the stream whose tail is oldest; collectives stay on the main stream
+    int s_ = -1;
+    if (g->is_coll[gi]) s_ = 0;
+    else if (!deps.empty() && stream_last[on[deps.back()]] == deps.back()) s_ = on[deps.back()];
+    else {
+      s_ = 0;
+      for (int k = 1; k < NS; ++k)
+        if (stream_last[k] < stream_last[s_]) s_ = k;
+    }
+    for (int d : deps)
+      if (on[d] != s_ && cudaStreamWaitEvent(st[s_], g->gev[d], 0) != cudaSuccess) return false;
+    for (auto& L : g->glaunch[gi]) {
+      if (L.fn(st[s_]) != cudaSuccess) return false;
+      *kcount += L.kernels;
+    }
+    if (cudaEventRecord(g->gev[gi], st[s_]) != cudaSuccess) return false;
+    on[gi] = s_;
+    stream_last[s_] = (int)gi;
+    issued.push_back((int)gi);
+    for (int b : g->rd_blocks[gi]) readers[b].push_back((int)gi);
+    for (int b : g->wr_blocks[gi]) {
+      last_writer[b] = (int)gi;
+      readers[b].clear();
+    }
+    if (g->uses_ws[gi]) last_ws = (int)gi;
+    if (g->is_coll[gi]) last_coll = (int)gi;
+  }
+  for (int k = 1; k < NS; ++k)  // join
+    if (stream_last[k] >= 0 && cudaStreamWaitEvent(g->stream, g->gev[stream_last[k]], 0) != cudaSuccess) return false;
+  return true;
+}
+
 static int run_launches(cg_graph* g, const std::vector<char>& R, bool full) {
   HostGraph& hg = g->hg;
   if (full && !g->graph_failed && !getenv("CG_DEBUG_CLOBBER")) {
@@ -654,11 +771,7 @@ static int run_launches(cg_graph* g, const std::vector<char>& R, bool full) {
       cudaGraph_t graph;
       bool ok = cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
       int kcount = 0;
-      for (size_t gi = 0; ok && gi < hg.groups.size(); ++gi)
-        for (auto& L : g->glaunch[gi]) {
-          if (L.fn(g->stream) != cudaSuccess) ok = false;
-          kcount += L.kernels;
-        }
+      ok = ok && enqueue_groups(g, nullptr, &kcount);
       cudaError_t e = cudaStreamEndCapture(g->stream, &graph);
       ok = ok && e == cudaSuccess;
       if (ok) {
@@ -691,13 +804,7 @@ static int run_launches(cg_graph* g, const std::vector<char>& R, bool full) {
       cudaGraphExec_t exec = nullptr;
       bool ok = cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
       int kcount = 0;
-      for (size_t gi = 0; ok && gi < hg.groups.size(); ++gi) {
-        if (!R[gi]) continue;
-        for (auto& L : g->glaunch[gi]) {
-          if (L.fn(g->stream) != cudaSuccess) ok = false;
-          kcount += L.kernels;
-        }
-      }
+      ok = ok && enqueue_groups(g, &R, &kcount);
       cudaError_t e = cudaStreamEndCapture(g->stream, &graph);
       ok = ok && e == cudaSuccess;
       if (ok) {
@@ -886,6 +993,17 @@ int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint3
     if ((r = allocate(g)) < 0) return r;
     if ((r = build_launches(g)) < 0) return r;
     if ((r = setup_updates(g)) < 0) return r;
+    // concurrent capture (CG_STREAMS, default 1: Gamma order on one stream)
+    const char* ns_env = getenv("CG_STREAMS");
+    g->n_streams = std::max(1, std::min(8, ns_env ? atoi(ns_env) : 1));
+    if (g->n_streams > 1) {
+      g->side.resize(g->n_streams - 1);
+      for (auto& st : g->side)
+        CUDA_TRY(g, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate(side)");
+      g->gev.resize(hg.groups.size());
+      for (auto& ev : g->gev) CUDA_TRY(g, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+      CUDA_TRY(g, cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+    }
   }
   g->dirty.assign(hg.nodes.size(), 1);
   g->owner.assign(hg.pl.size.size(), -1);
@@ -1039,6 +1157,9 @@ void cg_destroy(cg_graph* g) {
     if (g->exec_full) cudaGraphExecDestroy(g->exec_full);
     for (auto& kv : g->exec_part)
       if (kv.second.first) cudaGraphExecDestroy(kv.second.first);
+    for (cudaStream_t st : g->side) cudaStreamDestroy(st);
+    for (cudaEvent_t ev : g->gev) cudaEventDestroy(ev);
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
     cudaFree(g->pool);
     cudaFree(g->arena);
     cudaFree(g->ws);

@@ -740,3 +740,32 @@ def test_conv_bn_relu_epilogue_fusion(xs, ws):
     yv = evaluate(og, {ox: spec_vals["x"], ow: spec_vals["w"]})[oy]
     want = np.maximum(((((yv - mean) / sd) * gamma) + beta).astype(np.float32), 0)
     assert normwise(g.read(out), want) <= 5e-5
+
+
+def _run_training_state(spec, iters):
+    g, outs, _, _ = gpu_graph(spec, 0)
+    per = {n["name"]: n["data"] for n in spec["nodes"] if n.get("name") in spec["meta"]["per_iteration"]}
+    name_to_id = {n["name"]: n["id"] for n in spec["nodes"] if n["op"] == "VAR"}
+    for it in range(iters):
+        for name, d in per.items():
+            i = name_to_id[name]
+            g.assign(i, materialise(retag(d, f"{d['tag']}@{it}"), spec["nodes"][i]["shape"]))
+        g.eval(outs)
+    vals = [g.read(o) for o in outs] + [g.read(i) for i in name_to_id.values()]
+    g.destroy()
+    return vals
+
+
+@pytest.mark.parametrize("which", ["c3", "c4"])
+def test_concurrent_capture_bit_identical(which, monkeypatch):
+    """CG_STREAMS=4 captures independent groups on several streams (block-reuse,
+    workspace and collective dependencies as graph edges).  The kernels and their
+    internal summation orders are unchanged, so any missing dependency (a race)
+    shows up as a bit difference against the one-stream Gamma order."""
+    spec = configs.c3(batch=512, widths=(784, 256, 128, 10)) if which == "c3" else configs.c4(batch=128)
+    monkeypatch.setenv("CG_STREAMS", "1")
+    ref = _run_training_state(spec, 4)
+    monkeypatch.setenv("CG_STREAMS", "4")
+    got = _run_training_state(spec, 4)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
