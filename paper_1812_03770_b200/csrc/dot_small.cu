@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 
 #include "dot_small.h"
@@ -33,7 +34,7 @@ constexpr int NMAX = 32;
 // outstanding per SM to cover HBM latency.
 constexpr int RK = 8;  // float4 per lane per row held in registers (K <= 1024)
 template <int NT>
-__global__ void __launch_bounds__(256) dot_smalln_rows(const float* __restrict__ A, const float* __restrict__ B,
+__global__ void __launch_bounds__(NT >= 32 ? 256 : 512) dot_smalln_rows(const float* __restrict__ A, const float* __restrict__ B,
                                                        float* __restrict__ C, int M, int N, int K, int tb, int kc) {
   extern __shared__ float bs[];  // [NT][kc + 4] : op(B)^T chunk
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
@@ -397,9 +398,10 @@ cudaError_t launch_rows(const float* A, const float* B, float* C, int M, int N, 
     cudaFuncSetAttribute(dot_smalln_rows<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  const int warps = 8;
-  // few blocks, many rows each: op(B)^T is staged once per block and reused
-  const int blocks_per_sm = std::max(1, std::min(4, (int)(227 * 1024 / std::max<size_t>(smem, 1))));
+  // one 16-warp block per SM: op(B)^T is staged once per SM (not once per 16 rows --
+  // the staging was the kernel's cost) and every warp walks its rows two at a time
+  const int warps = NT >= 32 ? 8 : 16;  // (32 accumulators x 2 rows need the registers of 8 warps)
+  const int blocks_per_sm = warps >= 16 ? 1 : std::max(1, std::min(4, (int)(227 * 1024 / std::max<size_t>(smem, 1))));
   int grid = std::min((M + 2 * warps - 1) / (2 * warps), num_sms * blocks_per_sm);
   dot_smalln_rows<NT><<<grid, warps * 32, smem, s>>>(A, B, C, M, N, K, tb, kc);
   return cudaGetLastError();
