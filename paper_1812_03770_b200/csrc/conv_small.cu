@@ -25,6 +25,13 @@ namespace {
 
 constexpr int SMEM_LIMIT = 96 * 1024;
 
+// a / d for 0 <= a < 2^20 and 1 <= d <= 256 from a precomputed fp32 1/d (exact:
+// checked exhaustively for those ranges) -- the loaders' index math was the
+// instruction count of the few-channel kernels (runtime integer divisions)
+__device__ __forceinline__ int fdivs(int a, float inv) {
+  return __float2int_rd(__fmul_rn(__fadd_rn(__int2float_rn(a), 0.5f), inv));
+}
+
 // zero-padded image n of x [N,H,W,C] into s, channel-planar [C][Hp][Wp] so that
 // threads on adjacent pixels read adjacent words (no bank conflicts)
 template <int U = 8>  // loads in flight per thread
@@ -32,6 +39,7 @@ __device__ __forceinline__ void load_padded(float* s, const float* __restrict__ 
                                             int Wp, int pt, int pl) {
   const int tot = Hp * Wp * C;
   const float* xi = x + (size_t)n * H * W * C;
+  const float invC = 1.f / (float)C, invWp = 1.f / (float)Wp;
   // e walks the NHWC source order (coalesced); U loads in flight per thread
   for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
     float v[U];
@@ -39,7 +47,7 @@ __device__ __forceinline__ void load_padded(float* s, const float* __restrict__ 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int e = e0 + u * blockDim.x;
-      const int c = e % C, q = e / C, wp = q % Wp, hp = q / Wp;
+      const int q = fdivs(e, invC), c = e - q * C, hp = fdivs(q, invWp), wp = q - hp * Wp;
       const int h = hp - pt, w = wp - pl;
       dst[u] = e < tot ? (c * Hp + hp) * Wp + wp : -1;
       v[u] = (e < tot && h >= 0 && h < H && w >= 0 && w < W) ? __ldg(xi + ((size_t)h * W + w) * C + c) : 0.f;
@@ -53,12 +61,13 @@ __device__ __forceinline__ void load_padded(float* s, const float* __restrict__ 
 // dy image [P][C] -> shared [P][C4] (channels zero-padded to C4), 8 loads in flight
 __device__ __forceinline__ void load_dy_padded(float* ds, const float* __restrict__ dyi, int P, int C, int C4) {
   const int tot = P * C4;
+  const float invC4 = 1.f / (float)C4;
   for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * blockDim.x) {
     float v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = e0 + u * blockDim.x;
-      const int c = e % C4, p = e / C4;
+      const int p = fdivs(e, invC4), c = e - p * C4;
       v[u] = (e < tot && c < C) ? __ldg(dyi + (size_t)p * C + c) : 0.f;
     }
 #pragma unroll
@@ -283,6 +292,7 @@ __global__ void __launch_bounds__(256) conv_rt_kernel(const float* __restrict__ 
   for (int e = threadIdx.x; e < IMG * IS; e += blockDim.x) xs[e] = 0.f;
   const int per = g.hout * ((g.wout + PX - 1) / PX);
   const int isz = g.hin * g.win * g.cin;
+  const float invC = 1.f / (float)g.cin, invW = 1.f / (float)g.win, invH = 1.f / (float)g.hin;
   for (int n0 = blockIdx.x * IMG; n0 < g.n; n0 += gridDim.x * IMG) {
     const int nimg = min(IMG, g.n - n0);
     __syncthreads();
@@ -300,7 +310,14 @@ __global__ void __launch_bounds__(256) conv_rt_kernel(const float* __restrict__ 
       for (int u = 0; u < 8; ++u) {
         const int e = e0 + u * 256;
         if (e < tot) {
-          const int c = e % g.cin, q = e / g.cin, ww = q % g.win, q2 = q / g.win, h = q2 % g.hin, im = q2 / g.hin;
+          int c, ww, h, im;
+          if (tot < (1 << 20)) {  // fp32-reciprocal divisions (exact in this range)
+            const int q = fdivs(e, invC), q2 = fdivs(q, invW);
+            c = e - q * g.cin, ww = q - q2 * g.win, im = fdivs(q2, invH), h = q2 - im * g.hin;
+          } else {
+            const int q = e / g.cin, q2 = q / g.win;
+            c = e - q * g.cin, ww = q - q2 * g.win, im = q2 / g.hin, h = q2 - im * g.hin;
+          }
           xs[im * IS + (c * g.Hp + h + g.pt) * g.Wp + ww + g.pl] = v[u];
         }
       }
