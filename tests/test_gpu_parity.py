@@ -187,7 +187,8 @@ def test_dot_integer_exact(m, n, k, ta, tb):
 # shapes the tcgen05 path takes (16-byte row pitches), with ragged M / N / K tails
 TC_SHAPES = [(128, 128, 32), (300, 136, 100), (129, 260, 36), (784, 1024, 512), (4096, 1024, 784),
              (40000, 512, 36),  # 128x256 tiles
-             (1000, 48, 100), (500, 64, 64)]  # 128x64 tiles
+             (1000, 48, 100), (500, 64, 64),  # 128x64 tiles
+             (4100, 1024, 64), (19000, 256, 40)]  # CTA pairs with a ragged last 256-row tile
 
 
 @pytest.mark.parametrize("m,n,k", TC_SHAPES)
