@@ -228,7 +228,15 @@ def run_c2(args):
 
     secondary = None
     if not args.no_secondary:
-        secondary = run_secondary(rank, world, local, max(5, args.steps))
+        # the C2 line must survive a failure in the secondary configs (e.g. an NCCL
+        # communicator that cannot be created on some box); a failure that every
+        # rank sees identically (setup) keeps the ranks in step
+        try:
+            secondary = run_secondary(rank, world, local, max(5, args.steps))
+        except Exception as exc:  # noqa: BLE001
+            import traceback
+            traceback.print_exc(file=sys.stderr)
+            secondary = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank == 0:
         hbm, how = peaks()
