@@ -25,9 +25,11 @@ namespace {
 
 constexpr int SMEM_LIMIT = 96 * 1024;
 
-// a / d for 0 <= a < 2^20 and 1 <= d <= 256 from a precomputed fp32 1/d (exact:
-// checked exhaustively for those ranges) -- the loaders' index math was the
-// instruction count of the few-channel kernels (runtime integer divisions)
+// a / d (0 <= a < 2^20, d >= 1) from a precomputed fp32 1/d: (a + 0.5) is exact and
+// at least 0.5 from a multiple of d, while the two roundings perturb the quotient by
+// < 2^-23 relative, i.e. < 0.5 / d for a < 2^22 -- so the floor is exact (also
+// checked exhaustively for d <= 256).  The loaders' runtime integer divisions were
+// the instruction count of the few-channel kernels.
 __device__ __forceinline__ int fdivs(int a, float inv) {
   return __float2int_rd(__fmul_rn(__fadd_rn(__int2float_rn(a), 0.5f), inv));
 }
