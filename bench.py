@@ -1,23 +1,30 @@
 """Benchmark of the hot path: evaluate an optimised computation graph on B200.
 
 Default workload (BASELINE.json configs[1], the metric's "fused graph-eval HBM
-GB/s"): C2, the 20-op elementwise/broadcast chain on a [2^18, 1024] fp32
-ndarray per GPU, optimised to 17 ops in ONE generated kernel.  A "step" is
-one full cg_eval "without reusing pre-computed nodes" (the paper's protocol,
-P:385) — CG_EVAL_FULL — with inputs resident in HBM.  Multi-GPU: element-range
-sharding (each rank owns its own [2^18, 1024] row range of an N x larger
-global array; no collective on the data path) => "scaling": "weak".
+GB/s"): C2, the 20-op elementwise/broadcast chain on the fixed [2^18, 1024]
+fp32 ndarrays, optimised to 17 ops in ONE generated kernel.  A "step" is one
+full cg_eval "without reusing pre-computed nodes" (the paper's protocol,
+P:385) — CG_EVAL_FULL — with inputs resident in HBM.
+
+Multi-GPU, one process per GPU: C2 is sharded by element range —
+rank r owns rows [r*R/P, (r+1)*R/P) of the FIXED global arrays, no collective
+("scaling": "strong"); a weak-scaled C2 (every rank its own 2^18 rows) is a
+labelled secondary.  C3 / C4 are batch data-parallel (global batch 4096 / 8192
+split over the ranks, NCCL AllReduce nodes batched by the executor); C5 is
+batch-sharded replicas.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config C2|C1|C3|C4]
 
-Prints ONE JSON line on rank 0.
+With --gpus N > 1 and no torchrun environment the script re-launches itself
+under torch.distributed.run with N ranks.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -27,15 +34,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-HBM_FALLBACK_GBS = 6650.0
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+BF16_FALLBACK_TFLOPS = 1650.0
 
 
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return float(d.get("hbm_gbs", HBM_FALLBACK_GBS)), "measured"
-    return HBM_FALLBACK_GBS, "fallback"
+        return {"hbm_gbs": float(d.get("hbm_gbs", HBM_FALLBACK_GBS)),
+                "bf16_tflops": float(d.get("bf16_tflops", BF16_FALLBACK_TFLOPS)),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d.get("bf16_tflops", 0.0))),
+                "source": "MEASURED_PEAKS.json"}
+    return {"hbm_gbs": HBM_FALLBACK_GBS, "bf16_tflops": BF16_FALLBACK_TFLOPS,
+            "bf16_tflops_sustained": BF16_FALLBACK_TFLOPS, "source": "B200_PROFILING.md fallback"}
 
 
 class Clocks:
@@ -48,7 +60,7 @@ class Clocks:
     def __init__(self, device_index: int):
         self.dev = device_index
         self.p = None
-        self.path = os.path.join("/tmp", f"cg_clocks_{os.getpid()}.csv")
+        self.path = os.path.join("/tmp", f"cg_clocks_{os.getpid()}_{device_index}.csv")
 
     def start(self):
         try:
@@ -58,6 +70,7 @@ class Clocks:
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
+        return self
 
     def stop(self):
         if not self.p:
@@ -87,13 +100,51 @@ class Clocks:
 
 
 def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
 
-# ---------------------------------------------------------------------------- oracle (CPU) arm
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N without a torchrun environment: run this script under
+    torch.distributed.run with N ranks (one per GPU) and return its exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def host_info():
+    """Host side of the CPU baseline: core count, BLAS build and thread pools."""
+    info = {"os_cpu_count": os.cpu_count(), "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS")}
+    try:
+        import numpy as np
+        info["numpy"] = np.__version__
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{"api": p.get("internal_api"), "version": p.get("version"), "threads": p.get("num_threads")}
+                        for p in threadpool_info()]
+    except Exception as exc:  # noqa: BLE001
+        info["blas"] = f"unavailable: {exc}"
+    return info
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([p.get("num_threads") or 1 for p in threadpool_info()] or [1])
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------- oracle (CPU) legs
+# The oracle is the deliberately plain, slow reference (SURVEY §8(c)); bench.py
+# may execute it only here: the cpu_baseline objects and --impl reference.
 def oracle_c2_rate(budget_s=12.0, rows=2048):
     """The oracle as it stands (plain eager f64 interpreter), on a bounded row sample
     of the C2 workload; returns (GB/s algorithmic, sample description, seconds)."""
@@ -115,64 +166,241 @@ def oracle_c2_rate(budget_s=12.0, rows=2048):
     return gbs, f"C2 chain on a [{rows}, 1024] row sample, {n} eager evals ({dt * 1e3:.1f} ms each)", dt
 
 
+def oracle_secondary(name):
+    """Oracle timing for the training / inference configs on a bounded sample:
+    C3 10 full iterations (batch 4096); C4 2 iterations of a 1024-image sub-batch;
+    C5 images {0, 255} (inference is independent per image)."""
+    from oracle.eager import evaluate, leaf_values, run_iterations
+    from oracle.graph import from_spec
+    from workloads import configs
+    from workloads.gen import materialise
+    if name == "C3":
+        spec = configs.c3()
+        og, oo = from_spec(spec)
+        per = {n["name"]: n["data"] for n in spec["nodes"] if n.get("name") in spec["meta"]["per_iteration"]}
+        t0 = time.perf_counter()
+        run_iterations(og, oo, 10, per)
+        dt = (time.perf_counter() - t0) / 10
+        return {"value": 1.0 / dt, "unit": "iters/s", "s_per_iter": dt, "sample": "C3 full size, 10 iterations"}
+    if name == "C4":
+        spec = configs.c4(batch=1024, batch_global=8192)
+        og, oo = from_spec(spec)
+        per = {n["name"]: n["data"] for n in spec["nodes"] if n.get("name") in spec["meta"]["per_iteration"]}
+        t0 = time.perf_counter()
+        run_iterations(og, oo, 2, per)
+        dt = (time.perf_counter() - t0) / 2 * 8  # 8 sub-batches of 1024 per global-batch iteration
+        return {"value": 1.0 / dt, "unit": "iters/s", "s_per_iter": dt,
+                "sample": "C4: 2 iterations of a 1024-image sub-batch, scaled x8 to the 8192 batch"}
+    spec = configs.c5(batch=2)
+    og, oo = from_spec(spec)
+    full = configs.c5()
+    xs = materialise(full["nodes"][0]["data"], full["nodes"][0]["shape"], rows=[0, 255])
+    vals = leaf_values(og, {0: xs})
+    t0 = time.perf_counter()
+    evaluate(og, vals)
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 / dt, "unit": "images/s", "s_per_image": dt / 2, "sample": "C5 images {0, 255}"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
     per_step = max(1.0, 60.0 / max(1, args.steps + args.warmup))
     gbs, sample, dt = oracle_c2_rate(budget_s=per_step * max(1, args.steps))
     line = {"impl": "reference", "metric": "fused graph-eval HBM GB/s", "value": gbs, "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 compute / fp32 storage",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 compute / fp32 storage",
             "data": "synthetic (seeded splitmix64, SURVEY §8(d))",
             "config": {"workload": "C2 20-op chain (oracle on a row sample)", "rows": 2048, "cols": 1024},
-            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "host": host_info()},
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-# ---------------------------------------------------------------------------- CUDA arm: C2
+# ---------------------------------------------------------------------------- helpers (CUDA arm)
+def plan_traffic_bytes(g) -> int:
+    """Algorithmic bytes of one full evaluation of the PLANNED graph: every group
+    reads each of its distinct inputs once and writes its materialised values
+    once (interior values of fused groups never touch HBM)."""
+    plan = json.loads(g.dump_json(1))
+    shapes = {}
+
+    def nbytes(v):
+        if v not in shapes:
+            shapes[v] = 4 * math.prod(g.shape(v))
+        return shapes[v]
+    return sum(sum(nbytes(p) for p in gr["inputs"]) + sum(nbytes(m) for m in gr["materialised"])
+               for gr in plan["groups"])
+
+
+def graph_flops(g, spec) -> int:
+    """Algorithmic FLOPs of the dot / conv nodes: 2*M*N*K per DOT, 2*N*Ho*Wo*Co*KH*KW*Ci
+    per convolution (forward, backward-input and backward-kernel alike)."""
+    total = 0
+    for rec in spec["nodes"]:
+        op = rec["op"]
+        if op == "DOT":
+            m, n = g.shape(rec["id"])
+            a = g.shape(rec["preds"][0])
+            total += 2 * m * n * (a[0] if rec["attrs"].get("ta") else a[1])
+        elif op == "CONV2D":
+            kh, kw, ci, co = g.shape(rec["preds"][1])
+            nb, ho, wo, _ = g.shape(rec["id"])
+            total += 2 * nb * ho * wo * co * kh * kw * ci
+        elif op == "CONV2D_BWD_INPUT":
+            nb, ho, wo, co = g.shape(rec["preds"][0])
+            kh, kw, ci, _ = g.shape(rec["preds"][1])
+            total += 2 * nb * ho * wo * co * kh * kw * ci
+        elif op == "CONV2D_BWD_KERNEL":
+            kh, kw, ci, co = g.shape(rec["id"])
+            nb, ho, wo, _ = g.shape(rec["preds"][1])
+            total += 2 * nb * ho * wo * co * kh * kw * ci
+    return total
+
+
+def measure_tf32_peak(dev):
+    """Dense TF32 tensor throughput (SURVEY §8(d) roofline denominator): torch.matmul
+    8192^3 fp32 with TF32 allowed, best of 10 (burst), CUDA events."""
+    import torch
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(3):
+            torch.matmul(a, b)
+        best = float("inf")
+        for _ in range(10):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch.matmul(a, b)
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_time(e))
+        del a, b
+        return 2 * n ** 3 / (best * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
+def _max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t[0])
+
+
+def _all_ok(ok, world):
+    """MIN over ranks of a per-rank success flag: a failure on one rank skips the
+    rest of the secondary configs on EVERY rank (no rank left waiting in a collective)."""
+    if world == 1:
+        return ok
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t[0])
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _timed(ws, fn, iters, world, local, min_s=0.6):
+    """Warm-up, a load phase of >= 0.3 s (so the sampled clocks are this kernel
+    mix's clocks), then `iters` steps (raised to fill >= min_s) timed with CUDA
+    events on the graph's work stream between barriers + synchronize; returns
+    (ms per step over ranks' max, clocks, iters)."""
+    import torch
+    for k in range(3):
+        fn(k)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fn(0)
+    torch.cuda.synchronize()
+    est = max(time.perf_counter() - t0, 1e-5)
+    iters = max(iters, int(min_s / est))
+    iters = int(_max_over_ranks(iters, world))
+    clk = Clocks(local).start()
+    t_end = time.perf_counter() + 0.3
+    k = 0
+    while time.perf_counter() < t_end:
+        fn(k)
+        k += 1
+        if k % 8 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+    _barrier(world)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(ws)
+    for k in range(iters):
+        fn(k)
+    e.record(ws)
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / iters
+    clocks = clk.stop()
+    _barrier(world)
+    return _max_over_ranks(ms, world), clocks, iters
+
+
+# ---------------------------------------------------------------------------- CUDA arm: C2 (primary)
+def build_c2(rows_local, row0, local):
+    from paper_1812_03770_b200 import cg
+    from workloads import configs
+    from workloads.gen import materialise
+    cols = configs.C2_COLS
+    spec = configs.c2(rows_local, cols)
+
+    def data(rec):
+        if rec["op"] not in ("VAR", "CONST"):
+            return None
+        shp = rec["shape"]
+        off = row0 if (len(shp) == 2 and shp[0] == rows_local) else 0
+        return materialise(rec["data"], shp, row_offset=off)
+    t0 = time.perf_counter()
+    g, outs = cg.build_from_spec(spec, device=local, data_fn=data)
+    t_gen = time.perf_counter()
+    rep = g.optimise(outs)
+    info = g.plan_memory(outs, 0)
+    build_s = time.perf_counter() - t_gen
+    return g, outs, spec, data, rep, info, build_s, t_gen - t0
+
+
 def run_c2(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_1812_03770_b200 import build as _build
     _build.build()
     from paper_1812_03770_b200 import cg
+    from paper_1812_03770_b200.dist import shard_range
     from workloads import configs
-    from workloads.gen import materialise
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rows, cols = configs.C2_ROWS, configs.C2_COLS
-    spec = configs.c2(rows, cols)
-    row0 = rank * rows  # element-range shard of the global [world*rows, cols] array
-
-    def data(rec):
-        if rec["op"] not in ("VAR", "CONST"):
-            return None
-        shp = rec["shape"]
-        off = row0 if (len(shp) == 2 and shp[0] == rows) else 0
-        return materialise(rec["data"], shp, row_offset=off)
-
-    g, outs = cg.build_from_spec(spec, device=local, data_fn=data)
-    rep = g.optimise(outs)
-    info = g.plan_memory(outs, 0)
+    rows_g, cols = configs.C2_ROWS, configs.C2_COLS
+    row0, rows = shard_range(rows_g, rank, world)  # strong scaling: a slice of the FIXED global arrays
+    g, outs, spec, data, rep, info, build_s, gen_s = build_c2(rows, row0, local)
     ws = torch.cuda.ExternalStream(g.work_stream(), device=torch.device("cuda", local))
-    algo = configs.c2_algo_bytes(rows, cols)
+    algo_local = configs.c2_algo_bytes(rows, cols)
+    algo_total = sum(configs.c2_algo_bytes(shard_range(rows_g, r, world)[1], cols) for r in range(world))
     torch.cuda.synchronize()
-    for _ in range(args.warmup):
+    for _ in range(max(3, args.warmup)):
         g.eval(outs, cg.EVAL_FULL)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = Clocks(local)
-    clocks.start()
+    _barrier(world)
+    clocks = Clocks(local).start()
     # keep the GPU under this same load for ~0.5 s before the timed region so the
     # sampled clocks are the clocks of the measured kernel (nvidia-smi samples every 100 ms)
     t_end = time.perf_counter() + 0.5
@@ -180,8 +408,7 @@ def run_c2(args):
         for _ in range(20):
             g.eval(outs, cg.EVAL_FULL)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    _barrier(world)
     torch.cuda.synchronize()
     l0 = g.launch_count()
     s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -197,20 +424,17 @@ def run_c2(args):
     ms = s_ev.elapsed_time(e_ev) / args.steps
     kernel_ms = k_s.elapsed_time(k_e) / args.steps
     clk = clocks.stop()
-    if world > 1:
-        t = torch.tensor([ms, kernel_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kernel_ms = float(t[0]), float(t[1])
-        dist.barrier()
-    value = world * algo / (ms * 1e-3) / 1e9
+    _barrier(world)
+    ms_max = _max_over_ranks(ms, world)
+    kernel_ms_max = _max_over_ranks(kernel_ms, world)
+    value = algo_total / (ms_max * 1e-3) / 1e9
 
     # e2e: through the public API with HOST buffers (pinned), copies inside the timed region
     e2e_steps = max(1, min(args.steps, 3))
     hx = torch.from_numpy(data(spec["nodes"][0])).pin_memory()
     hy = torch.from_numpy(data(spec["nodes"][1])).pin_memory()
     hout = torch.empty((rows, cols), dtype=torch.float32).pin_memory()
-    if world > 1:
-        dist.barrier()
+    _barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
@@ -219,53 +443,46 @@ def run_c2(args):
         g.eval(outs)
         g.read_into(outs[0], hout)
     torch.cuda.synchronize()
-    e2e_ms = (time.perf_counter() - t0) * 1e3 / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t[0])
-    e2e_val = world * algo / (e2e_ms * 1e-3) / 1e9
+    e2e_ms = _max_over_ranks((time.perf_counter() - t0) * 1e3 / e2e_steps, world)
+    e2e_val = algo_total / (e2e_ms * 1e-3) / 1e9
+    del hx, hy, hout
+    g.destroy()
 
     secondary = None
     if not args.no_secondary:
-        # the C2 line must survive a failure in the secondary configs (e.g. an NCCL
-        # communicator that cannot be created on some box); a failure that every
-        # rank sees identically (setup) keeps the ranks in step
-        try:
-            secondary = run_secondary(rank, world, local, max(5, args.steps))
-        except Exception as exc:  # noqa: BLE001
-            import traceback
-            traceback.print_exc(file=sys.stderr)
-            secondary = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+        secondary = run_secondary(rank, world, local, max(5, args.steps), args)
 
     if rank == 0:
-        hbm, how = peaks()
-        achieved = algo / (kernel_ms * 1e-3) / 1e9
+        pk = peaks()
+        achieved = algo_local / (kernel_ms * 1e-3) / 1e9  # rank 0's kernel: its own bytes / its own time
         traffic = None
         tp = os.path.join(ROOT, "profiles", "c2_traffic.json")
         if os.path.exists(tp):
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+            tj = json.load(open(tp))
+            # ncu captures the single-GPU kernel (2^28 elements); scale to this rank's shard
+            traffic = tj.get("dram_bytes_per_launch") * rows / rows_g if tj.get("dram_bytes_per_launch") else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             gbs, sample, _ = oracle_c2_rate(budget_s=args.cpu_budget)
-            cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample}
+            cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                   "host": host_info()}
         line = {
             "metric": "fused graph-eval HBM GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64)",
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded splitmix64)",
             "config": {"workload": "C2: 20-op elementwise/broadcast chain (CSE+CF -> 17 ops, 1 fused kernel)",
-                       "rows_per_gpu": rows, "cols": cols, "elements_per_gpu": rows * cols,
-                       "algorithmic_bytes_per_step_per_gpu": algo, "parallelism": f"element-range x{world}",
+                       "global_rows": rows_g, "cols": cols, "elements": rows_g * cols, "rows_per_gpu": rows,
+                       "algorithmic_bytes_per_step": algo_total, "parallelism": f"element-range x{world} (no collective)",
                        "l2": "3 GiB moved per step >> 126 MB L2: no flush needed",
                        "eval": "CG_EVAL_FULL (no reuse of pre-computed nodes, P:385)",
-                       "optimiser": rep, "plan": {k: info[k] for k in ("n_groups", "n_blocks", "pool_bytes",
-                                                                       "unshared_bytes")}},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "peak_source": how,
-                         "kernel_ms": kernel_ms},
+                       "build_s": build_s, "optimiser": rep,
+                       "plan": {k: info[k] for k in ("n_groups", "n_blocks", "pool_bytes", "unshared_bytes")}},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_source": pk["source"],
+                         "kernel_ms": kernel_ms, "kernel_ms_max_over_ranks": kernel_ms_max},
             "clocks": clk,
-            "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 2 * rows * cols * 4,
-                    "d2h_bytes_per_step": rows * cols * 4, "ms_per_step": e2e_ms},
+            "e2e": {"value": e2e_val, "unit": "GB/s", "h2d_bytes_per_step": 2 * rows * cols * 4 * world,
+                    "d2h_bytes_per_step": rows * cols * 4 * world, "ms_per_step": e2e_ms},
             "gpu_launches": launches,
             "cpu_baseline": cpu,
             "secondary": secondary,
@@ -276,129 +493,218 @@ def run_c2(args):
 
 
 # ---------------------------------------------------------------------------- secondary workloads
-def _time_region(ws, fn, iters):
+def run_secondary(rank, world, local, iters, args):
+    """BASELINE.json's other metrics: C1 full / incremental eval latency; C3 / C4
+    data-parallel training iterations/s (global batch fixed: strong; at N > 1 also
+    per-GPU batch fixed: weak); C5 images/s with plan peak bytes vs unshared; at
+    N > 1 a weak-scaled C2.  Each carries its own clocks and, where it applies, a
+    roofline over the whole step and an oracle timing (rank 0, N = 1)."""
+    out = {}
+    pk = peaks()
     import torch
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record(ws)
-    for k in range(iters):
-        fn(k)
-    e.record(ws)
-    torch.cuda.synchronize()
-    return s.elapsed_time(e) / iters
+    tf32 = None
+    try:
+        tf32 = measure_tf32_peak(torch.device("cuda", local))
+    except Exception as exc:  # noqa: BLE001
+        out["tf32_peak_error"] = str(exc)[:200]
+    out["peaks"] = {"tf32_tflops_measured": tf32, "hbm_gbs": pk["hbm_gbs"], "source": pk["source"],
+                    "tf32_how": "torch.matmul 8192^3 fp32, allow_tf32, best of 10"}
+    jobs = [("C1", _sec_c1), ("C3", lambda: _sec_train("C3", 4096, False)),
+            ("C4", lambda: _sec_train("C4", 8192, False)), ("C5", _sec_c5)]
+    if world > 1:
+        jobs += [("C2_weak", _sec_c2_weak), ("C3_weak", lambda: _sec_train("C3", 4096, True)),
+                 ("C4_weak", lambda: _sec_train("C4", 8192, True))]
+    ctx = {"rank": rank, "world": world, "local": local, "iters": iters, "tf32": tf32, "pk": pk}
+    for name, fn in jobs:
+        ok = True
+        try:
+            _CTX.update(ctx)
+            out[name] = fn()
+        except Exception as exc:  # noqa: BLE001
+            import traceback
+            traceback.print_exc(file=sys.stderr)
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            ok = False
+        torch.cuda.synchronize()
+        if not _all_ok(ok, world):
+            out["skipped_after"] = name
+            break
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        for name in ("C3", "C4", "C5"):
+            if isinstance(out.get(name), dict) and "error" not in out[name]:
+                try:
+                    cb = oracle_secondary(name)
+                    cb.update({"kind": "oracle", "cores": blas_threads(),
+                               "cores_note": "numpy f64; DOT/CONV through the BLAS thread pool, elementwise 1 core"})
+                    out[name]["cpu_baseline"] = cb
+                except Exception as exc:  # noqa: BLE001
+                    out[name]["cpu_baseline"] = {"error": str(exc)[:200]}
+    return out
 
 
-def _max_over_ranks(x, world):
-    if world == 1:
-        return x
+_CTX: dict = {}
+
+
+def _leaf(rec, off=0):
+    from workloads.gen import materialise
+    if rec["op"] not in ("VAR", "CONST"):
+        return None
+    return materialise(rec["data"], rec["shape"], row_offset=off)
+
+
+def _sec_c1():
     import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t[0])
+
+    from paper_1812_03770_b200 import cg
+    from workloads import configs
+    from workloads.gen import materialise, retag
+    local, world = _CTX["local"], _CTX["world"]
+    dev = torch.device("cuda", local)
+    spec = configs.c1(1024)
+    t0 = time.perf_counter()
+    g, outs = cg.build_from_spec(spec, device=local, data_fn=_leaf)
+    g.plan_memory(outs, cg.PLAN_INCREMENTAL)
+    build_s = time.perf_counter() - t0
+    ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
+    x3 = [torch.from_numpy(materialise(retag(spec["nodes"][3]["data"], f"x3#{k}"), [1024])).to(dev) for k in range(2)]
+    full_ms, clk, _ = _timed(ws, lambda k: g.eval(outs, cg.EVAL_FULL), 200, world, local, min_s=0.3)
+
+    def inc(k):
+        g.assign(3, x3[k % 2])
+        g.eval(outs)
+    inc_ms, _, _ = _timed(ws, inc, 200, world, local, min_s=0.3)
+    r = {"metric": "eval latency", "unit": "us", "full_eval_us": full_ms * 1e3,
+         "incremental_eval_us (assign x3 + eval)": inc_ms * 1e3, "x2_evaluations": g.eval_count(2),
+         "x5_evaluations": g.eval_count(5), "build_s": build_s, "clocks": clk,
+         "roofline": {"bound": "launch latency", "note": "12 KiB per eval: HBM time ~2 ns (SURVEY §8(d))"}}
+    g.destroy()
+    return r
 
 
-def run_secondary(rank, world, local, iters):
-    """BASELINE.json's other metrics on the other configs: C1 full / incremental
-    eval latency, C3 / C4 data-parallel training iterations per second (global
-    batch fixed: 4096 / 8192, split over the ranks), C5 images/s with the plan's
-    peak bytes vs the unshared (eager) allocation."""
+def _sec_train(name, gb, weak):
     import torch
 
     from paper_1812_03770_b200 import cg
     from paper_1812_03770_b200.dist import dp_spec, make_graph, shard_range
     from workloads import configs
     from workloads.gen import materialise, retag
-
-    out = {}
+    rank, world, local = _CTX["rank"], _CTX["world"], _CTX["local"]
     dev = torch.device("cuda", local)
-
-    def leaf(rec, off=0):
-        if rec["op"] not in ("VAR", "CONST"):
-            return None
-        return materialise(rec["data"], rec["shape"], row_offset=off)
-
-    # C1: Fig. 1 graph, full eval and incremental re-eval after cg_assign(x3) (P:42)
-    spec = configs.c1(1024)
-    g, outs = cg.build_from_spec(spec, device=local, data_fn=leaf)
-    g.plan_memory(outs, cg.PLAN_INCREMENTAL)
-    ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
-    x3 = [torch.from_numpy(materialise(retag(spec["nodes"][3]["data"], f"x3#{k}"), [1024])).to(dev) for k in range(2)]
-    for _ in range(5):
-        g.eval(outs, cg.EVAL_FULL)
-    torch.cuda.synchronize()
-    full_ms = _time_region(ws, lambda k: g.eval(outs, cg.EVAL_FULL), 200)
-
-    def inc(k):
-        g.assign(3, x3[k % 2])
-        g.eval(outs)
-    inc_ms = _time_region(ws, inc, 200)
-    out["C1"] = {"metric": "eval latency", "unit": "us", "full_eval_us": full_ms * 1e3,
-                 "incremental_eval_us (assign x3 + eval)": inc_ms * 1e3, "x2_evaluations": g.eval_count(2),
-                 "x5_evaluations": g.eval_count(5)}
-    g.destroy()
-
-    # C3 / C4: data-parallel training, global batch split over ranks (strong scaling)
-    for name, fn, gb in (("C3", configs.c3, 4096), ("C4", configs.c4, 8192)):
+    fn = configs.c3 if name == "C3" else configs.c4
+    if weak:  # per-GPU batch fixed at gb, global batch gb * world
+        spec = fn(batch=gb, batch_global=gb * world)
+        start = rank * gb
+        count = gb
+    else:
         spec = dp_spec(fn, gb, rank, world)
         start, count = shard_range(gb, rank, world)
-        g = make_graph(local, world, rank)
-        for rec in spec["nodes"]:
-            data = leaf(rec)
-            if rec["op"] in ("VAR", "CONST"):
-                g.add_node(rec["op"], (), dims=rec["shape"], **({"data": data} if data is not None else {}))
-            else:
-                g.add_node(rec["op"], rec["preds"], **rec.get("attrs", {}))
-        for u, v in spec["updates"]:
-            g.add_update(u, v)
-        outs = spec["outputs"]
-        g.optimise(outs)
-        info = g.plan_memory(outs, 0)
-        ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
-        ids = {n["name"]: n["id"] for n in spec["nodes"] if n["op"] == "VAR"}
-        staged = []
-        for it in range(4):
-            d = {}
-            for nm in spec["meta"]["per_iteration"]:
-                rec = spec["nodes"][ids[nm]]
-                d[ids[nm]] = torch.from_numpy(materialise(retag(rec["data"], f"{rec['data']['tag']}@{it}"),
-                                                          rec["shape"], row_offset=start)).to(dev)
-            staged.append(d)
-
-        def step(k):
-            for i, t in staged[k % 4].items():
-                g.assign(i, t)
-            g.eval(outs, cg.EVAL_FULL)
-        for k in range(3):
-            step(k)
-        torch.cuda.synchronize()
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
-        ms = _max_over_ranks(_time_region(ws, step, iters), world)
-        out[name] = {"metric": "train iters/s", "value": 1e3 / ms, "unit": "iters/s", "ms_per_iter": ms,
-                     "global_batch": gb, "local_batch": count, "scaling": "strong",
-                     "parallelism": f"dp{world}" + (" (NCCL AllReduce nodes)" if world > 1 else ""),
-                     "plan_peak_bytes": info["pool_bytes"] + info["external_bytes"] + info["workspace_bytes"],
-                     "unshared_bytes": info["unshared_bytes"] + info["external_bytes"]}
-        g.destroy()
-
-    # C5: InceptionV3 inference, 256 images per GPU (batch-sharded replicas)
-    spec = configs.c5()
-    g, outs = cg.build_from_spec(spec, device=local, data_fn=leaf)
+    t0 = time.perf_counter()
+    g = make_graph(local, world, rank)
+    for rec in spec["nodes"]:
+        data = _leaf(rec)
+        if rec["op"] in ("VAR", "CONST"):
+            g.add_node(rec["op"], (), dims=rec["shape"], **({"data": data} if data is not None else {}))
+        else:
+            g.add_node(rec["op"], rec["preds"], **rec.get("attrs", {}))
+    for u, v in spec["updates"]:
+        g.add_update(u, v)
+    outs = spec["outputs"]
     g.optimise(outs)
     info = g.plan_memory(outs, 0)
+    build_s = time.perf_counter() - t0
     ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
-    for _ in range(2):
+    ids = {n["name"]: n["id"] for n in spec["nodes"] if n["op"] == "VAR"}
+    staged = []
+    for it in range(4):
+        d = {}
+        for nm in spec["meta"]["per_iteration"]:
+            rec = spec["nodes"][ids[nm]]
+            d[ids[nm]] = torch.from_numpy(materialise(retag(rec["data"], f"{rec['data']['tag']}@{it}"),
+                                                      rec["shape"], row_offset=start)).to(dev)
+        staged.append(d)
+
+    def step(k):
+        for i, t in staged[k % 4].items():
+            g.assign(i, t)
         g.eval(outs, cg.EVAL_FULL)
-    torch.cuda.synchronize()
-    ms = _max_over_ranks(_time_region(ws, lambda k: g.eval(outs, cg.EVAL_FULL), max(2, iters // 4)), world)
+    l0 = g.launch_count()
+    ms, clk, n = _timed(ws, step, _CTX["iters"], world, local)
+    launches_per_iter = (g.launch_count() - l0) / max(1, n)
+    flops = graph_flops(g, spec)
+    traffic = plan_traffic_bytes(g)
+    ms_s = ms * 1e-3
+    r = {"metric": "train iters/s", "value": 1e3 / ms, "unit": "iters/s", "ms_per_iter": ms,
+         "global_batch": gb * world if weak else gb, "local_batch": count, "scaling": "weak" if weak else "strong",
+         "parallelism": f"dp{world}" + (" (NCCL AllReduce nodes, batched per step)" if world > 1 else ""),
+         "build_s": build_s, "clocks": clk, "launches_per_iter": launches_per_iter,
+         "plan_peak_bytes": info["pool_bytes"] + info["external_bytes"] + info["workspace_bytes"],
+         "unshared_bytes": info["unshared_bytes"] + info["external_bytes"],
+         "algorithmic_flops_per_iter": flops, "plan_traffic_bytes_per_iter": traffic,
+         "collective_batches": g.coll_batches() if world > 1 else 0}
+    pk, tf32 = _CTX["pk"], _CTX["tf32"]
+    hbm_frac = traffic / ms_s / 1e9 / pk["hbm_gbs"]
+    if name == "C3" and tf32:
+        ach = 3 * flops / ms_s / 1e12
+        r["roofline"] = {"bound": "tensor", "scope": "whole iteration (dots dominate)", "achieved": ach,
+                         "peak": tf32, "unit": "TFLOP/s", "frac": ach / tf32,
+                         "note": "3xTF32: 3 tensor-core passes per algorithmic FLOP; peak = measured TF32",
+                         "hbm_frac_of_plan_traffic": hbm_frac}
+    else:
+        r["roofline"] = {"bound": "hbm", "scope": "whole iteration", "achieved": traffic / ms_s / 1e9,
+                         "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": hbm_frac,
+                         "note": "plan traffic = each group reads its inputs and writes its materialised values once"}
+    g.destroy()
+    return r
+
+
+def _sec_c5():
+    import torch
+
+    from paper_1812_03770_b200 import cg
+    from workloads import configs
+    world, local = _CTX["world"], _CTX["local"]
+    dev = torch.device("cuda", local)
+    spec = configs.c5()
+    t0 = time.perf_counter()
+    g, outs = cg.build_from_spec(spec, device=local, data_fn=_leaf)
+    g.optimise(outs)
+    info = g.plan_memory(outs, 0)
+    build_s = time.perf_counter() - t0
+    ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
+    l0 = g.launch_count()
+    ms, clk, n = _timed(ws, lambda k: g.eval(outs, cg.EVAL_FULL), max(2, _CTX["iters"] // 4), world, local)
+    launches = (g.launch_count() - l0) / max(1, n)
     peak = info["pool_bytes"] + info["external_bytes"] + info["workspace_bytes"]
     unshared = info["unshared_bytes"] + info["external_bytes"]
-    out["C5"] = {"metric": "images/s", "value": world * 256 / (ms * 1e-3), "unit": "images/s", "ms_per_eval": ms,
-                 "batch_per_gpu": 256, "scaling": "weak", "plan_peak_bytes": peak, "unshared_bytes": unshared,
-                 "peak_vs_unshared": peak / unshared, "n_groups": info["n_groups"], "n_blocks": info["n_blocks"]}
+    flops = graph_flops(g, spec)
+    tf32 = _CTX["tf32"]
+    r = {"metric": "images/s", "value": world * 256 / (ms * 1e-3), "unit": "images/s", "ms_per_eval": ms,
+         "batch_per_gpu": 256, "scaling": "weak", "plan_peak_bytes": peak, "unshared_bytes": unshared,
+         "peak_vs_unshared": peak / unshared, "n_groups": info["n_groups"], "n_blocks": info["n_blocks"],
+         "build_s": build_s, "clocks": clk, "launches_per_eval": launches, "algorithmic_flops_per_eval": flops}
+    if tf32:
+        ach = 3 * flops / (ms * 1e-3) / 1e12
+        r["roofline"] = {"bound": "tensor", "scope": "whole evaluation (convs dominate)", "achieved": ach,
+                         "peak": tf32, "unit": "TFLOP/s", "frac": ach / tf32,
+                         "note": "3xTF32: 3 tensor-core passes per algorithmic FLOP; peak = measured TF32"}
     g.destroy()
-    return out
+    return r
+
+
+def _sec_c2_weak():
+    import torch
+
+    from paper_1812_03770_b200 import cg
+    from workloads import configs
+    rank, world, local = _CTX["rank"], _CTX["world"], _CTX["local"]
+    rows = configs.C2_ROWS
+    g, outs, _, _, _, _, build_s, _ = build_c2(rows, rank * rows, local)
+    ws = torch.cuda.ExternalStream(g.work_stream(), device=torch.device("cuda", local))
+    ms, clk, _ = _timed(ws, lambda k: g.eval(outs, cg.EVAL_FULL), 20, world, local)
+    algo = configs.c2_algo_bytes(rows)
+    g.destroy()
+    return {"metric": "fused graph-eval HBM GB/s", "value": world * algo / (ms * 1e-3) / 1e9, "unit": "GB/s",
+            "ms_per_step": ms, "scaling": "weak", "rows_per_gpu": rows, "clocks": clk, "build_s": build_s}
 
 
 def main():
@@ -407,7 +713,6 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="C2 only (skip the C1/C3/C4/C5 lines)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
@@ -415,10 +720,9 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
-    if args.config == "C2":
-        run_c2(args)
-    else:
-        raise SystemExit(f"config {args.config} not wired into bench.py yet")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch_distributed(args))
+    run_c2(args)
 
 
 if __name__ == "__main__":

@@ -223,6 +223,21 @@ int64_t cg_eval_count(const cg_graph* g, cg_node node);
 int32_t cg_node_shape(const cg_graph* g, cg_node node, int64_t* dims8);
 /* Number of device kernel launches enqueued by this graph so far. */
 int64_t cg_launch_count(const cg_graph* g);
+/* Executor order with batched collectives (the paper's "natural
+ * support for parallel and distributed computing"), on synthetic access
+ * sets: ng groups in Gamma order, active[g] (NULL: all), the pool blocks group g
+ * reads rd_idx[rd_ptr[g]:rd_ptr[g+1]] and writes wr_idx[wr_ptr[g]:wr_ptr[g+1]],
+ * uses_ws[g] (kernel workspace), is_coll[g] (ALLREDUCE_SUM).  Writes the issue
+ * order to order[] and a step id per entry to step[] (entries with one step id
+ * are collectives issued in one ncclGroupStart/End); returns the number of
+ * scheduled groups or a cg_status.  Host only; caller owns every buffer
+ * (order, step: ng entries).  The executor uses the same routine. */
+int32_t cgx_collective_schedule(int32_t ng, const uint8_t* active, const int32_t* rd_ptr,
+                                const int32_t* rd_idx, const int32_t* wr_ptr, const int32_t* wr_idx,
+                                const uint8_t* uses_ws, const uint8_t* is_coll, int32_t* order,
+                                int32_t* step);
+/* Collective batches (ncclGroupStart/End pairs) g has issued, captured ones included. */
+int64_t cgx_coll_batches(const cg_graph* g);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcg.so")
-SOURCES = ["host.cpp", "codegen.cpp", "kernels.cu", "dot_tc.cu", "dot_small.cu", "conv_small.cu", "engine.cu"]
+SOURCES = ["host.cpp", "codegen.cpp", "schedule.cpp", "kernels.cu", "dot_tc.cu", "dot_small.cu", "conv_small.cu", "engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

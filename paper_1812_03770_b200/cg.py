@@ -99,6 +99,8 @@ def lib():
             "cg_eval_count": (I64, [P, I32]),
             "cg_node_shape": (I32, [P, I32, P]),
             "cg_launch_count": (I64, [P]),
+            "cgx_collective_schedule": (I32, [I32, P, P, P, P, P, P, P, P, P]),
+            "cgx_coll_batches": (I64, [P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -127,6 +129,37 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+def collective_schedule(rd, wr, uses_ws, is_coll, active=None):
+    """cgx_collective_schedule on synthetic access sets (lists of block-id lists per
+    group).  Returns a list of steps (lists of group ids) in issue order."""
+    ng = len(rd)
+
+    def csr(sets):
+        ptr = np.zeros(ng + 1, np.int32)
+        for i, s_ in enumerate(sets):
+            ptr[i + 1] = ptr[i] + len(s_)
+        idx = np.array([b for s_ in sets for b in s_] or [0], np.int32)
+        return ptr, idx
+    rp, ri = csr(rd)
+    wp, wi = csr(wr)
+    ws = np.asarray(uses_ws, np.uint8)
+    co = np.asarray(is_coll, np.uint8)
+    act = None if active is None else np.asarray(active, np.uint8)
+    order = np.zeros(max(ng, 1), np.int32)
+    step = np.zeros(max(ng, 1), np.int32)
+    n = lib().cgx_collective_schedule(ng, None if act is None else act.ctypes.data, rp.ctypes.data, ri.ctypes.data,
+                                      wp.ctypes.data, wi.ctypes.data, ws.ctypes.data, co.ctypes.data,
+                                      order.ctypes.data, step.ctypes.data)
+    if n < 0:
+        raise CGError(n, "cgx_collective_schedule")
+    steps = []
+    for k in range(n):
+        if k == 0 or step[k] != step[k - 1]:
+            steps.append([])
+        steps[-1].append(int(order[k]))
+    return steps
+
+
 class Graph:
     """One cg_graph.  device=-1: host-only planning mode (structure only)."""
 
@@ -134,7 +167,7 @@ class Graph:
         L = lib()
         self._keep = []
         dist = None
-        if world > 1:
+        if world > 1 or nccl_id:  # world == 1 with an id: a 1-rank NCCL communicator
             self._uid = ctypes.create_string_buffer(nccl_id, 128) if nccl_id else None
             dist = cg_dist(rank, world, ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None)
         if stream is None and device >= 0:
@@ -266,6 +299,10 @@ class Graph:
 
     def launch_count(self) -> int:
         return self._check(lib().cg_launch_count(self.h))
+
+    def coll_batches(self) -> int:
+        """Collective batches (one ncclGroupStart/End each) issued so far."""
+        return self._check(lib().cgx_coll_batches(self.h))
 
     def work_stream(self) -> int:
         """cudaStream_t (as int) that every kernel of this graph is launched on."""

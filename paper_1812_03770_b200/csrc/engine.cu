@@ -10,8 +10,15 @@
 // Full evaluations replay a captured CUDA graph.
 #include <dlfcn.h>
 #include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
+#include <chrono>
+#include <set>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -31,6 +38,7 @@
 #include "dot_small.h"
 #include "dot_tc.h"
 #include "kernels.h"
+#include "schedule.h"
 
 using namespace cg;
 
@@ -45,6 +53,8 @@ struct Nccl {
   int (*CommInitRank)(void**, int, char[128], int) = nullptr;  // (comm*, nranks, uniqueId by value, rank)
   int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*CommDestroy)(void*) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
   bool load(std::string* err) {
     if (h) return true;
@@ -58,7 +68,9 @@ struct Nccl {
     AllReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
     CommDestroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
     GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
-    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy) { *err = "libnccl lacks symbols"; return false; }
+    GroupStart = (int (*)())dlsym(h, "ncclGroupStart");
+    GroupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GroupStart || !GroupEnd) { *err = "libnccl lacks symbols"; return false; }
     return true;
   }
 };
@@ -75,56 +87,161 @@ struct KCache {
 };
 KCache g_kcache;
 
-int compile_kernel(const KernelSpec& ks, cudaKernel_t* out, std::string* err, bool* fresh) {
-  {
-    std::lock_guard<std::mutex> lk(g_kcache.mu);
-    auto it = g_kcache.by_name.find(ks.name);
-    if (it != g_kcache.by_name.end()) { *out = it->second; *fresh = false; return 0; }
-  }
+// On-disk cubin cache: $CG_CACHE_DIR (empty string disables), default
+// $HOME/.cache/cg_kernels.  A file is keyed by the kernel name (hash of its body)
+// and a hash of the full source, the NVRTC options and the NVRTC version, and is
+// written by rename (atomic), so concurrent processes never read a partial file.
+const char* const kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-default-device", "--std=c++17",
+                                  "-lineinfo"};
+
+std::string cache_dir() {
+  if (const char* d = getenv("CG_CACHE_DIR")) return std::string(d);
+  const char* h = getenv("HOME");
+  return h ? std::string(h) + "/.cache/cg_kernels" : std::string();
+}
+
+uint64_t fnv64(const std::string& s, uint64_t h = 1469598103934665603ull) {
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ull;
+  return h;
+}
+
+std::string cache_path(const std::string& dir, const std::string& name, const std::string& source) {
+  int maj = 0, min = 0;
+  nvrtcVersion(&maj, &min);
+  std::string key = source + "|" + std::to_string(maj) + "." + std::to_string(min);
+  for (const char* o : kNvrtcOpts) key += std::string("|") + o;
+  char hx[17];
+  snprintf(hx, sizeof hx, "%016llx", (unsigned long long)fnv64(key));
+  return dir + "/" + name + "-" + hx + ".cubin";
+}
+
+bool read_file(const std::string& path, std::vector<char>* out) {
+  FILE* f = fopen(path.c_str(), "rb");
+  if (!f) return false;
+  fseek(f, 0, SEEK_END);
+  long n = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  out->resize(n > 0 ? (size_t)n : 0);
+  bool ok = n > 0 && fread(out->data(), 1, (size_t)n, f) == (size_t)n;
+  fclose(f);
+  return ok;
+}
+
+void write_file_atomic(const std::string& path, const std::vector<char>& data) {
+  std::string tmp = path + ".tmp." + std::to_string((long long)getpid());
+  FILE* f = fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  bool ok = fwrite(data.data(), 1, data.size(), f) == data.size();
+  ok = (fclose(f) == 0) && ok;
+  if (!ok || rename(tmp.c_str(), path.c_str()) != 0) remove(tmp.c_str());
+}
+
+// NVRTC one translation unit to a cubin (thread-safe: one program per call).
+bool nvrtc_cubin(const std::string& name, const std::string& source, std::vector<char>* cubin, std::string* err) {
   nvrtcProgram prog;
-  if (nvrtcCreateProgram(&prog, ks.source.c_str(), (ks.name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+  if (nvrtcCreateProgram(&prog, source.c_str(), (name + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     *err = "nvrtcCreateProgram failed";
-    return CG_E_NVRTC;
+    return false;
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-default-device", "--std=c++17", "-lineinfo"};
-  nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+  nvrtcResult r = nvrtcCompileProgram(prog, (int)(sizeof kNvrtcOpts / sizeof kNvrtcOpts[0]), kNvrtcOpts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
     std::string log(n, '\0');
     nvrtcGetProgramLog(prog, &log[0]);
     nvrtcDestroyProgram(&prog);
-    *err = "NVRTC failed for " + ks.name + ": " + log;
-    return CG_E_NVRTC;
+    *err = "NVRTC failed for " + name + ": " + log;
+    return false;
   }
   size_t n = 0;
   nvrtcGetCUBINSize(prog, &n);
-  std::vector<char> cubin(n);
-  nvrtcGetCUBIN(prog, cubin.data());
+  cubin->resize(n);
+  nvrtcGetCUBIN(prog, cubin->data());
   nvrtcDestroyProgram(&prog);
-  if (const char* dir = getenv("CG_DUMP_KERNELS")) {  // inspection: <dir>/<name>.cu and .cubin
-    if (FILE* f = fopen((std::string(dir) + "/" + ks.name + ".cu").c_str(), "w")) {
-      fwrite(ks.source.data(), 1, ks.source.size(), f);
-      fclose(f);
-    }
-    if (FILE* f = fopen((std::string(dir) + "/" + ks.name + ".cubin").c_str(), "wb")) {
-      fwrite(cubin.data(), 1, cubin.size(), f);
-      fclose(f);
-    }
+  return true;
+}
+
+// Make every kernel of `specs` resident in the process-wide cache: already loaded
+// ones are skipped, the disk cache is consulted, the rest are compiled by NVRTC on
+// up to hardware_concurrency threads (distinct programs compile independently),
+// then loaded on the calling thread.  *compiled counts fresh NVRTC compiles.
+int compile_kernels(const std::vector<const KernelSpec*>& specs, std::string* err, int* compiled) {
+  struct Job { const KernelSpec* ks; std::string path; std::vector<char> cubin; std::string err; bool ok = false; };
+  std::vector<Job> jobs;
+  {
+    std::lock_guard<std::mutex> lk(g_kcache.mu);
+    std::set<std::string> seen;
+    for (const KernelSpec* ks : specs)
+      if (!g_kcache.by_name.count(ks->name) && seen.insert(ks->name).second) jobs.push_back({ks, "", {}, "", false});
   }
-  cudaLibrary_t lib;
-  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  if (e != cudaSuccess) { *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e); return CG_E_CUDA; }
-  cudaKernel_t k;
-  e = cudaLibraryGetKernel(&k, lib, ks.name.c_str());
-  if (e != cudaSuccess) { *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e); return CG_E_CUDA; }
-  std::lock_guard<std::mutex> lk(g_kcache.mu);
-  g_kcache.by_name[ks.name] = k;
-  g_kcache.libs.push_back(lib);
-  *out = k;
-  *fresh = true;
+  if (jobs.empty()) return 0;
+  const std::string dir = cache_dir();
+  if (!dir.empty())  // mkdir -p (failures only disable the disk cache: reads miss, writes are dropped)
+    for (size_t k = 1; k <= dir.size(); ++k)
+      if (k == dir.size() || dir[k] == '/') mkdir(dir.substr(0, k).c_str(), 0755);
+  std::vector<size_t> todo;
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    if (!dir.empty()) {
+      jobs[i].path = cache_path(dir, jobs[i].ks->name, jobs[i].ks->source);
+      if (read_file(jobs[i].path, &jobs[i].cubin)) { jobs[i].ok = true; continue; }
+    }
+    todo.push_back(i);
+  }
+  if (!todo.empty()) {
+    std::atomic<size_t> next{0};
+    auto worker = [&]() {
+      for (size_t t; (t = next.fetch_add(1)) < todo.size();) {
+        Job& j = jobs[todo[t]];
+        j.ok = nvrtc_cubin(j.ks->name, j.ks->source, &j.cubin, &j.err);
+      }
+    };
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(todo.size(), std::min(hw, 32u));
+    std::vector<std::thread> pool;
+    for (size_t t = 1; t < nt; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    *compiled += (int)todo.size();
+  }
+  for (size_t i = 0; i < jobs.size(); ++i) {
+    Job& j = jobs[i];
+    if (!j.ok) { *err = j.err; return CG_E_NVRTC; }
+    if (!j.path.empty() && std::find(todo.begin(), todo.end(), i) != todo.end()) write_file_atomic(j.path, j.cubin);
+    if (const char* kd = getenv("CG_DUMP_KERNELS")) {  // inspection: <dir>/<name>.cu and .cubin
+      if (FILE* f = fopen((std::string(kd) + "/" + j.ks->name + ".cu").c_str(), "w")) {
+        fwrite(j.ks->source.data(), 1, j.ks->source.size(), f);
+        fclose(f);
+      }
+      if (FILE* f = fopen((std::string(kd) + "/" + j.ks->name + ".cubin").c_str(), "wb")) {
+        fwrite(j.cubin.data(), 1, j.cubin.size(), f);
+        fclose(f);
+      }
+    }
+    cudaLibrary_t lib;
+    cudaError_t e = cudaLibraryLoadData(&lib, j.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess) { *err = std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e); return CG_E_CUDA; }
+    cudaKernel_t k;
+    e = cudaLibraryGetKernel(&k, lib, j.ks->name.c_str());
+    if (e != cudaSuccess) { *err = std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e); return CG_E_CUDA; }
+    std::lock_guard<std::mutex> lk(g_kcache.mu);
+    g_kcache.by_name[j.ks->name] = k;
+    g_kcache.libs.push_back(lib);
+  }
   return 0;
 }
+
+cudaKernel_t cached_kernel(const std::string& name) {
+  std::lock_guard<std::mutex> lk(g_kcache.mu);
+  auto it = g_kcache.by_name.find(name);
+  return it == g_kcache.by_name.end() ? nullptr : it->second;
+}
+
+struct EwLaunch {  // a generated kernel's launch; k is filled once compiled
+  cudaKernel_t k = nullptr;
+  dim3 grid;
+  unsigned block = 256;
+  std::vector<void*> argv;
+};
 
 struct Launch {
   std::function<cudaError_t(cudaStream_t)> fn;
@@ -181,6 +298,9 @@ struct cg_graph {
   int n_streams = 1;
   int64_t launches = 0;
   int n_kernels = 0;
+  int64_t coll_batches = 0;
+  int nvrtc_compiled = 0;   // fresh NVRTC compiles (not from the process or disk cache)
+  double compile_s = 0.0;   // wall time in the compile phase  // collective batches issued (ncclGroupStart/End pairs), captures included
   // f2 epilogue fusion: tensor-core plan per group; partner[g] = the fused elementwise
   // group of a DOT/CONV group and vice versa (-1: none); fused_away[d] = the DOT/CONV
   // value is never materialised (its consumer group is computed in the epilogue)
@@ -382,43 +502,28 @@ static int build_launches(cg_graph* g) {
     CUDA_TRY(g, cudaMalloc(&g->ws, ws_need * sizeof(float)), "cudaMalloc(workspace)");
     g->ws_floats = ws_need;
   }
-  // 2) compile + closures
+  // 2) closures
   g->tcplan.assign(hg.groups.size(), nullptr);
-  std::vector<std::string> seen;
+  std::vector<std::shared_ptr<EwLaunch>> ew(hg.groups.size());
   for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
     const Group& G = hg.groups[gi];
     auto& L = g->glaunch[gi];
     const Node& nd = hg.nodes[G.sink];
     if (G.kind == G_EW || G.kind == G_RED) {
+      // the kernel is compiled after epilogue fusion (a chain computed in its
+      // producer's epilogue is never compiled); the launch reads it from `st`
       KernelSpec& ks = specs[gi];
-      cudaKernel_t k;
-      bool fresh = false;
-      int rc = compile_kernel(ks, &k, &g->err, &fresh);
-      if (rc) return rc;
-      if (std::find(seen.begin(), seen.end(), ks.name) == seen.end()) {
-        seen.push_back(ks.name);
-        g->n_kernels++;
-      }
-      std::vector<void*> argv;
-      for (int p : ks.in_ids) argv.push_back(g->ptr[p]);
-      for (int m : ks.out_ids) argv.push_back(g->ptr[m]);
-      if (ks.uses_ws) argv.push_back(g->ws);
-      dim3 grid(ks.grid[0], ks.grid[1], ks.grid[2]);
-      unsigned block = ks.block;
-      if (ks.mode != "red") {  // grid-stride kernels: exactly one full wave of resident blocks
-        int occ = 0;
-        static const int occ_cap = getenv("CG_EW_BLOCKS_PER_SM") ? atoi(getenv("CG_EW_BLOCKS_PER_SM")) : 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k, (int)block, 0) == cudaSuccess && occ > 0) {
-          if (occ_cap > 0) occ = std::min(occ, occ_cap);
-          grid.x = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ks.work_blocks, (int64_t)g->num_sms * occ));
-        }
-        cudaGetLastError();
-      }
-      auto st = std::make_shared<std::vector<void*>>(argv);
-      L.push_back({[k, grid, block, st](cudaStream_t s) {
-                     std::vector<void*> ap(st->size());
-                     for (size_t i = 0; i < st->size(); ++i) ap[i] = &(*st)[i];
-                     return cudaLaunchKernel((const void*)k, grid, dim3(block), ap.data(), 0, s);
+      auto st = std::make_shared<EwLaunch>();
+      for (int p : ks.in_ids) st->argv.push_back(g->ptr[p]);
+      for (int m : ks.out_ids) st->argv.push_back(g->ptr[m]);
+      if (ks.uses_ws) st->argv.push_back(g->ws);
+      st->grid = dim3(ks.grid[0], ks.grid[1], ks.grid[2]);
+      st->block = ks.block;
+      ew[gi] = st;
+      L.push_back({[st](cudaStream_t s) {
+                     std::vector<void*> ap(st->argv.size());
+                     for (size_t i = 0; i < st->argv.size(); ++i) ap[i] = &st->argv[i];
+                     return cudaLaunchKernel((const void*)st->k, st->grid, dim3(st->block), ap.data(), 0, s);
                    },
                    1});
       if (ks.uses_ws) {
@@ -439,7 +544,7 @@ static int build_launches(cg_graph* g) {
       case CG_ALLREDUCE_SUM: {
         const float* src = in[0];
         long long cnt = numel(ys);
-        if (nd.op == CG_ALLREDUCE_SUM && g->world > 1) {
+        if (nd.op == CG_ALLREDUCE_SUM && g->comm) {
           void* comm = g->comm;
           L.push_back({[src, out, cnt, comm](cudaStream_t s) {
                          int r = g_nccl.AllReduce(src, out, (size_t)cnt, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm, s);
@@ -578,6 +683,38 @@ static int build_launches(cg_graph* g) {
   }
   (void)n;
   fuse_epilogues(g);
+  // 3) compile the generated kernels that still launch (parallel NVRTC + disk cache)
+  {
+    std::vector<const KernelSpec*> need;
+    for (size_t gi = 0; gi < hg.groups.size(); ++gi)
+      if (ew[gi] && !g->glaunch[gi].empty()) need.push_back(&specs[gi]);
+    const auto t0 = std::chrono::steady_clock::now();
+    int compiled = 0;
+    int rc = compile_kernels(need, &g->err, &compiled);
+    if (rc) return rc;
+    g->nvrtc_compiled += compiled;
+    g->compile_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::set<std::string> distinct;
+    static const int occ_cap = getenv("CG_EW_BLOCKS_PER_SM") ? atoi(getenv("CG_EW_BLOCKS_PER_SM")) : 0;
+    for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
+      if (!ew[gi] || g->glaunch[gi].empty()) continue;
+      const KernelSpec& ks = specs[gi];
+      EwLaunch& st = *ew[gi];
+      st.k = cached_kernel(ks.name);
+      if (!st.k) return g->fail(CG_E_NVRTC, "kernel " + ks.name + " missing after compile");
+      distinct.insert(ks.name);
+      if (ks.mode != "red") {  // grid-stride kernels: exactly one full wave of resident blocks
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)st.k, (int)st.block, 0) == cudaSuccess &&
+            occ > 0) {
+          if (occ_cap > 0) occ = std::min(occ, occ_cap);
+          st.grid.x = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ks.work_blocks, (int64_t)g->num_sms * occ));
+        }
+        cudaGetLastError();
+      }
+    }
+    g->n_kernels += (int)distinct.size();
+  }
   // block access sets for the concurrent capture (values of the fused-away DOT/CONV
   // output d are never touched; a fused chain's writes happen in its producer group)
   const size_t NG = hg.groups.size();
@@ -692,12 +829,33 @@ static bool enqueue_groups(cg_graph* g, const std::vector<char>* R, int* kcount)
   const size_t NG = hg.groups.size();
   const int NS = g->n_streams;
   if (NS <= 1) {
+    bool any_coll = false;
+    std::vector<char> act(NG);
     for (size_t gi = 0; gi < NG; ++gi) {
-      if (R && !(*R)[gi]) continue;
-      for (auto& L : g->glaunch[gi]) {
-        if (L.fn(g->stream) != cudaSuccess) return false;
-        *kcount += L.kernels;
+      act[gi] = !R || (*R)[gi];
+      any_coll = any_coll || (act[gi] && g->is_coll[gi]);
+    }
+    if (!any_coll) {  // Gamma order
+      for (size_t gi = 0; gi < NG; ++gi) {
+        if (!act[gi]) continue;
+        for (auto& L : g->glaunch[gi]) {
+          if (L.fn(g->stream) != cudaSuccess) return false;
+          *kcount += L.kernels;
+        }
       }
+      return true;
+    }
+    // collectives deferred and batched (schedule.h): one ncclGroupStart/End per batch
+    for (const auto& step : collective_schedule(act, g->rd_blocks, g->wr_blocks, g->uses_ws, g->is_coll)) {
+      const bool batch = step.size() > 1 && g->comm;
+      if (batch && g_nccl.GroupStart() != 0) return false;
+      for (int gi : step)
+        for (auto& L : g->glaunch[gi]) {
+          if (L.fn(g->stream) != cudaSuccess) return false;
+          *kcount += L.kernels;
+        }
+      if (batch && g_nccl.GroupEnd() != 0) return false;
+      g->coll_batches += batch ? 1 : 0;
     }
     return true;
   }
@@ -874,7 +1032,7 @@ cg_graph* cg_create(int device, void* cuda_stream, const cg_dist* dist) {
       return nullptr;
     }
     cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (dist && dist->world > 1) {
+    if (dist && (dist->world > 1 || dist->nccl_unique_id)) {  // a 1-rank communicator when an id is given
       std::string e;
       if (!g_nccl.load(&e)) { g_create_error = "cg_create: " + e; return nullptr; }
       if (!dist->nccl_unique_id) { g_create_error = "cg_create: world > 1 needs nccl_unique_id"; return nullptr; }
@@ -1270,3 +1428,6 @@ extern "C" int64_t cgx_kernel_source(cg_graph* g, int gi, int num_sms, char* buf
   }
   return (int64_t)s.size();
 }
+
+// collective batches (ncclGroupStart/End pairs) issued so far, captured ones included
+extern "C" int64_t cgx_coll_batches(const cg_graph* g) { return g ? g->coll_batches : CG_E_ARG; }

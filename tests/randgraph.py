@@ -16,7 +16,8 @@ BINARY = ["ADD", "SUB", "MUL", "DIV", "MAX2", "MIN2", "RELU_GRAD"]
 LEAF_SHAPES = [[4, 8], [1, 8], [4, 1], [8], []]
 
 
-def random_spec(seed: int, n_ops=None, allow_updates=True, simple_values=False, rewrite_bait=False):
+def random_spec(seed: int, n_ops=None, allow_updates=True, simple_values=False, rewrite_bait=False,
+                extra_binary=()):
     rng = random.Random(seed)
     n_ops = n_ops if n_ops is not None else rng.randint(3, 40)
     nodes = []
@@ -61,7 +62,7 @@ def random_spec(seed: int, n_ops=None, allow_updates=True, simple_values=False, 
         elif r < 0.75:
             a = pick()
             b = a if rng.random() < 0.1 else pick()
-            op, preds, attrs = rng.choice(BINARY), [a, b], {}
+            op, preds, attrs = rng.choice(BINARY + list(extra_binary)), [a, b], {}
         elif r < 0.80:
             op, preds, attrs = "FMA", [pick(), pick(), pick()], {}
         elif r < 0.88:

@@ -405,6 +405,81 @@ def test_elementwise_identities():
     assert np.allclose(_run1("FMA", [x, y, x]), x.astype(np.float64) * y + x, rtol=6e-8)
 
 
+def test_pow_closed_forms():
+    """POW (S:133 binary op list; numpy power semantics, DESIGN §3 c1) pinned by
+    what the mathematics fixes: x^2 = x*x and x^0.5 = sqrt(x) (both correctly
+    rounded in fp32 — the f64 product of two fp32 values is exact), x^1 = x,
+    x^0 = 1 (0^0 = 1 as in C99 pow), 2^3 = 8 and 3^2 = 9 (operand order),
+    x^-1 = 1/x, integer powers by repeated products, a negative base with a
+    non-integer exponent is NaN, 0^-1 = +inf."""
+    x = np.linspace(0.05, 7.0, 211, dtype=np.float32)
+    two = np.full_like(x, 2.0)
+    assert np.array_equal(_run1("POW", [x, two]), x * x)
+    assert np.array_equal(_run1("POW", [-x, two]), x * x)
+    assert np.array_equal(_run1("POW", [x, np.full_like(x, 0.5)]), np.sqrt(x))
+    assert np.array_equal(_run1("POW", [x, np.ones_like(x)]), x)
+    assert np.all(_run1("POW", [np.concatenate([x, [0.0, -3.0]]).astype(np.float32),
+                                np.zeros(213, np.float32)]) == 1.0)
+    assert _run1("POW", [np.float32([2.0]), np.float32([3.0])])[0] == 8.0
+    assert _run1("POW", [np.float32([3.0]), np.float32([2.0])])[0] == 9.0
+    assert np.array_equal(_run1("POW", [x, -np.ones_like(x)]), np.float32(1) / x)
+    # x^3 = x*x*x to within the one extra rounding of the fp32 product chain
+    cube = (x.astype(np.float64) ** 2) * x.astype(np.float64)
+    assert np.max(np.abs(_run1("POW", [x, np.full_like(x, 3.0)]) - cube) / cube) < 6e-8
+    assert np.all(np.isnan(_run1("POW", [np.float32([-2.0, -0.5]), np.float32([0.5, 1.5])])))
+    assert _run1("POW", [np.float32([0.0]), np.float32([-1.0])])[0] == np.inf
+    # broadcasting: a scalar exponent against a vector
+    assert np.array_equal(_run1("POW", [x, np.float32(2.0)]), x * x)
+
+
+def test_sign_and_selection_ops():
+    """ABS / NEG / MAX2 / MIN2 / COS pinned by identities, not by re-typing them:
+    |x| = max(x, -x); NEG is an involution that flips the sign bit (NEG(0) = -0);
+    max(a, b) + min(a, b) = a + b and max(a, b) >= both operands (exact in fp32);
+    NaN propagates through MAX2 / MIN2 (numpy maximum / minimum); cos 0 = 1,
+    cos pi = -1, cos^2 + sin^2 = 1 and cos x = sin(pi/2 - x) to rounding."""
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal(300).astype(np.float32)
+    b = rng.standard_normal(300).astype(np.float32)
+    ab = _run1("ABS", [a])
+    assert np.array_equal(ab, np.where(a < 0, -a, a)) and np.all(np.signbit(ab) == False)  # noqa: E712
+    assert np.signbit(_run1("ABS", [np.float32([-0.0])]))[0] == False  # noqa: E712
+    n = _run1("NEG", [a])
+    assert np.array_equal(_run1("NEG", [n]), a) and np.all(n + a == 0)
+    assert np.signbit(_run1("NEG", [np.float32([0.0])]))[0]
+    mx, mn = _run1("MAX2", [a, b]), _run1("MIN2", [a, b])
+    assert np.array_equal(mx + mn, a + b)
+    assert np.all(mx >= a) and np.all(mx >= b) and np.all(mn <= a) and np.all(mn <= b)
+    assert np.all((mx == a) | (mx == b)) and np.all((mn == a) | (mn == b))
+    nan = np.float32([np.nan, 1.0])
+    assert np.isnan(_run1("MAX2", [nan, np.float32([5.0, 5.0])])[0])
+    assert np.isnan(_run1("MIN2", [np.float32([5.0, 5.0]), nan])[0])
+    c = _run1("COS", [np.float32([0.0, np.pi])])
+    assert c[0] == 1.0 and c[1] == -1.0
+    s_ = _run1("SIN", [a]).astype(np.float64)
+    c_ = _run1("COS", [a]).astype(np.float64)
+    assert np.max(np.abs(s_ * s_ + c_ * c_ - 1)) < 2e-7
+    shifted = (np.float64(np.pi / 2) - a.astype(np.float64))
+    assert np.max(np.abs(c_ - np.sin(shifted))) < 1e-7
+
+
+def test_concat_and_reshape_values():
+    """CONCAT places its operands side by side along the axis (slicing the result
+    returns them); RESHAPE keeps row-major element order (the flat index of
+    [i, j] in a [R, C] view is i*C + j), so reshaping arange gives arange."""
+    a = np.arange(24, dtype=np.float32).reshape(2, 3, 4)
+    b = -np.arange(16, dtype=np.float32).reshape(2, 2, 4)
+    cat = _run1("CONCAT", [a, b], {"axis": 1})
+    assert cat.shape == (2, 5, 4)
+    assert np.array_equal(cat[:, :3], a) and np.array_equal(cat[:, 3:], b)
+    c = _run1("CONCAT", [a, a[:, :, :1]], {"axis": 2})
+    assert np.array_equal(c[..., 4], a[..., 0]) and np.array_equal(c[..., :4], a)
+    r = _run1("RESHAPE", [a], {"dims": [4, 6]})
+    for i in range(4):
+        for j in range(6):
+            assert r[i, j] == i * 6 + j
+
+
 def test_softmax_rows_sum_to_one():
     g = Graph()
     L = g.add_leaf("VAR", [6, 10])
