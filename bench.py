@@ -388,7 +388,11 @@ def run_c2(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # a bounded timeout: a rank that fails outside a collective must not leave the
+        # others blocked forever (the per-config MIN flag covers the common case)
+        import datetime
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=300))
     rows_g, cols = configs.C2_ROWS, configs.C2_COLS
     row0, rows = shard_range(rows_g, rank, world)  # strong scaling: a slice of the FIXED global arrays
     g, outs, spec, data, rep, info, build_s, gen_s = build_c2(rows, row0, local)

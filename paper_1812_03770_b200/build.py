@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcg.so")
-SOURCES = ["host.cpp", "codegen.cpp", "schedule.cpp", "kernels.cu", "dot_tc.cu", "dot_small.cu", "conv_small.cu", "engine.cu"]
+SOURCES = ["host.cpp", "codegen.cpp", "schedule.cpp", "kernels.cu", "dot_tc.cu", "dot_small.cu", "conv_small.cu", "conv_img_tc.cu", "engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -29,7 +29,7 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         obj = os.path.join(CSRC, "build", src + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
@@ -37,8 +37,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
                "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
+        cmds.append(cmd)
         objs.append(obj)
+    # translation units compile independently: one nvcc per source, in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c), cmds)):
+            if r.returncode != 0:
+                raise subprocess.CalledProcessError(r.returncode, r.args)
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-shared", *ARCH, "-cudart", "static", *objs, "-o", tmp, "-lnvrtc", "-ldl",
            "-L/usr/local/cuda/lib64", "-Xlinker", "-rpath,/usr/local/cuda/lib64"]

@@ -248,6 +248,10 @@ class Graph:
             self._check(lib().cg_assign(self.h, int(var), ctypes.c_void_p(value.data_ptr()),
                                         value.numel() * value.element_size(), 1))
         elif hasattr(value, "data_ptr"):  # pinned / CPU torch tensor
+            # A PINNED source is copied asynchronously on the graph's stream (stream order
+            # puts it before the next eval): the caller must not refill the buffer until
+            # that eval (or a read / synchronize) has returned.  Pageable memory is staged
+            # by the driver before cg_assign returns and may be reused at once.
             assert value.is_contiguous()
             self._check(lib().cg_assign(self.h, int(var), ctypes.c_void_p(value.data_ptr()),
                                         value.numel() * value.element_size(), 0))

@@ -473,7 +473,7 @@ int bwdk_blocks(const ConvGeom& g, int num_sms) { return std::min(g.n, num_sms *
 
 template <typename F>
 void set_smem(F f) {
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT);
+  smem_attr((const void*)f, SMEM_LIMIT);
 }
 
 constexpr int RT_PX = 4;
@@ -518,10 +518,10 @@ cudaError_t launch_rt(const float* x, const float* w, float* y, const RtGeom& r,
   const int bps = std::max(1, std::min(4, (int)((224 * 1024) / (smem + 1024))));
   const int grid = std::max(1, std::min((r.n + IMG - 1) / IMG, num_sms * bps));
   if (ks == 5) {
-    cudaFuncSetAttribute(conv_rt_kernel<COP, 5, PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
+    smem_attr((const void*)conv_rt_kernel<COP, 5, PX, FLIP>, (int)RT_SMEM);
     conv_rt_kernel<COP, 5, PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
   } else {
-    cudaFuncSetAttribute(conv_rt_kernel<COP, 3, PX, FLIP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RT_SMEM);
+    smem_attr((const void*)conv_rt_kernel<COP, 3, PX, FLIP>, (int)RT_SMEM);
     conv_rt_kernel<COP, 3, PX, FLIP><<<grid, 256, smem, s>>>(x, w, y, r, IMG);
   }
   return cudaGetLastError();

@@ -393,11 +393,8 @@ template <int NT>
 cudaError_t launch_rows(const float* A, const float* B, float* C, int M, int N, int K, int tb, int num_sms, cudaStream_t s) {
   const int kc = rows_kchunk(K, NT);
   const size_t smem = (size_t)NT * (kc + 4) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dot_smalln_rows<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  const cudaError_t ae = smem_attr((const void*)dot_smalln_rows<NT>, 227 * 1024);  // per device
+  if (ae != cudaSuccess) return ae;
   // one 16-warp block per SM: op(B)^T is staged once per SM (not once per 16 rows --
   // the staging was the kernel's cost) and every warp walks its rows two at a time
   const int warps = NT >= 32 ? 8 : 16;  // (32 accumulators x 2 rows need the registers of 8 warps)

@@ -34,6 +34,7 @@
 #include "../../include/cg.h"
 #include "codegen.h"
 #include "host.h"
+#include "conv_img_tc.h"
 #include "conv_small.h"
 #include "dot_small.h"
 #include "dot_tc.h"
@@ -588,7 +589,9 @@ static int build_launches(cg_graph* g) {
         const float *x = in[0], *w = in[1];
         int sms = g->num_sms;
         static const bool prefer_tc = getenv("CG_CONV_PREFER_TC") != nullptr;  // A/B measurement switch
-        if (conv_small_fwd_ok(cgm) && cgm.co <= 16 && !prefer_tc) {  // few channels: whole images in shared memory
+        if (conv_img_tc_supported(cgm, false)) {  // small images, few channels: tcgen05 with smem-staged images
+          L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_img_tc(x, w, out, cgm, false, sms, s); }, 1});
+        } else if (conv_small_fwd_ok(cgm) && cgm.co <= 16 && !prefer_tc) {  // few channels: whole images in shared memory
           L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
         } else if (cgm.kh == 1 && cgm.kw == 1 && cgm.sh == 1 && cgm.sw == 1 && cgm.pt == 0 && cgm.pl == 0 &&
                    (long long)cgm.n * cgm.h * cgm.w <= INT32_MAX &&
@@ -622,7 +625,9 @@ static int build_launches(cg_graph* g) {
         ConvGeom cgm = geom(nd, ys, hg.nodes[nd.preds[0]].shape, (int)ws[0], (int)ws[1]);
         const float *dy = in[0], *w = in[1];
         int sms = g->num_sms;
-        if (conv_small_bwdin_ok(cgm))
+        if (conv_img_tc_supported(cgm, true))
+          L.push_back({[dy, w, out, cgm, sms](cudaStream_t s) { return launch_conv_img_tc(dy, w, out, cgm, true, sms, s); }, 1});
+        else if (conv_small_bwdin_ok(cgm))
           L.push_back({[dy, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_bwdin(dy, w, out, cgm, sms, s); }, 1});
         else
           L.push_back({[dy, w, out, cgm](cudaStream_t s) { return launch_conv2d_bwd_input(dy, w, out, cgm, s); }, 1});

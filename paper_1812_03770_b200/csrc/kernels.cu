@@ -16,8 +16,24 @@
 #include <type_traits>
 #include <cstdlib>
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <tuple>
 
 namespace cg {
+
+cudaError_t smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({fn, dev, bytes})) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({fn, dev, bytes});
+  return e;
+}
 
 namespace {
 

@@ -48,6 +48,11 @@ struct ConcatArgs {
 };
 cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long long dst_inner, cudaStream_t s);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize for kernel fn on the CURRENT device,
+// set once per (kernel, device, bytes): the attribute is per device, so a process
+// driving graphs on several devices must set it on each of them (thread-safe).
+cudaError_t smem_attr(const void* fn, int bytes);
+
 // Debug only (CG_DEBUG_CLOBBER): checksum of n floats, synchronous on stream s.
 unsigned long long debug_checksum(const float* p, long long n, cudaStream_t s);
 
