@@ -28,6 +28,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
 #include <cstdlib>
 
 #include "conv_img_tc.h"
@@ -489,6 +492,553 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- backward-kernel as a K = pixels GEMM
+// dw[m, co] = sum_q A[m, q] dy[q, co],  m = (kh, kw, ci) (HWIO row), q = (n, oh, ow),
+// A[m, q] = x[n, oh+kh-PT, ow+kw-PL, ci]  (zero outside the image; stride 1).
+// M = KS*KS*CIN rows sit in TMEM lanes (A from TMEM), the pixels are the GEMM's K,
+// B = dy^T (K-major rows of 32 pixels per output channel) in shared memory.
+//
+// Rows: the first 128 (if M >= 128) form a direct tile per 32-pixel k-block; the
+// remaining R <= 32 rows use a block-diagonal tile: lane quadrant Q holds those rows
+// for k-block Q of a 128-pixel super-block, and B carries all four k-blocks as
+// N = 4*N0 columns -- D[(Q, r), (Q', co)] with Q == Q' is the wanted sum, the rest is
+// ignored.  Same MMA cost as four narrow tiles, but the builders of all four lane
+// quadrants (= all four SM sub-partitions) share the work instead of quadrant 0 alone.
+// Chains of BK_CH super-blocks accumulate in TMEM; the epilogue adds each chain into
+// a round-to-nearest register sum; per-CTA partials are summed in a fixed order by
+// reduce_finalize (deterministic).
+//
+// Data movement is TMA bulk copies issued by one producer warp (many KB in flight
+// per SM without registers): x chunks (G images, zero-padded in place) into two
+// buffers, dy super-blocks (128 pixels) into a ring.  Warps: 0..7 A builders (two
+// groups, alternate jobs), 8..11 B builders, 12..15 epilogue, 16 producer, 17 MMA.
+constexpr int BK_THREADS = 576;
+constexpr int BK_NG = 2;    // A builder groups
+constexpr int BK_CH = 2;    // super-blocks per TMEM accumulation chain
+
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
+struct BkGeo {
+  static constexpr int MR = KS * KS * CIN;     // real rows of dw
+  static constexpr int T0 = MR / 128;          // direct tiles (0 or 1)
+  static constexpr int R = MR - 128 * T0;      // rows of the block-diagonal tile
+  static constexpr int N0 = COUT <= 8 ? 8 : 16;
+  static constexpr int NB = 4 * N0;            // B rows = diagonal-tile N
+  static constexpr int P = OH * OW;
+  // Staged images [HP][WPS][CIN] at XBASE + g * IMGF, zero where the window leaves
+  // the image.  Staging modes:
+  //  WHOLE (VALID, HP == IH, WPS == IW): the staged layout is the source layout, one
+  //        bulk copy per chunk;
+  //  TMAP  (CIN = 1, padded): one 3-D tiled TMA per chunk, box {WPS, HP, G} at
+  //        (0, 0, n0) -- its out-of-bounds zero fill gives every staged row >= PL
+  //        trailing zeros and every image >= PT trailing zero rows, and those serve
+  //        as the left / top padding of the next row / image (a zero guard of XBASE
+  //        floats precedes image 0).  (Negative TMA start coordinates -- the direct
+  //        way to pad -- trap with an illegal instruction: tools/tma3d_probe.cu.)
+  //  rows  otherwise: one bulk copy per image row into a zero frame whose rows are
+  //        16-byte aligned (input column iw at staged column iw + PLS).
+  static constexpr bool TMAP = CIN == 1 && (PT > 0 || PL > 0) && (IW * 4) % 16 == 0;
+  static constexpr int PADW = PL > KS - 1 - PL ? PL : KS - 1 - PL;
+  static constexpr int PADH = PT > KS - 1 - PT ? PT : KS - 1 - PT;
+  static constexpr int PLS = TMAP ? 0 : (PL * CIN + 3) / 4 * 4 / CIN + (((PL * CIN + 3) / 4 * 4) % CIN ? 1 : 0);
+  static constexpr int WMIN = TMAP ? IW + PADW : OW + KS - 1 - PL + PLS;
+  static constexpr int WPS0 = ((WMIN * CIN + 3) / 4 * 4 + CIN - 1) / CIN;
+  // TMAP rows: a pitch of 4 (mod 8) words spreads the KS x KS taps of one pixel over
+  // distinct banks (pitch 32 put all five kh of a kw in one bank: 5-way conflicts)
+  static constexpr int WPS = TMAP && WPS0 % 8 == 0 ? WPS0 + 4 : WPS0;
+  static constexpr int HP = TMAP ? IH + PADH : OH + KS - 1;
+  static constexpr int XBASE = TMAP ? (PT * WPS + PL + 31) / 32 * 32 : 0;
+  static constexpr int IMGF = HP * WPS * CIN;
+  static constexpr int SRCF = IH * IW * CIN;
+  static constexpr bool WHOLE = PT == 0 && PLS == 0 && HP == IH && WPS == IW;  // staged layout == source layout
+  static constexpr int XBOX = HP * WPS * 4;    // bytes per image of a TMAP box
+  static_assert(!TMAP || (WPS <= 256 && HP <= 256), "TMA box");
+  // zero run covering every row offset, rounded so both image buffers stay 128-byte aligned
+  static constexpr int ZLEN = (((KS - 1) * WPS + KS - 1) * CIN + CIN + 31) / 32 * 32;
+  static constexpr int JOBS = 4 * T0 + 1;      // A tiles per 128-pixel super-block
+  static constexpr int DCOL1 = 0;              // diagonal accumulators: [0, NB), [NB, 2 NB)
+  static constexpr int DCOL0 = 2 * NB;         // direct accumulators: 16 columns each
+  static constexpr int ACOL = 2 * NB + (T0 ? 32 : 0);
+  static constexpr int L = (512 - ACOL) / 64;  // A ring slots (hi 32 + lo 32 columns)
+  static constexpr int B_STAGE = 2 * NB * 128; // hi + lo, K-major SWIZZLE_128B rows
+  static constexpr int DSK = COUT <= 8 ? 4 : 1;  // super-blocks of dy per ring slot (fewer, larger copies)
+  static constexpr int DSLOT = DSK * 128 * COUT * 4;
+  static constexpr int DS = COUT <= 8 ? 4 : 8;  // dy ring slots (48 / 64 KB in flight per SM)
+  static constexpr int NBS = COUT <= 8 ? 3 : 4; // B group stages (DSK super-blocks each: one sync per group)
+  static constexpr int B_GSTAGE = DSK * B_STAGE;
+  static_assert(T0 <= 1 && R >= 1 && R <= 32 && COUT <= 16, "geometry");
+  static_assert(T0 == 0 || N0 == 16, "direct tiles use N = 16");
+  static_assert(L >= 3, "TMEM");
+  static_assert((TMAP || (PLS * CIN) % 4 == 0) && (WPS * CIN) % 4 == 0 && (TMAP || PLS >= PL) && WPS >= WMIN, "staged rows 16-byte aligned");
+  static_assert(WHOLE || TMAP || (IW * CIN) % 4 == 0, "row copies are multiples of 16 bytes");
+  static_assert(!TMAP || HP <= 256, "box");
+  static_assert(SRCF % 4 == 0 && IMGF % 4 == 0 && (128 * COUT) % 4 == 0, "16-byte bulk copies");
+};
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
+__global__ void __launch_bounds__(BK_THREADS, 1)
+    conv_bwdk_tc_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ part, int nimgs,
+                        int G, int dbg, const __grid_constant__ CUtensorMap xmap) {
+  // dbg: per-role busy / wait cycles of CTA 0 (printf; measurement only, compiled in
+  // with -DCG_BK_TIMING -- the timers cost registers the roles need)
+  long long w_a = 0, w_b = 0, w_c = 0, t_role = 0;
+#ifdef CG_BK_TIMING
+#define BK_TIMED(acc, call)                \
+  do {                                     \
+    const long long t_ = dbg ? clock64() : 0; \
+    call;                                  \
+    if (dbg) acc += clock64() - t_;        \
+  } while (0)
+#else
+#define BK_TIMED(acc, call) \
+  do {                      \
+    call;                   \
+  } while (0)
+#endif
+  using Geo = BkGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
+  constexpr int MR = Geo::MR, T0 = Geo::T0, R = Geo::R, N0 = Geo::N0, NB = Geo::NB, P = Geo::P, WPS = Geo::WPS;
+  constexpr int IMGF = Geo::IMGF, SRCF = Geo::SRCF, JOBS = Geo::JOBS, L = Geo::L, ACOL = Geo::ACOL, DS = Geo::DS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  const int ZOFF = (Geo::XBASE + G * IMGF + 31) / 32 * 32;
+  const int buf_floats = ZOFF + Geo::ZLEN;          // images + a zero run (ZOFF)
+  const int nq = (G * P + 127) / 128 * 128;         // pixel slots of a chunk (whole super-blocks)
+  float* dring = reinterpret_cast<float*>(smem + Geo::NBS * Geo::B_GSTAGE);
+  float* xs = dring + DS * Geo::DSLOT / 4;          // 2 image buffers
+  int* cbase = reinterpret_cast<int*>(xs + 2 * buf_floats);  // pixel -> staged offset of its window
+  uint64_t* bars = reinterpret_cast<uint64_t*>(cbase + nq);
+  const uint32_t bar0 = smem_u32(bars);
+  auto imgfull = [&](int b) { return bar0 + 8u * b; };
+  auto imgfree = [&](int b) { return bar0 + 8u * (2 + b); };
+  auto tfull = [&](int b) { return bar0 + 8u * (4 + b); };
+  auto tempty = [&](int b) { return bar0 + 8u * (6 + b); };
+  auto afull = [&](int l) { return bar0 + 8u * (8 + l); };
+  auto lofree = [&](int l) { return bar0 + 8u * (8 + L + l); };
+  auto bfull = [&](int s) { return bar0 + 8u * (8 + 2 * L + s); };
+  auto bfree = [&](int s) { return bar0 + 8u * (8 + 2 * L + Geo::NBS + s); };
+  auto dfull = [&](int s) { return bar0 + 8u * (8 + 2 * L + 2 * Geo::NBS + s); };
+  auto dfree = [&](int s) { return bar0 + 8u * (8 + 2 * L + 2 * Geo::NBS + DS + s); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * L + 2 * Geo::NBS + 2 * DS);
+  // (the role index through a shuffle: provably warp-uniform, so the role branches
+  // stay convergent and elect.sync / tcgen05 issue need no WARPSYNC.COLLECTIVE)
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
+
+  // this CTA's images [i0, i1): contiguous, balanced; chunks of G images
+  const int i0 = (int)((long long)blockIdx.x * nimgs / gridDim.x);
+  const int i1 = (int)((long long)(blockIdx.x + 1) * nimgs / gridDim.x);
+  const int nchunks = (i1 - i0 + G - 1) / G;
+  auto chunk_imgs = [&](int c) { return min(G, i1 - (i0 + c * G)); };
+  auto chunk_sk = [&](int c) { return (chunk_imgs(c) * P + 127) / 128; };
+  int s_tot = 0;
+  for (int c = 0; c < nchunks; ++c) s_tot += chunk_sk(c);
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(imgfull(b), 1);            // the producer's arrive.expect_tx
+      mbar_init(imgfree(b), 4 * BK_NG);    // every A builder warp
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 4);
+    }
+    for (int l = 0; l < L; ++l) {
+      mbar_init(afull(l), 4);
+      mbar_init(lofree(l), 1);
+    }
+    for (int s = 0; s < Geo::NBS; ++s) {
+      mbar_init(bfull(s), 4);
+      mbar_init(bfree(s), 1);
+    }
+    for (int s = 0; s < DS; ++s) {
+      mbar_init(dfull(s), 1);
+      mbar_init(dfree(s), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = threadIdx.x; e < 2 * buf_floats; e += blockDim.x) xs[e] = 0.f;  // pads + zero runs stay zero
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    const int g = q / P, p = q - g * P, oh = p / OW, ow = p - oh * OW;
+    cbase[q] = q < G * P ? Geo::XBASE + g * IMGF + ((oh - (Geo::TMAP ? PT : 0)) * WPS + ow + Geo::PLS - PL) * CIN : ZOFF;
+  }
+  // the zeroing is generic-proxy; the TMA writes that follow are async-proxy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 17) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+#ifdef CG_BK_TIMING
+  if (dbg) t_role = clock64();
+#endif
+
+  if (warp < 4 * BK_NG) {
+    // ---------------- A builders: one 128-lane x 32-pixel tile per job (hi | lo columns)
+    const int grp = warp / 4, Q = warp % 4;
+    auto row_off = [](int m) {
+      const int c = m % CIN, t = m / CIN, kh = t / KS, kw = t % KS;
+      return (kh * WPS + kw) * CIN + c;
+    };
+    const int off_direct = T0 ? row_off(Q * 32 + lane) : 0;
+    const int off_diag = lane < R ? row_off(T0 * 128 + lane) : 0;
+    int it = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int b = c & 1, limit = chunk_imgs(c) * P, nsk = chunk_sk(c);
+      BK_TIMED(w_a, mbar_wait(imgfull(b), (c >> 1) & 1));
+      const float* img = xs + b * buf_floats;
+      for (int k = 0; k < nsk; ++k) {
+#pragma unroll
+        for (int j = 0; j < JOBS; ++j, ++it) {
+          if (it % BK_NG != grp) continue;
+          const int l = it % L;
+          const bool direct = j < 4 * T0;
+          const int q0 = k * 128 + (direct ? j : Q) * 32;
+          const float* src = img + (direct ? off_direct : off_diag);
+          // the window offsets of the 32 pixels are the same for every lane: broadcast
+          // LDS.128s, then 32 independent loads (no per-column shuffle -> load chain)
+          int cb[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int4 t = *reinterpret_cast<const int4*>(cbase + q0 + 4 * i);
+            cb[4 * i] = t.x; cb[4 * i + 1] = t.y; cb[4 * i + 2] = t.z; cb[4 * i + 3] = t.w;
+          }
+          if (q0 + 32 > limit) {  // (uniform) ragged end of a chunk: those pixels read the zero run
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (q0 + i >= limit) cb[i] = ZOFF;
+          }
+          const uint32_t ta = tmem + ((uint32_t)(Q * 32) << 16) + (uint32_t)(ACOL + l * 64);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = src[cb[half * 16 + i]];
+            if (half == 0) {
+              BK_TIMED(w_b, mbar_wait(lofree(l), ((it / L) & 1) ^ 1));
+              asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            uint32_t hv[16], lv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t h = __float_as_uint(v[i]) & 0xFFFFE000u;
+              hv[i] = h;
+              lv[i] = __float_as_uint(__fsub_rn(v[i], __uint_as_float(h)));
+            }
+            tmem_st16(ta + half * 16, hv);
+            tmem_st16(ta + 32 + half * 16, lv);
+          }
+          BK_TIMED(w_c, asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"));
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(afull(l));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(imgfree(b));
+    }
+  } else if (warp < 4 * BK_NG + 4) {
+    // ---------------- B builders: per group of DSK super-blocks, dy rows of one 32-pixel
+    // k-block each -> N0 K-major rows (hi, lo); one dy slot and one B stage per group
+    const int Qb = warp - 4 * BK_NG;
+    constexpr int GS = Geo::DSK;
+    int gi = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int nsk = chunk_sk(c), limit = chunk_imgs(c) * P;
+      for (int k0 = 0; k0 < nsk; k0 += GS, ++gi) {
+        const int ds = gi % DS, sb = gi % Geo::NBS;
+        float cur[GS][N0];
+#pragma unroll
+        for (int u = 0; u < GS; ++u)
+#pragma unroll
+          for (int i = 0; i < N0; ++i) cur[u][i] = 0.f;
+        BK_TIMED(w_a, mbar_wait(dfull(ds), (gi / DS) & 1));
+#pragma unroll
+        for (int u = 0; u < GS; ++u) {
+          const int q = (k0 + u) * 128 + Qb * 32 + lane;
+          if (k0 + u < nsk && q < limit) {
+            const float* src = dring + (size_t)ds * (Geo::DSLOT / 4) + (u * 128 + Qb * 32 + lane) * COUT;
+            if constexpr (COUT % 4 == 0) {
+#pragma unroll
+              for (int i = 0; i < COUT; i += 4) {
+                const float4 t = *reinterpret_cast<const float4*>(src + i);
+                cur[u][i] = t.x; cur[u][i + 1] = t.y; cur[u][i + 2] = t.z; cur[u][i + 3] = t.w;
+              }
+            } else if constexpr (COUT % 2 == 0) {
+#pragma unroll
+              for (int i = 0; i < COUT; i += 2) {
+                const float2 t = *reinterpret_cast<const float2*>(src + i);
+                cur[u][i] = t.x; cur[u][i + 1] = t.y;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < COUT; ++i) cur[u][i] = src[i];
+            }
+          }
+        }
+        // the slot is refilled by TMA (async proxy) once every B warp has arrived: the
+        // generic reads above must be complete first -- without this fence the last
+        // LDS.128 (channels 12..15) was still in flight when the refill landed
+        BK_TIMED(w_c, asm volatile("fence.proxy.async.shared::cta;" ::: "memory"));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dfree(ds));
+        BK_TIMED(w_b, mbar_wait(bfree(sb), ((gi / Geo::NBS) & 1) ^ 1));
+#pragma unroll
+        for (int u = 0; u < GS; ++u) {
+          uint8_t* bh = smem + sb * Geo::B_GSTAGE + u * Geo::B_STAGE;
+#pragma unroll
+          for (int co = 0; co < N0; ++co) {
+            const int n = Qb * N0 + co;
+            const int off = n * 128 + (((lane >> 2) ^ (n & 7)) << 4) + (lane & 3) * 4;
+            const float hi = __uint_as_float(__float_as_uint(cur[u][co]) & 0xFFFFE000u);
+            *reinterpret_cast<float*>(bh + off) = hi;
+            *reinterpret_cast<float*>(bh + NB * 128 + off) = __fsub_rn(cur[u][co], hi);
+          }
+        }
+        BK_TIMED(w_c, asm volatile("fence.proxy.async.shared::cta;" ::: "memory"));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bfull(sb));
+      }
+    }
+  } else if (warp < 4 * BK_NG + 8) {
+    // ---------------- epilogue: each chain's accumulators -> round-to-nearest register sums
+    const int Qe = warp - 4 * BK_NG - 4;
+    float s0[16], s1[N0];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s0[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i < N0; ++i) s1[i] = 0.f;
+    const int nch = (s_tot + BK_CH - 1) / BK_CH;
+    const uint32_t lrow = (uint32_t)(Qe * 32) << 16;
+    for (int ch = 0; ch < nch; ++ch) {
+      const int b = ch & 1;
+      BK_TIMED(w_a, mbar_wait(tfull(b), (ch >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if constexpr (T0 > 0) {
+        float v[16];
+        tmem_ld16(tmem + lrow + (uint32_t)(Geo::DCOL0 + b * 16), v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s0[i] = __fadd_rn(s0[i], v[i]);
+      }
+      {
+        float v[N0];
+        if constexpr (N0 == 16) tmem_ld16(tmem + lrow + (uint32_t)(Geo::DCOL1 + b * NB + Qe * N0), v);
+        else tmem_ld8(tmem + lrow + (uint32_t)(Geo::DCOL1 + b * NB + Qe * N0), v);
+#pragma unroll
+        for (int i = 0; i < N0; ++i) s1[i] = __fadd_rn(s1[i], v[i]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty(b));
+    }
+    float* out = part + (size_t)blockIdx.x * MR * COUT;
+    if constexpr (T0 > 0) {
+      const int m = Qe * 32 + lane;
+#pragma unroll
+      for (int co = 0; co < COUT; ++co) out[(size_t)m * COUT + co] = s0[co];
+    }
+    // diagonal rows: the four quadrants hold partial sums over different k-blocks;
+    // combine them in a fixed order (Q = 0..3) through shared memory (the B ring is
+    // idle: every MMA has completed once the last chain was drained)
+    float* red = reinterpret_cast<float*>(smem);
+#pragma unroll
+    for (int i = 0; i < N0; ++i) red[(Qe * 32 + lane) * N0 + i] = s1[i];
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (Qe == 0 && lane < R) {
+      const int m = T0 * 128 + lane;
+#pragma unroll
+      for (int co = 0; co < COUT; ++co) {
+        float t = red[lane * N0 + co];
+        t = __fadd_rn(t, red[(32 + lane) * N0 + co]);
+        t = __fadd_rn(t, red[(64 + lane) * N0 + co]);
+        t = __fadd_rn(t, red[(96 + lane) * N0 + co]);
+        out[(size_t)m * COUT + co] = t;
+      }
+    }
+  } else if (warp == 4 * BK_NG + 8) {
+    // ---------------- producer: TMA bulk copies of x chunks and dy super-blocks.
+    // Chunk c + 1's images are requested before chunk c's dy, so the A builders
+    // never wait for an image buffer at a chunk boundary.
+    // (the tensor map's address is taken here, on the __grid_constant__ parameter
+    // itself: captured inside the lambda by reference it was copied to the stack and
+    // the TMA saw a local address -> illegal instruction)
+    const uint64_t xmap_addr = reinterpret_cast<uint64_t>(&xmap);
+    auto load_x = [&](int c) {
+      const int b = c & 1, nimg = chunk_imgs(c);
+      BK_TIMED(w_a, mbar_wait(imgfree(b), ((c >> 1) & 1) ^ 1));
+      const uint32_t dst = smem_u32(xs + b * buf_floats);
+      const float* src = x + (size_t)(i0 + c * G) * SRCF;
+      if (lane == 0) mbar_expect_tx(imgfull(b), Geo::TMAP ? (uint32_t)(G * Geo::XBOX) : (uint32_t)(nimg * SRCF * 4));
+      __syncwarp();
+      if constexpr (Geo::WHOLE) {
+        if (lane == 0) bulk_g2s(dst, src, (uint32_t)(nimg * SRCF * 4), imgfull(b));
+      } else if constexpr (Geo::TMAP) {
+        // box {WPS, HP, G} at (0, 0, first image) behind the zero guard
+        if (lane == 0)
+          asm volatile(
+              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst + Geo::XBASE * 4),
+              "l"(xmap_addr), "r"(0), "r"(0), "r"(i0 + c * G), "r"(imgfull(b))
+              : "memory");
+      } else {
+        for (int r = lane; r < nimg * IH; r += 32) {  // one copy per image row, into the padded frame
+          const int im = r / IH, h = r - im * IH;
+          bulk_g2s(dst + (uint32_t)((im * IMGF + ((h + PT) * WPS + Geo::PLS) * CIN) * 4), src + (size_t)r * IW * CIN,
+                   (uint32_t)(IW * CIN * 4), imgfull(b));
+        }
+      }
+      __syncwarp();
+    };
+    int s = 0;
+    if (nchunks > 0) load_x(0);
+    for (int c = 0; c < nchunks; ++c) {
+      const int nsk = chunk_sk(c), limit = chunk_imgs(c) * P;
+      if (c + 1 < nchunks) load_x(c + 1);
+      for (int k0 = 0; k0 < nsk; k0 += Geo::DSK, ++s) {  // (s counts dy slot groups here)
+        const int ds = s % DS;
+        BK_TIMED(w_b, mbar_wait(dfree(ds), ((s / DS) & 1) ^ 1));
+        if (lane == 0) {
+          const uint32_t bytes = (uint32_t)(min(Geo::DSK * 128, limit - k0 * 128) * COUT * 4);
+          mbar_expect_tx(dfull(ds), bytes);
+          bulk_g2s(smem_u32(dring) + (uint32_t)(ds * Geo::DSLOT),
+                   dy + ((size_t)(i0 + c * G) * P + (size_t)k0 * 128) * COUT, bytes, dfull(ds));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- warp 17: MMA issuer
+    const uint32_t idesc0 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t idesc1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    int it = 0, s = 0, gi = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int nsk = chunk_sk(c);
+      for (int k = 0; k < nsk; ++k, ++s) {
+        const int sub = k % Geo::DSK, sb = gi % Geo::NBS, ch = s / BK_CH, b = ch & 1;
+        const bool group_end = sub == Geo::DSK - 1 || k == nsk - 1;
+        const bool first = s % BK_CH == 0, last = s % BK_CH == BK_CH - 1 || s == s_tot - 1;
+        if (first) BK_TIMED(w_a, mbar_wait_warp(tempty(b), ((ch >> 1) & 1) ^ 1));
+        if (sub == 0) BK_TIMED(w_b, mbar_wait_warp(bfull(sb), (gi / Geo::NBS) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t bh = sbase + (uint32_t)(sb * Geo::B_GSTAGE + sub * Geo::B_STAGE), bl = bh + NB * 128;
+#pragma unroll
+        for (int j = 0; j < JOBS; ++j, ++it) {
+          const int l = it % L;
+          BK_TIMED(w_a, mbar_wait_warp(afull(l), (it / L) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ahi = tm + (uint32_t)(ACOL + l * 64), alo = ahi + 32;
+          const bool direct = j < 4 * T0;
+          const uint32_t d = direct ? tm + (uint32_t)(Geo::DCOL0 + b * 16) : tm + (uint32_t)(Geo::DCOL1 + b * NB);
+          const uint32_t boff = direct ? (uint32_t)(j * N0 * 128) : 0u;
+          const uint32_t idesc = direct ? idesc0 : idesc1;
+          const bool acc0 = !(first && (direct ? j == 0 : true));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t dhi = sdesc(bh + boff + kk * 32, 16, 1024, 2), dlo = sdesc(bl + boff + kk * 32, 16, 1024, 2);
+            mma_tf32_e<1>(d, alo + kk * 8, dhi, idesc, (kk > 0 || acc0) ? 1u : 0u);
+            mma_tf32_e<1>(d, ahi + kk * 8, dlo, idesc, 1u);
+            mma_tf32_e<1>(d, ahi + kk * 8, dhi, idesc, 1u);
+          }
+          mma_commit_e<1>(lofree(l));
+        }
+        if (group_end) {
+          mma_commit_e<1>(bfree(sb));
+          ++gi;
+        }
+        if (last) mma_commit_e<1>(tfull(b));
+      }
+    }
+  }
+#ifdef CG_BK_TIMING
+  if (dbg && blockIdx.x == 0 && lane == 0)
+    printf("bwdk role-warp %2d: busy %8lld  wait_a %8lld  wait_b %8lld  fence/st %8lld (cycles)\n", warp, clock64() - t_role,
+           w_a, w_b, w_c);
+#else
+  (void)w_a; (void)w_b; (void)w_c; (void)t_role;
+#endif
+#undef BK_TIMED
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 17) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// 3-D tiled map over single-channel images x[n][h][w] (fp32), box {bw, bh, g}: a
+// load at (-pl, -pt, n0) returns the zero-padded frames of g images.
+typedef CUresult (*EncodeTiledFnCI)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool make_img_map(CUtensorMap* m, const float* x, int n, int h, int w, int bw, int bh, int g) {
+  static EncodeTiledFnCI fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFnCI)p;
+  });
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)w * h * 4};
+  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)g};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
+struct BkLaunch {
+  using Geo = BkGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
+  static int grid(int n, int num_sms) { return std::max(1, std::min(n, num_sms)); }
+  static size_t smem_for(int G) {
+    const int nq = (G * Geo::P + 127) / 128 * 128;
+    return 1024 + (size_t)Geo::NBS * Geo::B_GSTAGE + (size_t)Geo::DS * Geo::DSLOT +
+           2 * (((size_t)Geo::XBASE + G * Geo::IMGF + 31) / 32 * 32 + Geo::ZLEN) * 4 + (size_t)nq * 4 +
+           (size_t)(10 + 2 * Geo::L + 2 * Geo::NBS + 2 * Geo::DS) * 8;  // barriers + TMEM slot
+  }
+  // images per chunk: the least padding in the last super-block with the two image
+  // buffers within 48 KB (the rest of shared memory goes to the dy ring and B stages)
+  static int pick_g() {
+    int best = 1;
+    double best_cost = 1e30;
+    for (int G = 1; G <= 64; ++G) {
+      if (2 * (size_t)G * Geo::IMGF * 4 > 48 * 1024 && G > 1) break;
+      const int nq = (G * Geo::P + 127) / 128 * 128;
+      const double cost = (double)nq / (G * Geo::P) * (1.0 + 0.02 / G);
+      if (cost < best_cost) { best_cost = cost; best = G; }
+    }
+    return best;
+  }
+  static cudaError_t run(const float* x, const float* dy, float* dw, float* ws, int n, int num_sms, cudaStream_t s) {
+    if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dy)) & 15) return cudaErrorMisalignedAddress;
+    const int G = pick_g(), gr = grid(n, num_sms);
+    CUtensorMap xmap;
+    std::memset(&xmap, 0, sizeof(xmap));
+    if (Geo::TMAP && !make_img_map(&xmap, x, n, IH, IW, Geo::WPS, Geo::HP, G)) return cudaErrorInvalidValue;
+    const size_t smem = smem_for(G);
+    if (getenv("CG_BK_DEBUG")) fprintf(stderr, "bwdk_tc: G=%d grid=%d smem=%zu NBS=%d DS=%d L=%d\n", G, gr, smem, Geo::NBS, Geo::DS, Geo::L);
+    auto kern = conv_bwdk_tc_kernel<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
+    cudaError_t e = smem_attr((const void*)kern, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<gr, BK_THREADS, smem, s>>>(x, dy, ws, n, G, getenv("CG_BK_DEBUG") ? 1 : 0, xmap);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_reduce_finalize(ws, dw, (long long)Geo::MR * COUT, gr, 0, s);
+  }
+};
+
 template <int CO, int KS, int HO, int WO, int H, int W, int PT, int PL, int CI>
 cudaError_t launch_bwdin(const float* dy, const float* w, float* dx, int n, int num_sms, cudaStream_t s) {
   using Geo = BiGeo<CO, KS, HO, WO, H, W, PT, PL, CI>;
@@ -541,6 +1091,26 @@ CiKind kind_of(const ConvGeom& g, bool flip) {
 }
 
 }  // namespace
+
+bool conv_img_tc_bwdk_supported(const ConvGeom& g) {
+  return kind_of(g, false) != CI_NONE && !getenv("CG_NO_CONV_IMG_TC");
+}
+
+size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms) {
+  return (size_t)std::max(1, std::min(g.n, num_sms)) * g.kh * g.kw * g.ci * g.co;
+}
+
+cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g, int num_sms,
+                                    cudaStream_t s) {
+  switch (kind_of(g, false)) {
+    case CI_C4_CONV1:  // x [n,28,28,1], dy [n,28,28,6] -> dw [5,5,1,6] (SAME)
+      return BkLaunch<1, 5, 28, 28, 28, 28, 2, 2, 6>::run(x, dy, dw, ws, g.n, num_sms, s);
+    case CI_C4_CONV2:  // x [n,14,14,6], dy [n,10,10,16] -> dw [5,5,6,16] (VALID)
+      return BkLaunch<6, 5, 14, 14, 10, 10, 0, 0, 16>::run(x, dy, dw, ws, g.n, num_sms, s);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
 
 bool conv_img_tc_supported(const ConvGeom& g, bool flip) {
   return kind_of(g, flip) != CI_NONE && !getenv("CG_NO_CONV_IMG_TC");

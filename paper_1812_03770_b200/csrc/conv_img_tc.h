@@ -16,4 +16,12 @@ bool conv_img_tc_supported(const ConvGeom& g, bool flip);
 cudaError_t launch_conv_img_tc(const float* in, const float* w, float* out, const ConvGeom& g, bool flip, int num_sms,
                                cudaStream_t s);
 
+// backward-kernel (C4 geometries; g = the forward conv): dw[kh,kw,ci,co] =
+// sum_{n,oh,ow} x[n,oh+kh-pt,ow+kw-pl,ci] dy[n,oh,ow,co]; per-CTA partials in ws
+// (conv_img_tc_bwdk_ws floats), summed in a fixed order into dw
+bool conv_img_tc_bwdk_supported(const ConvGeom& g);
+size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms);
+cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g, int num_sms,
+                                    cudaStream_t s);
+
 }  // namespace cg

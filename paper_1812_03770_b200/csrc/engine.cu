@@ -489,8 +489,9 @@ static int build_launches(cg_graph* g) {
     } else if (hg.nodes[G.sink].op == CG_CONV2D_BWD_KERNEL) {
       const Node& nd = hg.nodes[G.sink];
       ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
-      ws_need = std::max(ws_need, conv_small_bwdk_ok(cgm) ? conv_small_bwdk_ws(cgm, g->num_sms)
-                                                          : conv2d_bwd_kernel_ws(cgm, g->num_sms));
+      ws_need = std::max(ws_need, conv_img_tc_bwdk_supported(cgm) ? conv_img_tc_bwdk_ws(cgm, g->num_sms)
+                                  : conv_small_bwdk_ok(cgm)          ? conv_small_bwdk_ws(cgm, g->num_sms)
+                                                                     : conv2d_bwd_kernel_ws(cgm, g->num_sms));
     }
     // conservative: any group of a kind that may take partials in the workspace
     if (G.kind != G_EW && G.kind != G_RED) {
@@ -638,7 +639,10 @@ static int build_launches(cg_graph* g) {
         const float *x = in[0], *dy = in[1];
         float* ws = g->ws;
         int sms = g->num_sms;
-        if (conv_small_bwdk_ok(cgm))
+        if (conv_img_tc_bwdk_supported(cgm))  // small images, few channels: K = pixels GEMM on tcgen05
+          L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv_img_tc_bwdk(x, dy, out, ws, cgm, sms, s); },
+                       2});
+        else if (conv_small_bwdk_ok(cgm))
           L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv_small_bwdk(x, dy, out, ws, cgm, sms, s); },
                        2});
         else
