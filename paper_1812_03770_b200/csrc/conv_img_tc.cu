@@ -41,20 +41,109 @@ namespace {
 
 #include "tc_prims.cuh"
 
-constexpr int CI_THREADS = 544;   // 17 warps
+constexpr int CI_THREADS = 448;   // 14 warps
 constexpr int CI_L = 6;           // A stages in TMEM (64 columns each: 32 hi + 32 lo)
 constexpr int CI_ACOL = 32;       // TMEM columns 0..31: two 16-column accumulators
 
-template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT, bool FLIP>
+// Staged images for the small-image kernels: [HP][WPS][CIN] at XBASE + g * IMGF,
+// zero where a window leaves the image.  Staging modes (one TMA-engine operation per
+// chunk of G images wherever possible: many KB in flight per SM without registers):
+//  WHOLE (VALID, HP == IH, WPS == IW): the staged layout is the source layout, one
+//        bulk copy per chunk;
+//  TMAP  (CIN = 1, padded): one 3-D tiled TMA per chunk, box {WPS, HP, G} at
+//        (0, 0, n0) -- its out-of-bounds zero fill gives every staged row >= PL
+//        trailing zeros and every image >= PT trailing zero rows, and those serve
+//        as the left / top padding of the next row / image (a zero guard of XBASE
+//        floats precedes image 0).  (Negative TMA start coordinates -- the direct
+//        way to pad -- trap with an illegal instruction: tools/tma3d_probe.cu.)
+//  rows  otherwise: one bulk copy per image row into a zero frame whose rows are
+//        16-byte aligned (input column iw at staged column iw + PLS).
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL>
+struct StageGeo {
+  static constexpr bool TMAP = CIN == 1 && (PT > 0 || PL > 0) && (IW * 4) % 16 == 0;
+  static constexpr int PADW = PL > KS - 1 - PL ? PL : KS - 1 - PL;
+  static constexpr int PADH = PT > KS - 1 - PT ? PT : KS - 1 - PT;
+  static constexpr int PLS = TMAP ? 0 : (PL * CIN + 3) / 4 * 4 / CIN + (((PL * CIN + 3) / 4 * 4) % CIN ? 1 : 0);
+  static constexpr int WMIN = TMAP ? IW + PADW : OW + KS - 1 - PL + PLS;
+  static constexpr int WPS0 = ((WMIN * CIN + 3) / 4 * 4 + CIN - 1) / CIN;
+  // TMAP rows: a pitch of 4 (mod 8) words spreads the KS x KS taps of one pixel over
+  // distinct banks (pitch 32 put all five kh of a kw in one bank: 5-way conflicts)
+  static constexpr int WPS = TMAP && WPS0 % 8 == 0 ? WPS0 + 4 : WPS0;
+  static constexpr int HP = TMAP ? IH + PADH : OH + KS - 1;
+  static constexpr int XBASE = TMAP ? (PT * WPS + PL + 31) / 32 * 32 : 0;
+  static constexpr int IMGF = HP * WPS * CIN;  // floats per staged image
+  static constexpr int SRCF = IH * IW * CIN;   // floats per source image
+  static constexpr bool WHOLE = PT == 0 && PLS == 0 && HP == IH && WPS == IW;
+  static constexpr int XBOX = HP * WPS * 4;    // bytes per image of a TMAP box
+  static constexpr int H_ = IH, W_ = IW, PT_ = PT, C_ = CIN;
+  // staged offset of the window origin (kh = kw = 0) of output pixel (oh, ow) of image g
+  __host__ __device__ static constexpr int window(int g, int oh, int ow) {
+    return XBASE + g * IMGF + ((oh - (TMAP ? PT : 0)) * WPS + ow + PLS - PL) * CIN;
+  }
+  __host__ __device__ static constexpr int tap(int kh, int kw, int c) { return (kh * WPS + kw) * CIN + c; }
+  static_assert(!TMAP || (WPS <= 256 && HP <= 256), "TMA box");
+  static_assert((TMAP || (PLS * CIN) % 4 == 0) && (WPS * CIN) % 4 == 0 && (TMAP || PLS >= PL) && WPS >= WMIN,
+                "staged rows 16-byte aligned");
+  static_assert(WHOLE || TMAP || (IW * CIN) % 4 == 0, "row copies are multiples of 16 bytes");
+  static_assert(SRCF % 4 == 0 && IMGF % 4 == 0, "16-byte bulk copies");
+};
+
+// Producer-warp side of the staging: images [n0, n0 + nimg) of x into the buffer at
+// shared address `buf` (XBASE-relative frame), completion on `bar` (count 1 + tx).
+template <class SG>
+__device__ __forceinline__ void stage_images(uint32_t buf, const float* x, uint64_t xmap_addr, int n0, int nimg, int G,
+                                             uint32_t bar, int lane) {
+  if (lane == 0) mbar_expect_tx(bar, SG::TMAP ? (uint32_t)(G * SG::XBOX) : (uint32_t)(nimg * SG::SRCF * 4));
+  __syncwarp();
+  if constexpr (SG::WHOLE) {
+    if (lane == 0) bulk_g2s(buf, x + (size_t)n0 * SG::SRCF, (uint32_t)(nimg * SG::SRCF * 4), bar);
+  } else if constexpr (SG::TMAP) {
+    if (lane == 0)
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+              buf + SG::XBASE * 4),
+          "l"(xmap_addr), "r"(0), "r"(0), "r"(n0), "r"(bar)
+          : "memory");
+  } else {
+    for (int r = lane; r < nimg * SG::H_; r += 32) {  // one copy per image row, into the padded frame
+      const int im = r / SG::H_, h = r - im * SG::H_;
+      bulk_g2s(buf + (uint32_t)((im * SG::IMGF + ((h + SG::PT_) * SG::WPS + SG::PLS) * SG::C_) * 4),
+               x + ((size_t)n0 * SG::H_ + r) * SG::W_ * SG::C_, (uint32_t)(SG::W_ * SG::C_ * 4), bar);
+    }
+  }
+  __syncwarp();
+}
+
+// 3-D tiled map over single-channel images x[n][h][w] (fp32), box {bw, bh, g}: a load
+// at (0, 0, n0) returns g frames with zero-filled trailing rows / columns (StageGeo TMAP).
+typedef CUresult (*EncodeTiledFnCI)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool make_img_map(CUtensorMap* m, const float* x, int n, int h, int w, int bw, int bh, int g) {
+  static EncodeTiledFnCI fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFnCI)p;
+  });
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)w * h * 4};
+  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)g};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
 struct CiGeo {
+  using SG = StageGeo<CIN, KS, IH, IW, OH, OW, PT, PL>;
   static constexpr int K = CIN * KS * KS;
   static constexpr int NKB = (K + 31) / 32;
   static constexpr int P = OH * OW;            // output pixels per image
-  // zero-padded planes: the window of every output pixel is in bounds (no masks)
-  static constexpr int HP = OH + KS - 1, WP = OW + KS - 1;
-  static constexpr int PLANE = HP * WP;
-  static constexpr int IMGF = CIN * PLANE;     // floats per staged (padded) image
-  static constexpr int SRCF = CIN * IH * IW;   // floats per source image
   static constexpr int B_BYTES = NKB * 4096;   // per k-block: hi tile 2 KiB + lo tile 2 KiB
 };
 
@@ -78,20 +167,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT, bool FLIP>
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
 __global__ void __launch_bounds__(CI_THREADS, 1)
     conv_img_tc_kernel(const float* __restrict__ in, const float* __restrict__ w, float* __restrict__ out, int nimgs,
-                       int G, int T) {
-  using Geo = CiGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT, FLIP>;
-  constexpr int K = Geo::K, NKB = Geo::NKB, P = Geo::P, PLANE = Geo::PLANE, IMGF = Geo::IMGF, WP = Geo::WP;
-  constexpr int SRCF = Geo::SRCF;
+                       int G, int T, const __grid_constant__ CUtensorMap xmap) {
+  using Geo = CiGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
+  using SG = typename Geo::SG;
+  constexpr int K = Geo::K, NKB = Geo::NKB, P = Geo::P;
   extern __shared__ uint8_t smem_raw[];
   // align to 1024 B by pointer arithmetic on the __shared__ array (keeps the shared
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   float* imgs = reinterpret_cast<float*>(smem + Geo::B_BYTES);   // 2 buffers x G images
-  const int buf_floats = G * IMGF;
+  const int buf_floats = (SG::XBASE + G * SG::IMGF + 31) / 32 * 32;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Geo::B_BYTES + 2 * (size_t)buf_floats * 4);
   const uint32_t bar0 = smem_u32(bars);
   auto imgfull = [&](int b) { return bar0 + 8u * b; };
@@ -102,12 +191,13 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   auto tempty = [&](int b) { return bar0 + 8u * (6 + 2 * CI_L + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * CI_L);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // role index through a shuffle: provably warp-uniform (convergent role branches)
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
   const int units = (nimgs + G - 1) / G;
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
-      mbar_init(imgfull(b), 128);  // every loader thread
+      mbar_init(imgfull(b), 1);    // the producer's arrive.expect_tx
       mbar_init(imgfree(b), 8);    // every builder warp
       mbar_init(tfull(b), 1);
       mbar_init(tempty(b), 4);     // the epilogue warps
@@ -125,11 +215,7 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     float v = 0.f;
     if (k < K && n < COUT) {
       const int c = k / (KS * KS), t = k % (KS * KS), kh = t / KS, kw = t % KS;
-      if (!FLIP) {  // w [KS][KS][CIN][COUT]
-        v = __ldg(w + ((size_t)(kh * KS + kw) * CIN + c) * COUT + n);
-      } else {      // w [KS][KS][COUT (= ci of the forward)][CIN (= co)], flipped taps
-        v = __ldg(w + ((size_t)((KS - 1 - kh) * KS + (KS - 1 - kw)) * COUT + n) * CIN + c);
-      }
+      v = __ldg(w + ((size_t)(kh * KS + kw) * CIN + c) * COUT + n);  // w [KS][KS][CIN][COUT]
     }
     const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     const float lo = __fsub_rn(v, hi);
@@ -137,10 +223,10 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     *reinterpret_cast<float*>(smem + kb * 4096 + off) = hi;
     *reinterpret_cast<float*>(smem + kb * 4096 + 2048 + off) = lo;
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core
-  // the padding of both image buffers stays zero: the loaders only rewrite interiors
+  // the padding / guard of both image buffers stays zero (TMA writes only the frames)
   for (int e = threadIdx.x; e < 2 * buf_floats; e += blockDim.x) imgs[e] = 0.f;
-  if (warp == 16) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core / TMA
+  if (warp == 13) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -149,38 +235,9 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 4) {
-    // ---------------- loaders: G images, global NHWC (contiguous) -> planar [c][h][w]
-    int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const int b = j & 1;
-      const int n0 = u * G, nimg = min(G, nimgs - n0);
-      mbar_wait(imgfree(b), ((j >> 1) & 1) ^ 1);
-      float* dst = imgs + b * buf_floats;
-      const float* src = in + (size_t)n0 * SRCF;
-      const int tot = nimg * SRCF;
-      for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * 128) {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int e = e0 + q * 128;
-          v[q] = e < tot ? __ldg(src + e) : 0.f;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int e = e0 + q * 128;
-          if (e < tot) {
-            const int im = e / SRCF, r = e - im * SRCF;        // r = (h * IW + w) * CIN + c
-            const int pix = r / CIN, c = r - pix * CIN, h = pix / IW, ww = pix - h * IW;
-            dst[im * IMGF + c * PLANE + (h + PT) * WP + ww + PL] = v[q];
-          }
-        }
-      }
-      mbar_arrive(imgfull(b));
-    }
-  } else if (warp < 12) {
+  if (warp < 8) {
     // ---------------- builders: A slab (128 pixels x 32 k) -> TMEM hi / lo columns
-    const int grp = warp < 8 ? 0 : 1;
+    const int grp = warp / 4;
     const int wq = warp % 4, rr = wq * 32 + lane;  // TMEM lane quadrant / tile row
     int it = 0, j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -189,34 +246,42 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
       mbar_wait(imgfull(b), (j >> 1) & 1);
       const float* img = imgs + b * buf_floats;
       for (int t = 0; t < T; ++t, it += NKB) {
-        // this row's output pixel: image g, (oh, ow); its window starts at (oh, ow) of the
-        // padded planes (rows past the unit read image 0: their outputs are not stored)
+        // this row's output pixel: image g, (oh, ow) (rows past the unit read image 0:
+        // their outputs are not stored)
         const int q = t * 128 + rr;
         const int g = q / P, p = q - g * P, oh = p / OW, ow = p - oh * OW;
-        const float* base = img + (g < nimg ? g * IMGF + oh * WP + ow : 0);
+        const float* base = img + SG::window(g < nimg ? g : 0, oh, ow);
 #pragma unroll
         for (int kb = 0; kb < NKB; ++kb) {
           const int step = it + kb;
           if ((step & 1) != grp) continue;
           const int l = step % CI_L;
-          mbar_wait(lofree(l), ((step / CI_L) & 1) ^ 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          uint32_t hv[32], lv[32];
+          float v[32];
 #pragma unroll
           for (int kl = 0; kl < 32; ++kl) {
             const int k = kb * 32 + kl;
-            float v = 0.f;
+            v[kl] = 0.f;
             if (k < K) {
               const int c = k / (KS * KS), tt = k % (KS * KS), kh = tt / KS, kw = tt % KS;
-              v = base[c * PLANE + kh * WP + kw];
+              v[kl] = base[SG::tap(kh, kw, c)];
             }
-            const uint32_t h = __float_as_uint(v) & 0xFFFFE000u;
-            hv[kl] = h;
-            lv[kl] = __float_as_uint(__fsub_rn(v, __uint_as_float(h)));
           }
+          mbar_wait(lofree(l), ((step / CI_L) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ta = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(CI_ACOL + l * 64);
-          tmem_st32(ta, hv);
-          tmem_st32(ta + 32, lv);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t hv[16], lv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float x = v[half * 16 + i];
+              const uint32_t h = __float_as_uint(x) & 0xFFFFE000u;
+              hv[i] = h;
+              lv[i] = __float_as_uint(__fsub_rn(x, __uint_as_float(h)));
+            }
+            tmem_st16(ta + half * 16, hv);
+            tmem_st16(ta + 32 + half * 16, lv);
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
@@ -226,7 +291,7 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(imgfree(b));  // this warp has read the images of unit j
     }
-  } else if (warp < 16) {
+  } else if (warp < 12) {
     // ---------------- epilogue: each k-block's accumulator -> round-to-nearest register sum
     const int wq = warp % 4, rr = wq * 32 + lane;
     int it = 0;
@@ -265,8 +330,18 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
         }
       }
     }
+  } else if (warp == 12) {
+    // ---------------- producer: one TMA-engine copy per unit of G images (double-buffered)
+    const uint64_t xmap_addr = reinterpret_cast<uint64_t>(&xmap);  // (address of the parameter itself)
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int b = j & 1;
+      const int n0 = u * G, nimg = min(G, nimgs - n0);
+      mbar_wait(imgfree(b), ((j >> 1) & 1) ^ 1);
+      stage_images<SG>(smem_u32(imgs + b * buf_floats), in, xmap_addr, n0, nimg, G, imgfull(b), lane);
+    }
   } else {
-    // ---------------- warp 16: MMA issuer (whole warp walks the loop; one elected lane issues)
+    // ---------------- warp 13: MMA issuer (whole warp walks the loop; one elected lane issues)
     // instruction descriptor: D f32, A / B tf32, A (TMEM) and B K-major, N = 16, M = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
@@ -295,7 +370,7 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 16) {
+  if (warp == 13) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
@@ -524,34 +599,9 @@ struct BkGeo {
   static constexpr int N0 = COUT <= 8 ? 8 : 16;
   static constexpr int NB = 4 * N0;            // B rows = diagonal-tile N
   static constexpr int P = OH * OW;
-  // Staged images [HP][WPS][CIN] at XBASE + g * IMGF, zero where the window leaves
-  // the image.  Staging modes:
-  //  WHOLE (VALID, HP == IH, WPS == IW): the staged layout is the source layout, one
-  //        bulk copy per chunk;
-  //  TMAP  (CIN = 1, padded): one 3-D tiled TMA per chunk, box {WPS, HP, G} at
-  //        (0, 0, n0) -- its out-of-bounds zero fill gives every staged row >= PL
-  //        trailing zeros and every image >= PT trailing zero rows, and those serve
-  //        as the left / top padding of the next row / image (a zero guard of XBASE
-  //        floats precedes image 0).  (Negative TMA start coordinates -- the direct
-  //        way to pad -- trap with an illegal instruction: tools/tma3d_probe.cu.)
-  //  rows  otherwise: one bulk copy per image row into a zero frame whose rows are
-  //        16-byte aligned (input column iw at staged column iw + PLS).
-  static constexpr bool TMAP = CIN == 1 && (PT > 0 || PL > 0) && (IW * 4) % 16 == 0;
-  static constexpr int PADW = PL > KS - 1 - PL ? PL : KS - 1 - PL;
-  static constexpr int PADH = PT > KS - 1 - PT ? PT : KS - 1 - PT;
-  static constexpr int PLS = TMAP ? 0 : (PL * CIN + 3) / 4 * 4 / CIN + (((PL * CIN + 3) / 4 * 4) % CIN ? 1 : 0);
-  static constexpr int WMIN = TMAP ? IW + PADW : OW + KS - 1 - PL + PLS;
-  static constexpr int WPS0 = ((WMIN * CIN + 3) / 4 * 4 + CIN - 1) / CIN;
-  // TMAP rows: a pitch of 4 (mod 8) words spreads the KS x KS taps of one pixel over
-  // distinct banks (pitch 32 put all five kh of a kw in one bank: 5-way conflicts)
-  static constexpr int WPS = TMAP && WPS0 % 8 == 0 ? WPS0 + 4 : WPS0;
-  static constexpr int HP = TMAP ? IH + PADH : OH + KS - 1;
-  static constexpr int XBASE = TMAP ? (PT * WPS + PL + 31) / 32 * 32 : 0;
-  static constexpr int IMGF = HP * WPS * CIN;
-  static constexpr int SRCF = IH * IW * CIN;
-  static constexpr bool WHOLE = PT == 0 && PLS == 0 && HP == IH && WPS == IW;  // staged layout == source layout
-  static constexpr int XBOX = HP * WPS * 4;    // bytes per image of a TMAP box
-  static_assert(!TMAP || (WPS <= 256 && HP <= 256), "TMA box");
+  using SG = StageGeo<CIN, KS, IH, IW, OH, OW, PT, PL>;
+  static constexpr bool TMAP = SG::TMAP;
+  static constexpr int PLS = SG::PLS, WPS = SG::WPS, HP = SG::HP, XBASE = SG::XBASE, IMGF = SG::IMGF;
   // zero run covering every row offset, rounded so both image buffers stay 128-byte aligned
   static constexpr int ZLEN = (((KS - 1) * WPS + KS - 1) * CIN + CIN + 31) / 32 * 32;
   static constexpr int JOBS = 4 * T0 + 1;      // A tiles per 128-pixel super-block
@@ -568,10 +618,8 @@ struct BkGeo {
   static_assert(T0 <= 1 && R >= 1 && R <= 32 && COUT <= 16, "geometry");
   static_assert(T0 == 0 || N0 == 16, "direct tiles use N = 16");
   static_assert(L >= 3, "TMEM");
-  static_assert((TMAP || (PLS * CIN) % 4 == 0) && (WPS * CIN) % 4 == 0 && (TMAP || PLS >= PL) && WPS >= WMIN, "staged rows 16-byte aligned");
-  static_assert(WHOLE || TMAP || (IW * CIN) % 4 == 0, "row copies are multiples of 16 bytes");
-  static_assert(!TMAP || HP <= 256, "box");
-  static_assert(SRCF % 4 == 0 && IMGF % 4 == 0 && (128 * COUT) % 4 == 0, "16-byte bulk copies");
+  static_assert((128 * COUT) % 4 == 0, "16-byte bulk copies");
+  static constexpr int SRCF = SG::SRCF;
 };
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
@@ -666,7 +714,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   for (int e = threadIdx.x; e < 2 * buf_floats; e += blockDim.x) xs[e] = 0.f;  // pads + zero runs stay zero
   for (int q = threadIdx.x; q < nq; q += blockDim.x) {
     const int g = q / P, p = q - g * P, oh = p / OW, ow = p - oh * OW;
-    cbase[q] = q < G * P ? Geo::XBASE + g * IMGF + ((oh - (Geo::TMAP ? PT : 0)) * WPS + ow + Geo::PLS - PL) * CIN : ZOFF;
+    cbase[q] = q < G * P ? Geo::SG::window(g, oh, ow) : ZOFF;
   }
   // the zeroing is generic-proxy; the TMA writes that follow are async-proxy
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -687,7 +735,7 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     const int grp = warp / 4, Q = warp % 4;
     auto row_off = [](int m) {
       const int c = m % CIN, t = m / CIN, kh = t / KS, kw = t % KS;
-      return (kh * WPS + kw) * CIN + c;
+      return Geo::SG::tap(kh, kw, c);
     };
     const int off_direct = T0 ? row_off(Q * 32 + lane) : 0;
     const int off_diag = lane < R ? row_off(T0 * 128 + lane) : 0;
@@ -873,29 +921,10 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
     // the TMA saw a local address -> illegal instruction)
     const uint64_t xmap_addr = reinterpret_cast<uint64_t>(&xmap);
     auto load_x = [&](int c) {
-      const int b = c & 1, nimg = chunk_imgs(c);
+      const int b = c & 1;
       BK_TIMED(w_a, mbar_wait(imgfree(b), ((c >> 1) & 1) ^ 1));
-      const uint32_t dst = smem_u32(xs + b * buf_floats);
-      const float* src = x + (size_t)(i0 + c * G) * SRCF;
-      if (lane == 0) mbar_expect_tx(imgfull(b), Geo::TMAP ? (uint32_t)(G * Geo::XBOX) : (uint32_t)(nimg * SRCF * 4));
-      __syncwarp();
-      if constexpr (Geo::WHOLE) {
-        if (lane == 0) bulk_g2s(dst, src, (uint32_t)(nimg * SRCF * 4), imgfull(b));
-      } else if constexpr (Geo::TMAP) {
-        // box {WPS, HP, G} at (0, 0, first image) behind the zero guard
-        if (lane == 0)
-          asm volatile(
-              "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst + Geo::XBASE * 4),
-              "l"(xmap_addr), "r"(0), "r"(0), "r"(i0 + c * G), "r"(imgfull(b))
-              : "memory");
-      } else {
-        for (int r = lane; r < nimg * IH; r += 32) {  // one copy per image row, into the padded frame
-          const int im = r / IH, h = r - im * IH;
-          bulk_g2s(dst + (uint32_t)((im * IMGF + ((h + PT) * WPS + Geo::PLS) * CIN) * 4), src + (size_t)r * IW * CIN,
-                   (uint32_t)(IW * CIN * 4), imgfull(b));
-        }
-      }
-      __syncwarp();
+      stage_images<typename Geo::SG>(smem_u32(xs + b * buf_floats), x, xmap_addr, i0 + c * G, chunk_imgs(c), G, imgfull(b),
+                                     lane);
     };
     int s = 0;
     if (nchunks > 0) load_x(0);
@@ -974,30 +1003,6 @@ __global__ void __launch_bounds__(BK_THREADS, 1)
   }
 }
 
-// 3-D tiled map over single-channel images x[n][h][w] (fp32), box {bw, bh, g}: a
-// load at (-pl, -pt, n0) returns the zero-padded frames of g images.
-typedef CUresult (*EncodeTiledFnCI)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-bool make_img_map(CUtensorMap* m, const float* x, int n, int h, int w, int bw, int bh, int g) {
-  static EncodeTiledFnCI fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFnCI)p;
-  });
-  if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
-  cuuint64_t strides[2] = {(cuuint64_t)w * 4, (cuuint64_t)w * h * 4};
-  cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)g};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
 struct BkLaunch {
   using Geo = BkGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
@@ -1050,16 +1055,19 @@ cudaError_t launch_bwdin(const float* dy, const float* w, float* dx, int n, int 
   return cudaGetLastError();
 }
 
-template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT, bool FLIP>
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
 cudaError_t launch_geo(const float* in, const float* w, float* out, int n, int num_sms, cudaStream_t s) {
-  using Geo = CiGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT, FLIP>;
+  using Geo = CiGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
+  using SG = typename Geo::SG;
+  if (reinterpret_cast<uintptr_t>(in) & 15) return cudaErrorMisalignedAddress;
   // images per unit: the largest G (<= 32) whose double-buffered images fit, preferring
   // little padding in the last 128-pixel tile of a unit
+  auto buf_bytes = [](int G) { return (size_t)((SG::XBASE + G * SG::IMGF + 31) / 32 * 32) * 4; };
   constexpr size_t budget = 200 * 1024;
   int best_g = 1;
   double best_cost = 1e30;
   for (int G = 1; G <= 32; ++G) {
-    const size_t bytes = Geo::B_BYTES + 2 * (size_t)G * Geo::IMGF * 4;
+    const size_t bytes = Geo::B_BYTES + 2 * buf_bytes(G);
     if (bytes > budget) break;
     const int T = (G * Geo::P + 127) / 128;
     const double waste = (double)T * 128 / ((double)G * Geo::P);   // padded rows per real row
@@ -1067,12 +1075,15 @@ cudaError_t launch_geo(const float* in, const float* w, float* out, int n, int n
     if (cost < best_cost) { best_cost = cost; best_g = G; }
   }
   const int G = best_g, T = (G * Geo::P + 127) / 128;
-  const size_t smem = 1024 + Geo::B_BYTES + 2 * (size_t)G * Geo::IMGF * 4 + 256;
-  auto kern = conv_img_tc_kernel<CIN, KS, IH, IW, OH, OW, PT, PL, COUT, FLIP>;
+  const size_t smem = 1024 + Geo::B_BYTES + 2 * buf_bytes(G) + 256;
+  CUtensorMap xmap;
+  std::memset(&xmap, 0, sizeof(xmap));
+  if (SG::TMAP && !make_img_map(&xmap, in, n, IH, IW, SG::WPS, SG::HP, G)) return cudaErrorInvalidValue;
+  auto kern = conv_img_tc_kernel<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
   cudaError_t e = smem_attr((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
   const int units = (n + G - 1) / G;
-  kern<<<std::min(units, num_sms), CI_THREADS, smem, s>>>(in, w, out, n, G, T);
+  kern<<<std::min(units, num_sms), CI_THREADS, smem, s>>>(in, w, out, n, G, T, xmap);
   return cudaGetLastError();
 }
 
@@ -1120,9 +1131,9 @@ cudaError_t launch_conv_img_tc(const float* in, const float* w, float* out, cons
                                cudaStream_t s) {
   switch (kind_of(g, flip)) {
     case CI_C4_CONV1:  // x [n,28,28,1] (*) w [5,5,1,6], SAME
-      return launch_geo<1, 5, 28, 28, 28, 28, 2, 2, 6, false>(in, w, out, g.n, num_sms, s);
+      return launch_geo<1, 5, 28, 28, 28, 28, 2, 2, 6>(in, w, out, g.n, num_sms, s);
     case CI_C4_CONV2:  // p1 [n,14,14,6] (*) w [5,5,6,16], VALID
-      return launch_geo<6, 5, 14, 14, 10, 10, 0, 0, 16, false>(in, w, out, g.n, num_sms, s);
+      return launch_geo<6, 5, 14, 14, 10, 10, 0, 0, 16>(in, w, out, g.n, num_sms, s);
     case CI_C4_CONV2_BWDIN:  // dy [n,10,10,16], w [5,5,6,16] -> dx [n,14,14,6] (VALID forward)
       return launch_bwdin<16, 5, 10, 10, 14, 14, 0, 0, 6>(in, w, out, g.n, num_sms, s);
     default:
