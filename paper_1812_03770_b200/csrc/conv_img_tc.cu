@@ -392,7 +392,10 @@ struct BiGeo {
   static constexpr int NJ = KS * KS * CI;                // GEMM N (real)
   static constexpr int NN = (NJ + 15) / 16 * 16;         // MMA N (multiple of 16)
   static constexpr int P = HO * WO;                      // dy pixels per image (<= 128)
-  static constexpr int CP = NJ | 1;                      // odd row pitch of C in smem
+  // row pitch of C in smem: even (8-byte col2im loads), CP / 2 odd (a half-warp's
+  // 8-byte reads of 16 consecutive rows hit 16 distinct bank pairs)
+  static constexpr int CP = ((NJ + 1) / 2 * 2 / 2) % 2 ? (NJ + 1) / 2 * 2 : (NJ + 1) / 2 * 2 + 2;
+  static_assert(CI % 2 == 0, "col2im reads channel pairs");
   static constexpr int B_BYTES = NN * 128 * 2;           // hi + lo tiles, K-major SW128 (K padded to 32)
   static constexpr int C_FLOATS = 128 * CP;
   static constexpr int ACC = NN;                         // TMEM columns per accumulator
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
   auto tfull = [&](int b) { return bar0 + 8u * (2 * BI_L + b); };
   auto tempty = [&](int b) { return bar0 + 8u * (2 * BI_L + 2 + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * BI_L + 4);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;  // (warp-uniform)
 
   if (threadIdx.x == 0) {
     for (int l = 0; l < BI_L; ++l) {
@@ -519,21 +522,39 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty(b));
       asm volatile("bar.sync 1, 256;" ::: "memory");  // Cs complete
+      // one thread per dx pixel, all CI channels: 25 taps x CI/2 8-byte reads; each
+      // channel in two fixed-order partial sums (even / odd kh, kh and kw ascending)
+      // added at the end -- deterministic, and half the dependent-add chain length
       float* o = dx + (size_t)n * H * W * CI;
-      for (int e = et; e < H * W * CI; e += 256) {
-        const int pix = e / CI, ci = e - pix * CI, h = pix / W, ww = pix - h * W;
-        float s = 0.f;
+      for (int pix = et; pix < H * W; pix += 256) {
+        const int h = pix / W, ww = pix - h * W;
+        float acc[2][CI];
+#pragma unroll
+        for (int i = 0; i < CI; ++i) acc[0][i] = acc[1][i] = 0.f;
 #pragma unroll
         for (int kh = 0; kh < KS; ++kh) {
           const int oh = h - kh + PT;
-          if ((unsigned)oh >= (unsigned)HO) continue;
+          const bool rok = (unsigned)oh < (unsigned)HO;
 #pragma unroll
           for (int kw = 0; kw < KS; ++kw) {
             const int ow = ww - kw + PL;
-            if ((unsigned)ow < (unsigned)WO) s = __fadd_rn(s, Cs[(oh * WO + ow) * CP + (kh * KS + kw) * CI + ci]);
+            if (rok && (unsigned)ow < (unsigned)WO) {
+              const float2* c2 = reinterpret_cast<const float2*>(Cs + (oh * WO + ow) * CP + (kh * KS + kw) * CI);
+#pragma unroll
+              for (int i = 0; i < CI / 2; ++i) {
+                const float2 t = c2[i];
+                acc[kh & 1][2 * i] = __fadd_rn(acc[kh & 1][2 * i], t.x);
+                acc[kh & 1][2 * i + 1] = __fadd_rn(acc[kh & 1][2 * i + 1], t.y);
+              }
+            }
           }
         }
-        o[e] = s;
+#pragma unroll
+        for (int i = 0; i < CI; ++i) acc[0][i] = __fadd_rn(acc[0][i], acc[1][i]);
+        float (&acc0)[CI] = acc[0];
+        float2* o2 = reinterpret_cast<float2*>(o + (size_t)pix * CI);
+#pragma unroll
+        for (int i = 0; i < CI / 2; ++i) o2[i] = make_float2(acc0[2 * i], acc0[2 * i + 1]);
       }
     }
   } else {
