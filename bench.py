@@ -518,7 +518,8 @@ def run_secondary(rank, world, local, iters, args):
     if world > 1:
         jobs += [("C2_weak", _sec_c2_weak), ("C3_weak", lambda: _sec_train("C3", 4096, True)),
                  ("C4_weak", lambda: _sec_train("C4", 8192, True))]
-    ctx = {"rank": rank, "world": world, "local": local, "iters": iters, "tf32": tf32, "pk": pk}
+    ctx = {"rank": rank, "world": world, "local": local, "iters": iters, "tf32": tf32, "pk": pk,
+           "coll": getattr(args, "coll", "fused")}
     for name, fn in jobs:
         ok = True
         try:
@@ -603,7 +604,8 @@ def _sec_train(name, gb, weak):
         spec = dp_spec(fn, gb, rank, world)
         start, count = shard_range(gb, rank, world)
     t0 = time.perf_counter()
-    g = make_graph(local, world, rank)
+    fused = _CTX.get("coll", "fused") == "fused"
+    g = make_graph(local, world, rank, fused=fused)
     for rec in spec["nodes"]:
         data = _leaf(rec)
         if rec["op"] in ("VAR", "CONST"):
@@ -614,7 +616,10 @@ def _sec_train(name, gb, weak):
         g.add_update(u, v)
     outs = spec["outputs"]
     g.optimise(outs)
-    info = g.plan_memory(outs, 0)
+    info = g.plan_memory(outs, cg.PLAN_FUSED_COLL if fused else 0)
+    if fused and world > 1:
+        from paper_1812_03770_b200.dist import connect_fused
+        connect_fused(g)
     build_s = time.perf_counter() - t0
     ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
     ids = {n["name"]: n["id"] for n in spec["nodes"] if n["op"] == "VAR"}
@@ -639,7 +644,10 @@ def _sec_train(name, gb, weak):
     ms_s = ms * 1e-3
     r = {"metric": "train iters/s", "value": 1e3 / ms, "unit": "iters/s", "ms_per_iter": ms,
          "global_batch": gb * world if weak else gb, "local_batch": count, "scaling": "weak" if weak else "strong",
-         "parallelism": f"dp{world}" + (" (NCCL AllReduce nodes, batched per step)" if world > 1 else ""),
+         "parallelism": f"dp{world}" + ((" (fused peer-memory AllReduce + SGD, one launch per step)" if fused else
+                                          " (NCCL AllReduce nodes, batched per step)") if world > 1 else ""),
+         "collectives": "fused (AllReduce + SGD update in one kernel, CG_PLAN_FUSED_COLL)" if fused else "nccl",
+         "n_fused": info["n_fused"],
          "build_s": build_s, "clocks": clk, "launches_per_iter": launches_per_iter,
          "plan_peak_bytes": info["pool_bytes"] + info["external_bytes"] + info["workspace_bytes"],
          "unshared_bytes": info["unshared_bytes"] + info["external_bytes"],
@@ -672,7 +680,10 @@ def _sec_c5():
     t0 = time.perf_counter()
     g, outs = cg.build_from_spec(spec, device=local, data_fn=_leaf)
     g.optimise(outs)
-    info = g.plan_memory(outs, 0)
+    info = g.plan_memory(outs, cg.PLAN_FUSED_COLL if fused else 0)
+    if fused and world > 1:
+        from paper_1812_03770_b200.dist import connect_fused
+        connect_fused(g)
     build_s = time.perf_counter() - t0
     ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
     l0 = g.launch_count()
@@ -718,6 +729,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--coll", default="fused", choices=["fused", "nccl"],
+                    help="C3/C4 gradient AllReduce: fused peer-memory kernel with the SGD update (default) or NCCL")
     ap.add_argument("--no-secondary", action="store_true", help="C2 only (skip the C1/C3/C4/C5 lines)")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()

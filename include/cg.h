@@ -113,7 +113,9 @@ typedef enum cg_status {
 
 /* Data-parallel placement [P:26]: rank r of `world` processes; the 128-byte
  * NCCL unique id comes from cg_nccl_unique_id on rank 0, broadcast by the
- * caller.  NULL or world == 1: single GPU, ALLREDUCE_SUM is the identity. */
+ * caller.  NULL or world == 1: single GPU, ALLREDUCE_SUM is the identity.
+ * nccl_unique_id == NULL with world > 1: no NCCL communicator; the graph must be
+ * planned with CG_PLAN_FUSED_COLL (peer-memory collectives). */
 typedef struct cg_dist {
   int32_t rank, world;
   const void* nccl_unique_id;
@@ -144,7 +146,9 @@ typedef struct cg_plan_info {
 
 enum { CG_PLAN_INCREMENTAL = 1u, /* pin Var frontiers, fresh blocks for kept values,
                                     signature-pure groups: minimal recompute sets */
-       CG_PLAN_NO_FUSION = 2u    /* one kernel per node (node-level Algorithm 1) */ };
+       CG_PLAN_NO_FUSION = 2u,   /* one kernel per node (node-level Algorithm 1) */
+       CG_PLAN_FUSED_COLL = 4u   /* ALLREDUCE_SUM (+ its elementwise update) as one
+                                    peer-memory kernel instead of NCCL (f3; same plan) */ };
 enum { CG_EVAL_NO_UPDATE = 1u,   /* skip update_iopair at the end of this evaluation */
        CG_EVAL_FULL = 2u,        /* ignore validity: recompute every group */
        CG_EVAL_SYNC = 4u         /* block the host until the evaluation finished */ };
@@ -208,6 +212,25 @@ void cg_destroy(cg_graph* g);
 
 /* Message of the last failing call on g (or of cg_create when g is NULL). */
 const char* cg_last_error(const cg_graph* g);
+
+/* Fused AllReduce + update over peer memory [P:26 "natural support for parallel
+ * and distributed computing"; SURVEY §8(f) f3].  With CG_PLAN_FUSED_COLL every
+ * ALLREDUCE_SUM group is one kernel that sums the gradient over all ranks in rank
+ * order 0..P-1 -- reading the other ranks' pools through CUDA IPC mappings (NVLink)
+ * at the same pool offset (every rank plans the same graph) -- and applies the
+ * elementwise update chain that consumes it (e.g. W - lr * g, Var / Const operands)
+ * before storing; independent collectives of one executor step are one launch.  A
+ * system-scope flag barrier orders the reads after every rank's gradient is final
+ * and keeps gradients alive until every rank has read them.
+ *   cg_coll_handle: after cg_plan_memory, writes this rank's 128-byte handle
+ *     (cudaIpcMemHandle of the pool, then of the flag words); returns 128.
+ *   cg_coll_connect: `handles` = world x 128 bytes in rank order (gathered by the
+ *     caller, e.g. over torch.distributed); maps the peers.  Required before the
+ *     first cg_eval when world > 1 (CG_E_STATE otherwise); not needed at world 1.
+ * Errors: CG_E_STATE (graph not planned with the flag), CG_E_SIZE (cap < 128),
+ * CG_E_ARG (world differs from cg_create's), CG_E_CUDA (IPC failure). */
+int cg_coll_handle(cg_graph* g, void* out, size_t cap);
+int cg_coll_connect(cg_graph* g, const void* handles, int32_t world);
 
 /* 128-byte NCCL unique id for cg_dist (call on rank 0 only). */
 int cg_nccl_unique_id(void* out128);

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcg.so")
-SOURCES = ["host.cpp", "codegen.cpp", "schedule.cpp", "kernels.cu", "dot_tc.cu", "dot_small.cu", "conv_small.cu", "conv_img_tc.cu", "engine.cu"]
+SOURCES = ["host.cpp", "codegen.cpp", "schedule.cpp", "kernels.cu", "dot_tc.cu", "dot_small.cu", "conv_small.cu", "conv_img_tc.cu", "coll.cu", "engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -33,7 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(CSRC, "build", src + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
-        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", *ARCH,
+        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", "-diag-suppress=177", "-Xcompiler", "-fPIC,-O3", *ARCH,
                "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

@@ -29,6 +29,7 @@ STATUS = {0: "CG_OK", -1: "CG_E_ARITY", -2: "CG_E_BAD_NODE", -3: "CG_E_SHAPE", -
 
 PLAN_INCREMENTAL = 1
 PLAN_NO_FUSION = 2
+PLAN_FUSED_COLL = 4
 EVAL_NO_UPDATE = 1
 EVAL_FULL = 2
 EVAL_SYNC = 4
@@ -42,7 +43,8 @@ DUMP_PLAN = 1
 # names exported by include/cg.h (tests check the library exports every one)
 ABI_SYMBOLS = ["cg_create", "cg_add_node", "cg_add_update", "cg_optimise", "cg_plan_memory", "cg_assign",
                "cg_eval", "cg_read", "cg_destroy", "cg_last_error", "cg_nccl_unique_id", "cg_dump_json",
-               "cg_eval_count", "cg_node_shape", "cg_launch_count", "cg_set_rewrites"]
+               "cg_eval_count", "cg_node_shape", "cg_launch_count", "cg_set_rewrites", "cg_coll_handle",
+               "cg_coll_connect"]
 
 
 class cg_attr(ctypes.Structure):
@@ -99,6 +101,8 @@ def lib():
             "cg_eval_count": (I64, [P, I32]),
             "cg_node_shape": (I32, [P, I32, P]),
             "cg_launch_count": (I64, [P]),
+            "cg_coll_handle": (ctypes.c_int, [P, P, SZ]),
+            "cg_coll_connect": (ctypes.c_int, [P, P, I32]),
             "cgx_collective_schedule": (I32, [I32, P, P, P, P, P, P, P, P, P]),
             "cgx_coll_batches": (I64, [P]),
         }
@@ -239,6 +243,18 @@ class Graph:
         info = cg_plan_info()
         self._check(lib().cg_plan_memory(self.h, _ids(outputs), len(outputs), int(flags), ctypes.byref(info)))
         return {f: getattr(info, f) for f, _ in cg_plan_info._fields_}
+
+    # ---- fused collectives (CG_PLAN_FUSED_COLL)
+    def coll_handle(self) -> bytes:
+        """cg_coll_handle: this rank's 128-byte peer-memory handle (pool + flag words)."""
+        buf = ctypes.create_string_buffer(128)
+        self._check(lib().cg_coll_handle(self.h, buf, 128))
+        return buf.raw
+
+    def coll_connect(self, handles):
+        """cg_coll_connect: ``handles`` = every rank's coll_handle() in rank order."""
+        blob = b"".join(bytes(h) for h in handles)
+        self._check(lib().cg_coll_connect(self.h, blob, len(handles)))
 
     # ---- run
     def assign(self, var: int, value):

@@ -37,6 +37,7 @@
 #include "conv_img_tc.h"
 #include "conv_small.h"
 #include "dot_small.h"
+#include "coll.h"
 #include "dot_tc.h"
 #include "kernels.h"
 #include "schedule.h"
@@ -306,6 +307,17 @@ struct cg_graph {
   // group of a DOT/CONV group and vice versa (-1: none); fused_away[d] = the DOT/CONV
   // value is never materialised (its consumer group is computed in the epilogue)
   std::vector<std::shared_ptr<DotTcPlan>> tcplan;
+  // f3 fused AllReduce + update over peer memory (CG_PLAN_FUSED_COLL): per
+  // ALLREDUCE group its segment (n == 0: none); device table = one entry per group
+  // followed by the batched steps of a full evaluation (contiguous per step)
+  bool fused_coll = false, coll_connected = false;
+  unsigned long long* coll_flags = nullptr;
+  CollArgs coll{};
+  std::vector<CollSeg> collseg;
+  std::vector<int> coll_entry;                       // group -> table index (-1 none)
+  std::map<std::vector<int>, std::pair<int, int>> coll_batch;  // step -> (first entry, count)
+  CollSeg* coll_dev = nullptr;
+  std::vector<void*> ipc_open;                       // peer mappings to close
   std::vector<int> partner;
   std::vector<char> fused_away;
   int n_fused = 0;
@@ -454,6 +466,76 @@ static void fuse_epilogues(cg_graph* g) {
     g->fused_away[d] = 1;
     g->n_fused++;
   }
+  // f3: the update chain of an ALLREDUCE_SUM (W - lr * g: a scalar / column / full
+  // tensor operand per op, all external) runs inside the fused collective
+  for (size_t gd = 0; gd < NG && g->fused_coll; ++gd) {
+    CollSeg& cs = g->collseg[gd];
+    if (cs.n == 0) continue;
+    const int d = hg.groups[gd].sink;
+    if (hg.keep[d] || consumers[d] != 1) continue;
+    const int ge = consumer_group[d];
+    const Group& E = hg.groups[ge];
+    if (E.kind != G_EW || E.materialised.size() != 1 || E.domain != hg.nodes[d].shape) continue;
+    const int64_t nall = numel(hg.nodes[d].shape), ncol = cs.ncol;
+    EpiProg prog{};
+    int prev = d;
+    bool ok = true;
+    for (int m : E.members) {
+      const Node& nd = hg.nodes[m];
+      int op = 0;
+      switch (nd.op) {
+        case CG_ADD: op = EPI_ADD; break;
+        case CG_SUB: op = EPI_SUB; break;
+        case CG_MUL: op = EPI_MUL; break;
+        case CG_DIV: op = EPI_DIV; break;
+        case CG_RELU: op = EPI_RELU; break;
+        case CG_MAX2: op = EPI_MAX; break;
+        case CG_MIN2: op = EPI_MIN; break;
+        default: ok = false;
+      }
+      if (!ok || prog.n == kEpiMax) { ok = false; break; }
+      const int e = prog.n++;
+      prog.op[e] = op;
+      if (op == EPI_RELU) {
+        ok = nd.preds.size() == 1 && nd.preds[0] == prev;
+      } else {
+        const int x0 = nd.preds[0], x1 = nd.preds[1];
+        if ((x0 == prev) == (x1 == prev)) { ok = false; break; }
+        const int x = x0 == prev ? x1 : x0;
+        prog.swap[e] = x0 == prev ? 0 : 1;
+        const Shape& xs = hg.nodes[x].shape;
+        const int64_t nx = numel(xs);
+        const bool col = nx == ncol && !xs.empty() && xs.back() == ncol;
+        const bool full = nx == nall && xs == hg.nodes[d].shape;
+        if (!hg.is_external(x) || !(nx == 1 || col || full)) { ok = false; break; }
+        prog.scalar[e] = nx == 1 ? 1 : (full && !col) ? 2 : 0;
+        prog.x[e] = g->ptr[x];
+      }
+      if (!ok) break;
+      prev = m;
+    }
+    if (!ok || prev != E.sink) continue;
+    {  // same block-clash rule as the DOT / CONV epilogues
+      const int B = hg.pl.block_of[E.sink];
+      bool clash = false;
+      if (B != hg.pl.block_of[d]) {
+        for (int gm = (int)gd + 1; gm < ge && !clash; ++gm) {
+          for (int p : hg.groups[gm].inputs)
+            if (!hg.is_external(p) && hg.pl.block_of[p] == B) clash = true;
+          for (int m : hg.groups[gm].materialised)
+            if (hg.pl.block_of[m] == B) clash = true;
+        }
+      }
+      if (clash) continue;
+    }
+    cs.epi = prog;
+    cs.out = g->ptr[E.sink];
+    g->glaunch[ge].clear();
+    g->partner[gd] = ge;
+    g->partner[ge] = (int)gd;
+    g->fused_away[d] = 1;
+    g->n_fused++;
+  }
 }
 
 // ---------------------------------------------------------------- plan: allocate + build launches
@@ -461,6 +543,7 @@ static int build_launches(cg_graph* g) {
   HostGraph& hg = g->hg;
   const int n = (int)hg.nodes.size();
   g->glaunch.assign(hg.groups.size(), {});
+  g->collseg.assign(hg.groups.size(), CollSeg{});
   size_t ws_need = 0;
   std::vector<KernelSpec> specs(hg.groups.size());
   // 1) specs + workspace sizes
@@ -546,13 +629,33 @@ static int build_launches(cg_graph* g) {
       case CG_ALLREDUCE_SUM: {
         const float* src = in[0];
         long long cnt = numel(ys);
-        if (nd.op == CG_ALLREDUCE_SUM && g->comm) {
+        if (nd.op == CG_ALLREDUCE_SUM && g->fused_coll) {  // f3: one peer-memory kernel (+ fused update)
+          const char* sp = reinterpret_cast<const char*>(src);
+          if (!g->pool || sp < g->pool || sp >= g->pool + hg.pl.pool_bytes)
+            return g->fail(CG_E_ARG, "ALLREDUCE_SUM node " + std::to_string(G.sink) + ": gradient is not a pool value");
+          CollSeg& cs = g->collseg[gi];
+          cs = CollSeg{};
+          cs.goff = (long long)((sp - g->pool) / (long long)sizeof(float));
+          cs.n = cnt;
+          cs.ncol = ys.empty() ? 1 : ys.back();
+          cs.out = out;
+          const int group = (int)gi;
+          L.push_back({[g, group](cudaStream_t s) {
+                         CollArgs a = g->coll;
+                         a.segs = g->coll_dev + g->coll_entry[group];
+                         a.nseg = 1;
+                         return launch_fused_allreduce(a, g->num_sms, s);
+                       },
+                       1});
+        } else if (nd.op == CG_ALLREDUCE_SUM && g->comm) {
           void* comm = g->comm;
           L.push_back({[src, out, cnt, comm](cudaStream_t s) {
                          int r = g_nccl.AllReduce(src, out, (size_t)cnt, /*ncclFloat32*/ 7, /*ncclSum*/ 0, comm, s);
                          return r == 0 ? cudaSuccess : cudaErrorUnknown;
                        },
                        1});
+        } else if (nd.op == CG_ALLREDUCE_SUM && g->world > 1) {
+          return g->fail(CG_E_ARG, "ALLREDUCE_SUM at world > 1 needs an NCCL id (cg_dist) or CG_PLAN_FUSED_COLL");
         } else if (src != out) {  // slid in place -> no work at all
           L.push_back({[src, out, cnt](cudaStream_t s) { return launch_copy(src, out, cnt, s); }, 1});
         }
@@ -740,6 +843,32 @@ static int build_launches(cg_graph* g) {
     for (int m : G.materialised)
       if (!g->fused_away[m] && hg.pl.block_of[m] >= 0) g->wr_blocks[host].push_back(hg.pl.block_of[m]);
   }
+  if (g->fused_coll) {  // f3 segment table: per group, then the batched steps of a full evaluation
+    std::vector<CollSeg> tab;
+    g->coll_entry.assign(NG, -1);
+    for (size_t gi = 0; gi < NG; ++gi) {
+      CollSeg& cs = g->collseg[gi];
+      if (cs.n == 0) continue;
+      cs.vec = (cs.n & 3) == 0 && (reinterpret_cast<uintptr_t>(cs.out) & 15) == 0 && (cs.goff & 3) == 0;
+      g->coll_entry[gi] = (int)tab.size();
+      tab.push_back(cs);
+    }
+    std::vector<char> all(NG, 1);
+    g->coll_batch.clear();
+    for (const auto& step : collective_schedule(all, g->rd_blocks, g->wr_blocks, g->uses_ws, g->is_coll)) {
+      if (step.size() < 2) continue;
+      bool every = true;
+      for (int gi : step) every = every && g->collseg[gi].n > 0;
+      if (!every) continue;
+      g->coll_batch[step] = {(int)tab.size(), (int)step.size()};
+      for (int gi : step) tab.push_back(g->collseg[gi]);
+    }
+    if (!tab.empty()) {
+      CUDA_TRY(g, cudaMalloc(&g->coll_dev, tab.size() * sizeof(CollSeg)), "cudaMalloc(coll table)");
+      CUDA_TRY(g, cudaMemcpy(g->coll_dev, tab.data(), tab.size() * sizeof(CollSeg), cudaMemcpyHostToDevice),
+               "cudaMemcpy(coll table)");
+    }
+  }
   return 0;
 }
 
@@ -856,6 +985,18 @@ static bool enqueue_groups(cg_graph* g, const std::vector<char>* R, int* kcount)
     }
     // collectives deferred and batched (schedule.h): one ncclGroupStart/End per batch
     for (const auto& step : collective_schedule(act, g->rd_blocks, g->wr_blocks, g->uses_ws, g->is_coll)) {
+      if (g->fused_coll && step.size() > 1) {  // f3: the whole step is ONE peer-memory kernel
+        auto it = g->coll_batch.find(step);
+        if (it != g->coll_batch.end()) {
+          CollArgs a = g->coll;
+          a.segs = g->coll_dev + it->second.first;
+          a.nseg = it->second.second;
+          if (launch_fused_allreduce(a, g->num_sms, g->stream) != cudaSuccess) return false;
+          *kcount += 1;
+          g->coll_batches += 1;
+          continue;
+        }
+      }
       const bool batch = step.size() > 1 && g->comm;
       if (batch && g_nccl.GroupStart() != 0) return false;
       for (int gi : step)
@@ -1041,10 +1182,16 @@ cg_graph* cg_create(int device, void* cuda_stream, const cg_dist* dist) {
       return nullptr;
     }
     cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (dist && (dist->world > 1 || dist->nccl_unique_id)) {  // a 1-rank communicator when an id is given
+    if (dist && (dist->rank < 0 || dist->world < 1 || dist->rank >= dist->world)) {
+      g_create_error = "cg_create: bad rank / world";
+      return nullptr;
+    }
+    if (dist && !dist->nccl_unique_id) {  // no NCCL: ALLREDUCE_SUM needs CG_PLAN_FUSED_COLL at world > 1
+      g->rank = dist->rank;
+      g->world = dist->world;
+    } else if (dist) {  // a communicator (1 rank when world == 1 and an id is given)
       std::string e;
       if (!g_nccl.load(&e)) { g_create_error = "cg_create: " + e; return nullptr; }
-      if (!dist->nccl_unique_id) { g_create_error = "cg_create: world > 1 needs nccl_unique_id"; return nullptr; }
       NcclUid uid;
       memcpy(uid.b, dist->nccl_unique_id, 128);
       int r = ((CommInitRankFn)g_nccl.CommInitRank)(&g->comm, dist->world, uid, dist->rank);
@@ -1149,15 +1296,27 @@ int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint3
   if (!g) return CG_E_ARG;
   if (g->state > 1) return g->fail(CG_E_STATE, "cg_plan_memory called twice");
   if (n_outputs <= 0 || !outputs) return g->fail(CG_E_ARG, "cg_plan_memory needs outputs");
-  if (flags & ~3u) return g->fail(CG_E_ARG, "unknown plan flag");
+  if (flags & ~7u) return g->fail(CG_E_ARG, "unknown plan flag");
   std::vector<int> outs(outputs, outputs + n_outputs);
   Error e{0, ""};
-  int r = g->hg.plan(outs, flags, &e);
+  int r = g->hg.plan(outs, flags & 3u, &e);  // (CG_PLAN_FUSED_COLL is an executor choice: same plan)
   if (r < 0) return g->fail(r, e.msg);
   HostGraph& hg = g->hg;
   g->info = cg_plan_info{};
   if (!g->host_only) {
     if ((r = allocate(g)) < 0) return r;
+    if (flags & CG_PLAN_FUSED_COLL) {  // f3: flag words; this rank's own pool and flags
+      if (g->world > kCollMaxRanks) return g->fail(CG_E_ARG, "fused collectives support at most 8 ranks");
+      g->fused_coll = true;
+      CUDA_TRY(g, cudaMalloc(&g->coll_flags, kCollFlagWords * sizeof(unsigned long long)), "cudaMalloc(coll flags)");
+      CUDA_TRY(g, cudaMemset(g->coll_flags, 0, kCollFlagWords * sizeof(unsigned long long)), "cudaMemset(coll flags)");
+      g->coll = CollArgs{};
+      g->coll.nranks = g->world;
+      g->coll.rank = g->rank;
+      g->coll.base[g->rank] = reinterpret_cast<const float*>(g->pool);
+      g->coll.flags[g->rank] = g->coll_flags;
+      g->coll_connected = g->world == 1;
+    }
     if ((r = build_launches(g)) < 0) return r;
     if ((r = setup_updates(g)) < 0) return r;
     // concurrent capture (CG_STREAMS, default 1: Gamma order on one stream)
@@ -1216,6 +1375,7 @@ int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float*
   if (!g) return CG_E_ARG;
   if (g->state != 2) return g->fail(CG_E_STATE, "cg_eval before cg_plan_memory");
   if (g->host_only) return g->fail(CG_E_NO_DEVICE, "host-only graph: no evaluation");
+  if (g->fused_coll && !g->coll_connected) return g->fail(CG_E_STATE, "fused collectives: call cg_coll_connect first");
   if (n_outputs < 0 || (n_outputs > 0 && !outputs)) return g->fail(CG_E_ARG, "bad outputs");
   HostGraph& hg = g->hg;
   std::vector<int> outs;
@@ -1333,6 +1493,9 @@ void cg_destroy(cg_graph* g) {
     cudaFree(g->upd_dev);
     cudaFree(g->stage_dev);
     cudaFree(g->stage_buf);
+    for (void* p : g->ipc_open) cudaIpcCloseMemHandle(p);
+    cudaFree(g->coll_dev);
+    cudaFree(g->coll_flags);
     if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);
     if (g->ev_in) cudaEventDestroy(g->ev_in);
     if (g->ev_out) cudaEventDestroy(g->ev_out);
@@ -1342,6 +1505,40 @@ void cg_destroy(cg_graph* g) {
 }
 
 const char* cg_last_error(const cg_graph* g) { return g ? g->err.c_str() : g_create_error.c_str(); }
+
+int cg_coll_handle(cg_graph* g, void* out, size_t cap) {
+  if (!g || !out) return CG_E_ARG;
+  if (g->state != 2 || !g->fused_coll) return g->fail(CG_E_STATE, "cg_coll_handle needs a graph planned with CG_PLAN_FUSED_COLL");
+  if (cap < 2 * sizeof(cudaIpcMemHandle_t)) return g->fail(CG_E_SIZE, "cg_coll_handle needs 128 bytes");
+  cudaIpcMemHandle_t h[2];
+  CUDA_TRY(g, cudaSetDevice(g->device), "cudaSetDevice");
+  CUDA_TRY(g, cudaIpcGetMemHandle(&h[0], g->pool), "cudaIpcGetMemHandle(pool)");
+  CUDA_TRY(g, cudaIpcGetMemHandle(&h[1], g->coll_flags), "cudaIpcGetMemHandle(flags)");
+  memcpy(out, h, sizeof(h));
+  return (int)sizeof(h);
+}
+
+int cg_coll_connect(cg_graph* g, const void* handles, int32_t world) {
+  if (!g || !handles) return CG_E_ARG;
+  if (g->state != 2 || !g->fused_coll) return g->fail(CG_E_STATE, "cg_coll_connect needs a graph planned with CG_PLAN_FUSED_COLL");
+  if (world != g->world) return g->fail(CG_E_ARG, "cg_coll_connect: world differs from cg_create's");
+  if (g->coll_connected) return 0;
+  CUDA_TRY(g, cudaSetDevice(g->device), "cudaSetDevice");
+  const auto* h = reinterpret_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int r = 0; r < world; ++r) {
+    if (r == g->rank) continue;
+    void* pool = nullptr;
+    void* flags = nullptr;
+    CUDA_TRY(g, cudaIpcOpenMemHandle(&pool, h[2 * r], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(pool)");
+    g->ipc_open.push_back(pool);
+    CUDA_TRY(g, cudaIpcOpenMemHandle(&flags, h[2 * r + 1], cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle(flags)");
+    g->ipc_open.push_back(flags);
+    g->coll.base[r] = reinterpret_cast<const float*>(pool);
+    g->coll.flags[r] = reinterpret_cast<unsigned long long*>(flags);
+  }
+  g->coll_connected = true;
+  return 0;
+}
 
 int cg_nccl_unique_id(void* out128) {
   std::string e;

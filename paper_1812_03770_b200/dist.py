@@ -11,7 +11,8 @@ without a concrete scheme; SURVEY §8(e) fixes two:
   (ncclAllReduce on the graph's stream, inside the captured CUDA graph) and the
   loss is scaled by 1/B_global, so the summed gradient is the global-batch mean.
 
-torch.distributed is used only to exchange the 128-byte NCCL unique id and for
+torch.distributed is used only to exchange the 128-byte NCCL unique id (or the
+128-byte peer-memory handles of the fused collectives, CG_PLAN_FUSED_COLL) and for
 barriers / max-over-ranks timing; the collective itself runs inside libcg.so.
 """
 from __future__ import annotations
@@ -52,9 +53,12 @@ def broadcast_nccl_id(make_id=None) -> bytes:
     return bytes(uid)
 
 
-def make_graph(device: int, world: int | None = None, rank: int | None = None, nccl_id: bytes | None = None):
+def make_graph(device: int, world: int | None = None, rank: int | None = None, nccl_id: bytes | None = None,
+               fused: bool = False):
     """cg.Graph on ``device``; with world > 1 it owns an NCCL communicator for its
-    ALLREDUCE_SUM nodes (the unique id is broadcast if not supplied)."""
+    ALLREDUCE_SUM nodes (the unique id is broadcast if not supplied) -- or, with
+    ``fused``, none: the graph is then planned with cg.PLAN_FUSED_COLL and
+    connected with connect_fused()."""
     import torch.distributed as dist
 
     if world is None:
@@ -63,9 +67,33 @@ def make_graph(device: int, world: int | None = None, rank: int | None = None, n
         return cg.Graph(device)
     if rank is None:
         rank = dist.get_rank()
+    if fused:
+        return cg.Graph(device, rank=rank, world=world, nccl_id=None)
     if nccl_id is None:
         nccl_id = broadcast_nccl_id()
     return cg.Graph(device, rank=rank, world=world, nccl_id=nccl_id)
+
+
+def gather_handles(handle: bytes) -> list:
+    """Every rank's 128-byte peer-memory handle, in rank order (all_gather_object
+    over the torch process group; world 1: just this one)."""
+    import torch.distributed as dist
+
+    if len(handle) != 128:
+        raise ValueError("peer-memory handle must be 128 bytes")
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [bytes(handle)]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, bytes(handle))
+    if any(not isinstance(h, (bytes, bytearray)) or len(h) != 128 for h in out):
+        raise RuntimeError("a rank sent a malformed peer-memory handle")
+    return [bytes(h) for h in out]
+
+
+def connect_fused(g) -> None:
+    """After g.plan_memory(..., cg.PLAN_FUSED_COLL): exchange the peer-memory handles
+    and map every rank's pool and flag words (cg_coll_connect)."""
+    g.coll_connect(gather_handles(g.coll_handle()))
 
 
 def dp_spec(config_fn, global_batch: int, rank: int, world: int, **kw) -> dict:

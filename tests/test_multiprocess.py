@@ -158,3 +158,50 @@ def test_c2_element_range_shards_concatenate_to_full():
     og, oo = from_spec(configs.c2(rows=rows, cols=cols))
     full = evaluate(og, leaf_values(og))[oo[0]]
     assert np.array_equal(np.concatenate([res[0], res[1]], axis=0), full)
+
+
+def _host_data(rec):
+    return materialise(rec["data"], rec["shape"]) if rec["op"] == "CONST" else None
+
+
+class _FakeGraph:
+    """Stands in for a planned cg.Graph on CPU: a per-rank handle, records connect."""
+
+    def __init__(self, rank):
+        self.handle = bytes([rank + 1]) * 64 + bytes([0xA0 + rank]) * 64
+        self.connected = None
+
+    def coll_handle(self):
+        return self.handle
+
+    def coll_connect(self, handles):
+        self.connected = list(handles)
+
+
+def _fused_connect(rank):
+    from paper_1812_03770_b200.dist import connect_fused
+    g = _FakeGraph(rank)
+    connect_fused(g)
+    return [h.hex() for h in g.connected]
+
+
+def test_fused_coll_handle_exchange():
+    """connect_fused (CG_PLAN_FUSED_COLL, f3): every rank receives every rank's
+    128-byte peer-memory handle, in rank order, identically."""
+    res = _run(_fused_connect)
+    want = [(bytes([r + 1]) * 64 + bytes([0xA0 + r]) * 64).hex() for r in range(WORLD)]
+    for r in range(WORLD):
+        assert res[r] == want
+
+
+def test_fused_coll_flag_host_only_plan():
+    """The flag is an executor choice: a host-only plan with it equals the plain plan."""
+    spec = configs.c3(batch=64, widths=(784, 32, 10))
+    dumps = []
+    for flags in (0, cg.PLAN_FUSED_COLL):
+        g, outs = cg.build_from_spec(spec, device=-1, data_fn=_host_data)
+        g.optimise(outs)
+        g.plan_memory(outs, flags)
+        dumps.append(g.dump_json(cg.DUMP_PLAN))
+        g.destroy()
+    assert dumps[0] == dumps[1]
