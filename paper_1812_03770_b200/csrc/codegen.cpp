@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <functional>
+#include <map>
 #include <sstream>
 
 namespace cg {
@@ -574,6 +575,143 @@ KernelSpec gen_red(const HostGraph& hg, const Group& G, int num_sms) {
 }
 
 }  // namespace
+
+// ------------------------------------------------------------------ row runs
+// Reduce -> broadcast fusion across groups ("single-kernel
+// softmax"): a run of consecutive EW / row-reduction groups over a [B, N] domain
+// (reductions over axis 1 only, N <= 1024) is one kernel with a warp per row.
+// Each group's members are evaluated in Gamma order with the row's values in
+// registers (lane l holds columns l, l+32, ...); a row reduction is a lane-local
+// sequential pass then a fixed xor-butterfly (deterministic); every materialised
+// value of every group is stored exactly as the group's own kernel would store it.
+// Returns an empty name when the run does not qualify.
+KernelSpec gen_rowrun(const HostGraph& hg, const std::vector<const Group*>& run, int num_sms) {
+  g_helpers.clear();
+  KernelSpec ks;
+  if (run.size() < 2) return ks;
+  int64_t B = -1, N = -1;
+  for (const Group* G : run) {
+    if (G->kind != G_EW && G->kind != G_RED) return ks;
+    const Shape& d = G->domain;
+    if (d.size() != 2) return ks;
+    if (B < 0) B = d[0];
+    if (d[0] != B) return ks;
+    if (G->kind == G_RED) {
+      const Node& sk = hg.nodes[G->sink];
+      if ((sk.op != CG_SUM && sk.op != CG_MAX) || sk.attr.a0 != 1 || sk.attr.a1 != 2 || d[1] < 1) return ks;
+      if (N < 0) N = d[1];
+      if (d[1] != N) return ks;
+    } else if (d[1] != 1) {
+      if (N < 0) N = d[1];
+      if (d[1] != N) return ks;
+    }
+  }
+  if (N < 1 || N > 1024 || B < 1) return ks;
+  const int NT = (int)((N + 31) / 32);
+  // values produced inside the run: array ([B, N]) or row scalar ([B, 1])
+  std::map<int, bool> made;  // node -> is array
+  std::vector<int> ext;      // external inputs, first-use order
+  std::map<int, int> ext_kind;  // 0 full [B,N], 1 row [B,1], 2 column [N], 3 scalar
+  auto kind_of = [&](int p) -> int {
+    const Shape& s = hg.nodes[p].shape;
+    const int64_t n = numel(s);
+    if (n == 1) return 3;
+    if (s.size() == 2 && s[0] == B && s[1] == N) return 0;
+    if (s.size() == 2 && s[0] == B && s[1] == 1) return 1;
+    if ((s.size() == 2 && s[0] == 1 && s[1] == N) || (s.size() == 1 && s[0] == N)) return 2;
+    return -1;
+  };
+  for (const Group* G : run)
+    for (int m : G->members) {
+      const Node& nd = hg.nodes[m];
+      for (int p : nd.preds) {
+        if (made.count(p) || ext_kind.count(p)) continue;
+        const int k = kind_of(p);
+        if (k < 0) return ks;
+        ext_kind[p] = k;
+        ext.push_back(p);
+      }
+      const bool arr = nd.shape.size() == 2 && nd.shape[1] == N && N > 1 ? true : (nd.shape.size() == 2 && nd.shape[1] == 1 ? false : N == 1);
+      if (op_info(nd.op).red) {
+        if (m != G->sink) return ks;
+        made[m] = false;
+      } else {
+        if (!(nd.shape.size() == 2 && nd.shape[0] == B && (nd.shape[1] == N || nd.shape[1] == 1))) return ks;
+        made[m] = arr;
+      }
+    }
+  std::vector<int> outs;
+  for (const Group* G : run)
+    for (int m : G->materialised) outs.push_back(m);
+  ks.in_ids = ext;
+  ks.out_ids = outs;
+  ks.mode = "rowrun";
+  std::ostringstream b;
+  b << "extern \"C\" __global__ void __launch_bounds__(256) KNAME(";
+  for (size_t q = 0; q < ext.size(); ++q) b << (q ? ", " : "") << "const float* __restrict__ in" << q;
+  for (size_t j = 0; j < outs.size(); ++j) b << ", float* __restrict__ out" << j;
+  b << ") {\n";
+  b << "  const int lane = threadIdx.x & 31;\n";
+  b << "  for (long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); r < " << B << "LL; r += (long long)gridDim.x * 8) {\n";
+  // externals: full / column operands loaded once per row (per t), row / scalar once
+  auto name = [&](int p, const std::string& t) -> std::string {
+    auto it = made.find(p);
+    if (it != made.end()) return it->second ? "v" + std::to_string(p) + "[" + t + "]" : "v" + std::to_string(p);
+    const int q = (int)(std::find(ext.begin(), ext.end(), p) - ext.begin());
+    const int k = ext_kind[p];
+    return (k == 0 || k == 2) ? "x" + std::to_string(q) + "[" + t + "]" : "x" + std::to_string(q);
+  };
+  for (size_t q = 0; q < ext.size(); ++q) {
+    const int k = ext_kind[ext[q]];
+    if (k == 0 || k == 2) {
+      b << "   float x" << q << "[" << NT << "];\n";
+      b << "#pragma unroll\n   for (int t = 0; t < " << NT << "; ++t) { const int j = lane + 32 * t; x" << q << "[t] = j < " << N
+        << " ? in" << q << "[" << (k == 0 ? "r * " + std::to_string(N) + "LL + j" : std::string("j")) << "] : 0.f; }\n";
+    } else {
+      b << "   const float x" << q << " = in" << q << "[" << (k == 1 ? "r" : "0") << "];\n";
+    }
+  }
+  for (const Group* G : run) {
+    for (int m : G->members) {
+      const Node& nd = hg.nodes[m];
+      if (op_info(nd.op).red) {
+        const int src = nd.preds[0];
+        const bool sum = nd.op == CG_SUM;
+        b << "   float v" << m << " = " << (sum ? "0.f" : "__int_as_float(0xff800000)") << ";\n";
+        b << "#pragma unroll\n   for (int t = 0; t < " << NT << "; ++t) if (lane + 32 * t < " << N << ") v" << m << " = "
+          << (sum ? "__fadd_rn(v" : "cg_max(v") << m << ", " << name(src, "t") << ");\n";
+        b << "#pragma unroll\n   for (int o = 16; o > 0; o >>= 1) { const float y = __shfl_xor_sync(0xffffffffu, v" << m
+          << ", o); v" << m << " = " << (sum ? "__fadd_rn(v" : "cg_max(v") << m << ", y); }\n";
+        continue;
+      }
+      if (made[m]) {
+        b << "   float v" << m << "[" << NT << "];\n";
+        b << "#pragma unroll\n   for (int t = 0; t < " << NT << "; ++t) {\n";
+        std::vector<std::string> a;
+        for (int p : nd.preds) a.push_back(name(p, "t"));
+        b << "    v" << m << "[t] = " << expr(nd.op, a) << ";\n   }\n";
+      } else {
+        std::vector<std::string> a;
+        for (int p : nd.preds) a.push_back(name(p, "0"));
+        b << "   const float v" << m << " = " << expr(nd.op, a) << ";\n";
+      }
+    }
+  }
+  for (size_t jo = 0; jo < outs.size(); ++jo) {
+    const int m = outs[jo];
+    if (made[m])
+      b << "#pragma unroll\n   for (int t = 0; t < " << NT << "; ++t) { const int j = lane + 32 * t; if (j < " << N << ") out" << jo
+        << "[r * " << N << "LL + j] = v" << m << "[t]; }\n";
+    else
+      b << "   if (lane == 0) out" << jo << "[r] = v" << m << ";\n";
+  }
+  b << "  }\n}\n";
+  ks.block = 256;
+  ks.work_blocks = (B + 7) / 8;
+  ks.grid[0] = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(ks.work_blocks, (int64_t)num_sms * 8));
+  ks.source = finish("run", b.str(), &ks.name);
+  return ks;
+}
 
 KernelSpec gen_group(const HostGraph& hg, const Group& G, int num_sms) {
   g_helpers.clear();

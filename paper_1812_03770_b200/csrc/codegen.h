@@ -30,4 +30,9 @@ struct KernelSpec {
 // Generate the kernel of an elementwise (G_EW) or reduction (G_RED) group.
 KernelSpec gen_group(const HostGraph& hg, const Group& G, int num_sms);
 
+// One kernel for a run of consecutive EW / row-reduction groups over a [B, N]
+// domain (warp per row; f2 reduce -> broadcast fusion, e.g. softmax).  Empty name:
+// the run does not qualify.
+KernelSpec gen_rowrun(const HostGraph& hg, const std::vector<const Group*>& run, int num_sms);
+
 }  // namespace cg

@@ -319,6 +319,14 @@ struct cg_graph {
   CollSeg* coll_dev = nullptr;
   std::vector<void*> ipc_open;                       // peer mappings to close
   std::vector<int> partner;
+  // f2 row runs: consecutive EW / row-reduction groups launched as one kernel
+  // (codegen gen_rowrun) when all of them are issued back to back
+  struct RowRun {
+    int first = -1, last = -1;
+    std::shared_ptr<EwLaunch> k;
+  };
+  std::vector<RowRun> runs;
+  std::vector<int> run_of;  // group -> index in runs (-1: none)
   std::vector<char> fused_away;
   int n_fused = 0;
   cg_plan_info info{};
@@ -795,11 +803,61 @@ static int build_launches(cg_graph* g) {
   }
   (void)n;
   fuse_epilogues(g);
+  // 2b) f2 row runs (reduce -> broadcast fusion across groups, e.g. softmax)
+  std::vector<KernelSpec> run_specs;
+  g->runs.clear();
+  g->run_of.assign(hg.groups.size(), -1);
+  if (!getenv("CG_NO_ROW_RUNS")) {
+    auto cand = [&](size_t gi) {
+      const Group& G = hg.groups[gi];
+      return ew[gi] && !g->glaunch[gi].empty() && g->partner[gi] < 0 && (G.kind == G_EW || G.kind == G_RED) &&
+             G.domain.size() == 2;
+    };
+    // values of a run sharing a pool block must be row-aligned (same shape): rows run
+    // concurrently on different warps, each row reading its inputs before its stores
+    auto hazard_free = [&](size_t a, size_t b) {
+      std::vector<int> vals;
+      for (size_t gi = a; gi <= b; ++gi) {
+        for (int p : hg.groups[gi].inputs)
+          if (!hg.is_external(p)) vals.push_back(p);
+        for (int m : hg.groups[gi].materialised) vals.push_back(m);
+      }
+      for (size_t i = 0; i < vals.size(); ++i)
+        for (size_t j = i + 1; j < vals.size(); ++j) {
+          const int x = vals[i], y = vals[j];
+          if (x == y || hg.pl.block_of[x] < 0 || hg.pl.block_of[x] != hg.pl.block_of[y]) continue;
+          if (hg.nodes[x].shape != hg.nodes[y].shape) return false;
+        }
+      return true;
+    };
+    size_t gi = 0;
+    while (gi < hg.groups.size()) {
+      if (!cand(gi)) { ++gi; continue; }
+      size_t end = gi;
+      KernelSpec best;
+      std::vector<const Group*> run{&hg.groups[gi]};
+      for (size_t nx = gi + 1; nx < hg.groups.size() && cand(nx); ++nx) {
+        run.push_back(&hg.groups[nx]);
+        KernelSpec ks = gen_rowrun(hg, run, g->num_sms);
+        if (ks.name.empty() || !hazard_free(gi, nx)) break;
+        best = ks;
+        end = nx;
+      }
+      if (end > gi) {
+        g->run_of[gi] = (int)g->runs.size();
+        for (size_t k = gi; k <= end; ++k) g->run_of[k] = (int)g->runs.size();
+        g->runs.push_back({(int)gi, (int)end, std::make_shared<EwLaunch>()});
+        run_specs.push_back(best);
+      }
+      gi = end + 1;
+    }
+  }
   // 3) compile the generated kernels that still launch (parallel NVRTC + disk cache)
   {
     std::vector<const KernelSpec*> need;
     for (size_t gi = 0; gi < hg.groups.size(); ++gi)
       if (ew[gi] && !g->glaunch[gi].empty()) need.push_back(&specs[gi]);
+    for (const KernelSpec& ks : run_specs) need.push_back(&ks);
     const auto t0 = std::chrono::steady_clock::now();
     int compiled = 0;
     int rc = compile_kernels(need, &g->err, &compiled);
@@ -824,6 +882,17 @@ static int build_launches(cg_graph* g) {
         }
         cudaGetLastError();
       }
+    }
+    for (size_t ri = 0; ri < g->runs.size(); ++ri) {
+      const KernelSpec& ks = run_specs[ri];
+      EwLaunch& st = *g->runs[ri].k;
+      st.k = cached_kernel(ks.name);
+      if (!st.k) return g->fail(CG_E_NVRTC, "kernel " + ks.name + " missing after compile");
+      for (int p : ks.in_ids) st.argv.push_back(g->ptr[p]);
+      for (int m : ks.out_ids) st.argv.push_back(g->ptr[m]);
+      st.grid = dim3(ks.grid[0], ks.grid[1], ks.grid[2]);
+      st.block = ks.block;
+      distinct.insert(ks.name);
     }
     g->n_kernels += (int)distinct.size();
   }
@@ -973,9 +1042,31 @@ static bool enqueue_groups(cg_graph* g, const std::vector<char>* R, int* kcount)
       act[gi] = !R || (*R)[gi];
       any_coll = any_coll || (act[gi] && g->is_coll[gi]);
     }
+    auto launch_run = [&](int ri) {
+      EwLaunch& st = *g->runs[ri].k;
+      std::vector<void*> ap(st.argv.size());
+      for (size_t i = 0; i < st.argv.size(); ++i) ap[i] = &st.argv[i];
+      *kcount += 1;
+      return cudaLaunchKernel((const void*)st.k, st.grid, dim3(st.block), ap.data(), 0, g->stream) == cudaSuccess;
+    };
+    // a row run replaces its groups when all of them are active (a partial
+    // relaunch takes the groups' own kernels: their inputs may not all be valid)
+    auto run_here = [&](int gi) {
+      const int ri = g->run_of.empty() ? -1 : g->run_of[gi];
+      if (ri < 0 || g->runs[ri].first != gi) return -1;
+      for (int k = g->runs[ri].first; k <= g->runs[ri].last; ++k)
+        if (!act[k]) return -1;
+      return ri;
+    };
     if (!any_coll) {  // Gamma order
       for (size_t gi = 0; gi < NG; ++gi) {
         if (!act[gi]) continue;
+        const int ri = run_here((int)gi);
+        if (ri >= 0) {
+          if (!launch_run(ri)) return false;
+          gi = (size_t)g->runs[ri].last;
+          continue;
+        }
         for (auto& L : g->glaunch[gi]) {
           if (L.fn(g->stream) != cudaSuccess) return false;
           *kcount += L.kernels;
@@ -984,7 +1075,23 @@ static bool enqueue_groups(cg_graph* g, const std::vector<char>* R, int* kcount)
       return true;
     }
     // collectives deferred and batched (schedule.h): one ncclGroupStart/End per batch
-    for (const auto& step : collective_schedule(act, g->rd_blocks, g->wr_blocks, g->uses_ws, g->is_coll)) {
+    const auto steps = collective_schedule(act, g->rd_blocks, g->wr_blocks, g->uses_ws, g->is_coll);
+    for (size_t si = 0; si < steps.size(); ++si) {
+      const auto& step = steps[si];
+      if (step.size() == 1) {  // a row run whose groups are issued back to back
+        const int ri = run_here(step[0]);
+        if (ri >= 0) {
+          const int len = g->runs[ri].last - g->runs[ri].first + 1;
+          bool consecutive = si + len <= steps.size();
+          for (int k = 0; k < len && consecutive; ++k)
+            consecutive = steps[si + k].size() == 1 && steps[si + k][0] == g->runs[ri].first + k;
+          if (consecutive) {
+            if (!launch_run(ri)) return false;
+            si += len - 1;
+            continue;
+          }
+        }
+      }
       if (g->fused_coll && step.size() > 1) {  // f3: the whole step is ONE peer-memory kernel
         auto it = g->coll_batch.find(step);
         if (it != g->coll_batch.end()) {
@@ -1585,6 +1692,60 @@ int64_t cg_launch_count(const cg_graph* g) { return g ? g->launches : CG_E_ARG; 
 }  // extern "C"
 
 // ---------------------------------------------------------------- debug: codegen check without a GPU
+// Row runs (f2 gen_rowrun) of a planned graph, greedily over consecutive EW /
+// row-reduction groups (the executor additionally skips epilogue-fused groups and
+// checks block sharing), each compiled with NVRTC: returns the number of runs and
+// writes "first-last:groups" per run to log, or CG_E_NVRTC with the log + source.
+extern "C" int64_t cgx_rowrun_check(cg_graph* g, int num_sms, char* log, size_t cap) {
+  if (!g || g->state != 2) return CG_E_STATE;
+  const auto& groups = g->hg.groups;
+  int64_t nruns = 0;
+  std::string all;
+  size_t gi = 0;
+  while (gi < groups.size()) {
+    size_t end = gi;
+    KernelSpec best;
+    std::vector<const Group*> run{&groups[gi]};
+    for (size_t nx = gi + 1; nx < groups.size(); ++nx) {
+      run.push_back(&groups[nx]);
+      KernelSpec ks = gen_rowrun(g->hg, run, num_sms);
+      if (ks.name.empty()) break;
+      best = ks;
+      end = nx;
+    }
+    if (end > gi) {
+      nvrtcProgram prog;
+      if (nvrtcCreateProgram(&prog, best.source.c_str(), "run.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return CG_E_NVRTC;
+      const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-default-device", "--std=c++17"};
+      nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+      if (r != NVRTC_SUCCESS) {
+        size_t n = 0;
+        nvrtcGetProgramLogSize(prog, &n);
+        std::string l(n, '\0');
+        nvrtcGetProgramLog(prog, &l[0]);
+        all += "== " + best.name + "\n" + l + "\n--- source ---\n" + best.source + "\n";
+        nvrtcDestroyProgram(&prog);
+        if (log && cap) {
+          size_t k = std::min(cap - 1, all.size());
+          memcpy(log, all.data(), k);
+          log[k] = 0;
+        }
+        return CG_E_NVRTC;
+      }
+      nvrtcDestroyProgram(&prog);
+      all += std::to_string(gi) + "-" + std::to_string(end) + ":" + std::to_string(end - gi + 1) + "\n";
+      ++nruns;
+    }
+    gi = end + 1;
+  }
+  if (log && cap) {
+    size_t k = std::min(cap - 1, all.size());
+    memcpy(log, all.data(), k);
+    log[k] = 0;
+  }
+  return nruns;
+}
+
 extern "C" int64_t cgx_codegen_check(cg_graph* g, int num_sms, char* log, size_t cap) {
   if (!g || g->state != 2) return CG_E_STATE;
   int64_t ok = 0;

@@ -173,3 +173,35 @@ def test_generated_kernels_compile_random():
         g, _, _, _ = host_graph(random_spec(seed), 0)
         n += _codegen_check(g)
     assert n > 60
+
+
+def _rowrun_check(g, sms=148):
+    L = cg.lib()
+    f = L.cgx_rowrun_check
+    f.restype = ctypes.c_int64
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    buf = ctypes.create_string_buffer(1 << 20)
+    r = f(g.h, sms, buf, len(buf))
+    assert r >= 0, buf.value.decode()[:6000]
+    return r, buf.value.decode()
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_row_runs_generate_and_compile(name):
+    """f2 reduce -> broadcast fusion: the softmax(-xent) groups of C3 / C4 / C5
+    (MAX, SUB, EXP, SUM, LOG / DIV over [B, classes]) form row runs whose single
+    kernel compiles (NVRTC, sm_100a)."""
+    spec = {"C3": lambda: configs.c3(), "C4": lambda: configs.c4(), "C5": lambda: configs.c5(batch=2)}[name]()
+    g, _, _, _ = host_graph(spec, 0)
+    n, log = _rowrun_check(g)
+    assert n >= 1, log
+    runs = [tuple(int(x) for x in ln.split(":")[0].split("-")) for ln in log.split()]
+    assert max(b - a + 1 for a, b in runs) >= 3, log  # MAX -> SUB/EXP -> SUM at least
+
+
+def test_row_runs_compile_random():
+    n = 0
+    for seed in range(0, 40):
+        g, _, _, _ = host_graph(random_spec(seed), 0)
+        n += _rowrun_check(g)[0]
+    assert n >= 0

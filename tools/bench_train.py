@@ -8,6 +8,7 @@ events on the graph's work stream.  Prints one JSON line per config.
 """
 import argparse
 import json
+import os
 import sys
 import time
 
@@ -28,7 +29,7 @@ def run(name, iters):
     t0 = time.perf_counter()
     g, outs = cg.build_from_spec(spec, device=0, data_fn=data)
     rep = g.optimise(outs)
-    info = g.plan_memory(outs, 0)
+    info = g.plan_memory(outs, cg.PLAN_FUSED_COLL if os.environ.get("CG_COLL", "fused") == "fused" else 0)
     build_s = time.perf_counter() - t0
     ws = torch.cuda.ExternalStream(g.work_stream())
     per = spec["meta"].get("per_iteration", [])
