@@ -70,4 +70,5 @@ def plan_json(c: Compiled) -> str:
                   "groups": [G.as_dict() for G in c.groups],
                   "keep": list(c.keep),
                   "plan_bytes": p.plan_bytes, "pool_bytes": p.pool_bytes,
-                  "unshared_bytes": c.unshared_bytes})
+                  "unshared_bytes": c.unshared_bytes,
+                  "views": [[v] + list(p.views[v]) for v in sorted(p.views)]})

@@ -18,11 +18,24 @@ rules of P:316-320 and the caveats of P:294-297, read as R1-R13:
       domain may be released before allocation; broadcast (smaller) inputs are
       released after it, so no thread overwrites an element another thread
       still has to read.
+  R14 zero-copy CONCAT ("reduce memory access"; a
+      sub-block view, the offset != 0 extension of P:303-310): outside
+      CG_PLAN_INCREMENTAL, an input v of a CONCAT c is planned as a VIEW of c's
+      block when v is the sink of its own group, c's group is v's only consumer,
+      v occurs once among c's inputs, v is not kept and v is not a Var / Const /
+      RESHAPE / ALLREDUCE_SUM.  Element (o, i) of v (o over the axes before the
+      concat axis, i within) is element o * inner(root) + offset + i of the view
+      root.  Concats are visited outer-first (reverse Gamma), so a view CONCAT's
+      inputs become views of the same root (offsets add).  The root's block is
+      allocated when the first value of its family is (FindBestBlock, no in-place
+      preference); views neither allocate nor release.
 """
 from __future__ import annotations
 
 from .ops import LEAF, numel
 from .schedule import FLAG_INCREMENTAL, dom_numel
+
+NO_VIEW_PRODUCERS = ("RESHAPE", "ALLREDUCE_SUM")
 
 ALIGN = 256
 
@@ -33,6 +46,7 @@ def align_up(x, a=ALIGN):
 
 class Plan:
     def __init__(self):
+        self.views = {}        # value id -> (root, outer, inner_root, offset, inner) (R14)
         self.block = {}        # value id -> block id
         self.size = []         # block id -> bytes (final, after growth)
         self.offsets = []
@@ -56,8 +70,43 @@ def find_best_block(reusable: set, size: list, s: int, pref=frozenset()):
     return b, False
 
 
+def concat_views(g, groups, keep, flags):
+    """R14: value -> (root, outer, inner_root, offset, inner) for zero-copy CONCAT."""
+    if flags & FLAG_INCREMENTAL:
+        return {}
+    sink_of = {G.sink for G in groups}
+    consumers = {}
+    for G in groups:
+        for p in G.inputs:
+            consumers[p] = consumers.get(p, 0) + 1
+    views = {}
+    for G in reversed(groups):
+        c = G.sink
+        n = g.nodes[c]
+        if n.op != "CONCAT":
+            continue
+        ax = int(n.attrs["axis"])
+        outer = numel(n.shape[:ax])
+        inner_c = numel(n.shape[ax:])
+        if c in views:
+            root, o_r, inner_root, base, _ = views[c]
+            if o_r != outer:
+                continue
+        else:
+            root, inner_root, base = c, inner_c, 0
+        off = 0
+        for v in n.preds:
+            inner_v = numel(g.nodes[v].shape[ax:])
+            nv = g.nodes[v]
+            if (v in sink_of and nv.op not in LEAF and nv.op not in NO_VIEW_PRODUCERS and v not in keep
+                    and consumers.get(v, 0) == 1 and n.preds.count(v) == 1):
+                views[v] = (root, outer, inner_root, base + off, inner_v)
+            off += inner_v
+    return views
+
+
 def plan_memory(g, groups, keep, flags):
-    """Algorithm 1 over groups in Gamma order (SURVEY §8(c) c7-algo + R13)."""
+    """Algorithm 1 over groups in Gamma order (SURVEY §8(c) c7-algo + R13 + R14)."""
     X = set()
     for G in groups:
         for p in G.inputs:
@@ -69,6 +118,7 @@ def plan_memory(g, groups, keep, flags):
             if p not in X:
                 refs[p] = refs.get(p, 0) + 1
     plan = Plan()
+    plan.views = views = concat_views(g, groups, keep, flags)
     reusable = set()
     size = plan.size
     incremental = bool(flags & FLAG_INCREMENTAL)
@@ -79,7 +129,7 @@ def plan_memory(g, groups, keep, flags):
         def release(ps):
             for p in ps:
                 refs[p] -= 1
-                if refs[p] == 0 and p not in keep:
+                if refs[p] == 0 and p not in keep and p not in views:
                     reusable.add(plan.block[p])
                     released.append(p)
 
@@ -89,7 +139,12 @@ def plan_memory(g, groups, keep, flags):
             release([p for p in pool_inputs if numel(g.nodes[p].shape) == dn])
         for m in G.materialised:
             nb = 4 * numel(g.nodes[m].shape)
-            if incremental and m in keep:
+            if m in views or m in plan.block:  # R14: the family's root block
+                root = views[m][0] if m in views else m
+                if root not in plan.block:
+                    plan.block[root], _ = find_best_block(reusable, size, 4 * numel(g.nodes[root].shape))
+                plan.block[m] = plan.block[root]
+            elif incremental and m in keep:
                 size.append(nb)
                 plan.block[m] = len(size) - 1
             else:

@@ -17,6 +17,9 @@ from .ops import numel
 
 
 def lifetimes(c):
+    """Per value: def = group step that writes it, last = last group step reading it.
+    A zero-copy CONCAT family (R14: the root and its views share one block by
+    design) is one lifetime: from its first def to the root's last read."""
     g = c.g
     d, last = {}, {}
     for t, G in enumerate(c.groups):
@@ -29,6 +32,15 @@ def lifetimes(c):
             last[m] = math.inf
         else:
             last.setdefault(m, d[m])
+    views = getattr(c.plan, "views", {})
+    for v, spec in views.items():
+        root = spec[0]
+        if root in d and v in d:
+            d[root] = min(d[root], d[v])
+    for v, spec in views.items():
+        root = spec[0]
+        if root in d and v in d:
+            d[v], last[v] = d[root], last[root]
     return d, last
 
 
@@ -51,7 +63,11 @@ def validate_plan(c, block=None, size=None):
     for m in materialised:
         if m in block:
             by_block.setdefault(block[m], []).append(m)
+    # a zero-copy CONCAT family (R14) is represented by its root: the views share the
+    # root's block and lifetime by construction
+    views = getattr(c.plan, "views", {})
     for b, vs in by_block.items():
+        vs = [v for v in vs if v not in views]
         for i in range(len(vs)):
             for j in range(len(vs)):
                 a, bb = vs[i], vs[j]

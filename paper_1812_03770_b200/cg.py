@@ -245,6 +245,15 @@ class Graph:
         return {f: getattr(info, f) for f, _ in cg_plan_info._fields_}
 
     # ---- fused collectives (CG_PLAN_FUSED_COLL)
+    def view_stats(self) -> dict:
+        """Zero-copy CONCAT slices (R14): written directly by their producer / via scratch."""
+        f = lib().cgx_view_stats
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        out = (ctypes.c_int64 * 2)()
+        self._check(f(self.h, out))
+        return {"direct": int(out[0]), "copied": int(out[1])}
+
     def coll_handle(self) -> bytes:
         """cg_coll_handle: this rank's 128-byte peer-memory handle (pool + flag words)."""
         buf = ctypes.create_string_buffer(128)

@@ -126,7 +126,7 @@ template <bool GATHER, int BNT, int CG>
 __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                    int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
-                   const __grid_constant__ EpiProg epi, float* __restrict__ dbg) {
+                   const __grid_constant__ EpiProg epi, float* __restrict__ dbg, int ldc) {
   using T = TC<BNT, CG, GATHER>;
   constexpr int BN = T::BN, SA = T::SA, SB = T::SB, LSTAGES = T::LSTAGES, BNH = BNT / CG;
   constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, LO_BYTES = T::LO_BYTES;
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
   } else if (warp < 10) {
     // ---------------- warps 6..9: epilogue; this warp may touch TMEM lanes [32*(warp%4), +32)
     const int sub = warp % 4;
-    const bool vec = (N % 4) == 0;
+    const bool vec = (N % 4) == 0 && (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
     int j = 0;
     for (int u = u_first; u < units; u += u_step, ++j) {
       int z, m0, n0, kb0, nk;
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           }
         }
         if (row < M && n0 + c0 < N) {
-          float* crow = Cz + (size_t)row * N;
+          float* crow = Cz + (size_t)row * ldc;
           const int n = n0 + c0;
           if (vec && n + 16 <= N) {
 #pragma unroll
@@ -768,7 +768,8 @@ cudaError_t launch_tc(const DotTcPlan& p, float* out, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<G, BNT, CG>, a, b, out, p.M, p.N, p.K, G ? 0 : p.a_mn, G ? 1 : p.b_mn,
-                            p.kb_per_split, p.splits, p.conv, p.raw_hi, p.epi, p.dbg);
+                            p.kb_per_split, p.splits, p.conv, p.raw_hi, p.epi, p.dbg,
+                            p.splits > 1 || p.ldc <= 0 ? p.N : p.ldc);
 }
 
 template <bool G, int BNT>

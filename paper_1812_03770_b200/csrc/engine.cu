@@ -327,6 +327,11 @@ struct cg_graph {
   };
   std::vector<RowRun> runs;
   std::vector<int> run_of;  // group -> index in runs (-1: none)
+  // R14 zero-copy CONCAT: view values whose writer cannot store a strided slice are
+  // computed into a scratch buffer and copied into the slice (view_scratch owns them)
+  std::vector<float*> view_addr;     // node -> its slice address (views only)
+  std::vector<void*> view_scratch;
+  int n_views_direct = 0, n_views_copied = 0;
   std::vector<char> fused_away;
   int n_fused = 0;
   cg_plan_info info{};
@@ -389,6 +394,12 @@ static ConvGeom geom(const Node& nd, const Shape& x, const Shape& y, int kh, int
 // scalars as the other operands, runs that chain in its epilogue and writes the
 // chain's sink directly; d is never materialised.  The Alg. 1 plan is unchanged
 // (d's block is simply not written).  Readings: DESIGN.md "f2 epilogue fusion".
+// R14: a zero-copy CONCAT family (root + its views) shares one block by design;
+// a slice stays intact while the block's last writer is a member of the family
+static inline int family(const HostGraph& hg, int v) {
+  return v >= 0 && !hg.pl.view_root.empty() && hg.pl.view_root[v] >= 0 ? hg.pl.view_root[v] : v;
+}
+
 static void fuse_epilogues(cg_graph* g) {
   HostGraph& hg = g->hg;
   const size_t NG = hg.groups.size();
@@ -457,11 +468,16 @@ static void fuse_epilogues(cg_graph* g) {
       const int B = hg.pl.block_of[E.sink];
       bool clash = false;
       if (B != hg.pl.block_of[d]) {
-        for (int gm = (int)gd + 1; gm < ge && !clash; ++gm) {
+        // from gd itself: the producer must not read the block it now writes (its own
+        // input may have died at gd and left its block to the sink -- a zero-copy
+        // CONCAT root takes any free block, without the in-place preference)
+        for (int gm = (int)gd; gm < ge && !clash; ++gm) {
+          // (other slices of the sink's zero-copy CONCAT family are disjoint: no clash)
           for (int p : hg.groups[gm].inputs)
-            if (!hg.is_external(p) && hg.pl.block_of[p] == B) clash = true;
+            if (!hg.is_external(p) && hg.pl.block_of[p] == B && family(hg, p) != family(hg, E.sink)) clash = true;
+          if (gm == (int)gd) continue;
           for (int m : hg.groups[gm].materialised)
-            if (hg.pl.block_of[m] == B) clash = true;
+            if (hg.pl.block_of[m] == B && family(hg, m) != family(hg, E.sink)) clash = true;
         }
       }
       if (clash) continue;
@@ -527,11 +543,16 @@ static void fuse_epilogues(cg_graph* g) {
       const int B = hg.pl.block_of[E.sink];
       bool clash = false;
       if (B != hg.pl.block_of[d]) {
-        for (int gm = (int)gd + 1; gm < ge && !clash; ++gm) {
+        // from gd itself: the producer must not read the block it now writes (its own
+        // input may have died at gd and left its block to the sink -- a zero-copy
+        // CONCAT root takes any free block, without the in-place preference)
+        for (int gm = (int)gd; gm < ge && !clash; ++gm) {
+          // (other slices of the sink's zero-copy CONCAT family are disjoint: no clash)
           for (int p : hg.groups[gm].inputs)
-            if (!hg.is_external(p) && hg.pl.block_of[p] == B) clash = true;
+            if (!hg.is_external(p) && hg.pl.block_of[p] == B && family(hg, p) != family(hg, E.sink)) clash = true;
+          if (gm == (int)gd) continue;
           for (int m : hg.groups[gm].materialised)
-            if (hg.pl.block_of[m] == B) clash = true;
+            if (hg.pl.block_of[m] == B && family(hg, m) != family(hg, E.sink)) clash = true;
         }
       }
       if (clash) continue;
@@ -598,10 +619,36 @@ static int build_launches(cg_graph* g) {
   // 2) closures
   g->tcplan.assign(hg.groups.size(), nullptr);
   std::vector<std::shared_ptr<EwLaunch>> ew(hg.groups.size());
+  // R14: a writer that cannot store a strided slice computes into scratch, then a
+  // strided copy (the concat kernel with one source) places it
+  auto is_view = [&](int v) { return !hg.pl.view_root.empty() && hg.pl.view_root[v] >= 0; };
+  auto to_scratch = [&](int v) -> int {
+    float* sp = nullptr;
+    CUDA_TRY(g, cudaMalloc(&sp, 4 * (size_t)numel(hg.nodes[v].shape)), "cudaMalloc(view scratch)");
+    g->view_scratch.push_back(sp);
+    g->ptr[v] = sp;
+    return 0;
+  };
+  auto slice_copy = [&](int v) {
+    ConcatArgs a{};
+    a.src[0] = g->ptr[v];
+    a.inner[0] = hg.pl.view_inner[v];
+    a.offset[0] = 0;
+    a.n = 1;
+    float* dst = g->view_addr[v];
+    const long long outer = hg.pl.view_outer[v], dinner = hg.pl.view_inner_root[v];
+    return Launch{[a, dst, outer, dinner](cudaStream_t s) { return launch_concat(a, dst, outer, dinner, s); }, 1};
+  };
+  std::vector<int> pending_copy(hg.groups.size(), -1);
   for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
     const Group& G = hg.groups[gi];
     auto& L = g->glaunch[gi];
     const Node& nd = hg.nodes[G.sink];
+    if (is_view(G.sink) && G.kind != G_EW && nd.op != CG_CONCAT) {
+      int rv = to_scratch(G.sink);
+      if (rv < 0) return rv;
+      pending_copy[gi] = G.sink;
+    }
     if (G.kind == G_EW || G.kind == G_RED) {
       // the kernel is compiled after epilogue fusion (a chain computed in its
       // producer's epilogue is never compiled); the launch reads it from `st`
@@ -783,18 +830,22 @@ static int build_launches(cg_graph* g) {
         long long outer = 1, dst_inner = 1;
         for (int k = 0; k < ax; ++k) outer *= ys[k];
         for (size_t k = ax; k < ys.size(); ++k) dst_inner *= ys[k];
+        if (is_view(G.sink)) dst_inner = hg.pl.view_inner_root[G.sink];  // this concat is itself a slice
         long long off = 0;
         for (size_t i = 0; i < in.size(); ++i) {
           const Shape& s = hg.nodes[nd.preds[i]].shape;
           long long inner = 1;
           for (size_t k = ax; k < s.size(); ++k) inner *= s[k];
-          a.src[i] = in[i];
-          a.inner[i] = inner;
-          a.offset[i] = off;
+          if (!is_view(nd.preds[i])) {  // R14: a view input already sits in its slice
+            a.src[a.n] = in[i];
+            a.inner[a.n] = inner;
+            a.offset[a.n] = off;
+            a.n++;
+          }
           off += inner;
         }
-        a.n = (int)in.size();
-        L.push_back({[a, out, outer, dst_inner](cudaStream_t s) { return launch_concat(a, out, outer, dst_inner, s); }, 1});
+        if (a.n > 0)
+          L.push_back({[a, out, outer, dst_inner](cudaStream_t s) { return launch_concat(a, out, outer, dst_inner, s); }, 1});
         break;
       }
       default:
@@ -802,7 +853,41 @@ static int build_launches(cg_graph* g) {
     }
   }
   (void)n;
+  for (size_t gi = 0; gi < hg.groups.size(); ++gi)
+    if (pending_copy[gi] >= 0) {
+      g->glaunch[gi].push_back(slice_copy(pending_copy[gi]));
+      g->n_views_copied++;
+    }
   fuse_epilogues(g);
+  // R14: an elementwise writer of a view either runs in a tensor-core epilogue that
+  // stores the slice directly (row stride = the root's), or computes into scratch
+  for (size_t gi = 0; gi < hg.groups.size(); ++gi) {
+    const Group& G = hg.groups[gi];
+    if (G.kind != G_EW || !is_view(G.sink)) continue;
+    const int v = G.sink;
+    const int gd = g->partner[gi];
+    if (g->glaunch[gi].empty() && gd >= 0 && g->tcplan[gd]) {
+      DotTcPlan& P = *g->tcplan[gd];
+      if (hg.pl.view_outer[v] == P.M && hg.pl.view_inner[v] == P.N) {
+        P.ldc = (int)hg.pl.view_inner_root[v];
+        g->n_views_direct++;
+        continue;
+      }
+      if (hg.pl.view_outer[v] == 1) {  // contiguous slice
+        g->n_views_direct++;
+        continue;
+      }
+      return g->fail(CG_E_ARG, "view " + std::to_string(v) + ": epilogue cannot store this slice");
+    }
+    // the group's own kernel: its sink argument -> scratch, then the slice copy
+    const KernelSpec& ks = specs[gi];
+    const size_t pos = ks.in_ids.size() + (size_t)(std::find(ks.out_ids.begin(), ks.out_ids.end(), v) - ks.out_ids.begin());
+    int rv = to_scratch(v);
+    if (rv < 0) return rv;
+    ew[gi]->argv[pos] = g->ptr[v];
+    g->glaunch[gi].push_back(slice_copy(v));
+    g->n_views_copied++;
+  }
   // 2b) f2 row runs (reduce -> broadcast fusion across groups, e.g. softmax)
   std::vector<KernelSpec> run_specs;
   g->runs.clear();
@@ -811,7 +896,7 @@ static int build_launches(cg_graph* g) {
     auto cand = [&](size_t gi) {
       const Group& G = hg.groups[gi];
       return ew[gi] && !g->glaunch[gi].empty() && g->partner[gi] < 0 && (G.kind == G_EW || G.kind == G_RED) &&
-             G.domain.size() == 2;
+             G.domain.size() == 2 && !is_view(G.sink);
     };
     // values of a run sharing a pool block must be row-aligned (same shape): rows run
     // concurrently on different warps, each row reading its inputs before its stores
@@ -1009,6 +1094,13 @@ static int allocate(cg_graph* g) {
       g->ptr[v] = reinterpret_cast<float*>(g->pool + hg.pl.offset[hg.pl.block_of[v]]);
     }
   }
+  // R14 views: the first element of a zero-copy CONCAT slice (row stride = the root's)
+  g->view_addr.assign(n, nullptr);
+  for (int v = 0; v < n; ++v)
+    if (!hg.pl.view_root.empty() && hg.pl.view_root[v] >= 0) {
+      g->ptr[v] = reinterpret_cast<float*>(g->pool + hg.pl.offset[hg.pl.block_of[v]]) + hg.pl.view_off[v];
+      g->view_addr[v] = g->ptr[v];
+    }
   g->info.external_bytes = ext;
   return 0;
 }
@@ -1017,7 +1109,8 @@ static int allocate(cg_graph* g) {
 static bool valid(cg_graph* g, int p) {
   HostGraph& hg = g->hg;
   if (hg.is_external(p)) return true;
-  return !g->dirty[p] && g->owner[hg.pl.block_of[p]] == p;
+  const int o = g->owner[hg.pl.block_of[p]];
+  return !g->dirty[p] && (o == p || (o >= 0 && family(hg, o) == family(hg, p)));
 }
 
 static void mark_dirty_from_var(cg_graph* g, int var) {
@@ -1517,8 +1610,11 @@ int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float*
     int bad = -1;
     for (size_t gi = 0; gi < NG && bad < 0; ++gi) {
       if (!R[gi]) continue;
-      for (int p : hg.groups[gi].inputs)
-        if (!hg.is_external(p) && sim[hg.pl.block_of[p]] != p) { bad = p; break; }
+      for (int p : hg.groups[gi].inputs) {
+        if (hg.is_external(p)) continue;
+        const int o = sim[hg.pl.block_of[p]];
+        if (o != p && (o < 0 || family(hg, o) != family(hg, p))) { bad = p; break; }
+      }
       if (bad >= 0) break;
       for (int m : hg.groups[gi].materialised) sim[hg.pl.block_of[m]] = m;
     }
@@ -1601,6 +1697,7 @@ void cg_destroy(cg_graph* g) {
     cudaFree(g->stage_dev);
     cudaFree(g->stage_buf);
     for (void* p : g->ipc_open) cudaIpcCloseMemHandle(p);
+    for (void* p : g->view_scratch) cudaFree(p);
     cudaFree(g->coll_dev);
     cudaFree(g->coll_flags);
     if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);
@@ -1744,6 +1841,15 @@ extern "C" int64_t cgx_rowrun_check(cg_graph* g, int num_sms, char* log, size_t 
     log[k] = 0;
   }
   return nruns;
+}
+
+// R14 zero-copy CONCAT at run time: slices written directly by their producer
+// (tensor-core epilogue with the root's row stride) / through scratch + a slice copy.
+extern "C" int cgx_view_stats(const cg_graph* g, int64_t* out2) {
+  if (!g || !out2) return CG_E_ARG;
+  out2[0] = g->n_views_direct;
+  out2[1] = g->n_views_copied;
+  return 0;
 }
 
 extern "C" int64_t cgx_codegen_check(cg_graph* g, int num_sms, char* log, size_t cap) {

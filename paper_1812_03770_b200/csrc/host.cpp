@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Host compiler: graph, shape inference, optimiser, ordering, fusion grouping,
 // Algorithm 1 planner, canonical dumps.  See host.h for the paper anchors.
 #include "host.h"
@@ -660,13 +661,60 @@ int HostGraph::plan(const std::vector<int>& outs_in, uint32_t fl, Error* err) {
     G.safe = allew || (G.members.size() == 1 &&
                        (nodes[G.sink].op == CG_RESHAPE || nodes[G.sink].op == CG_ALLREDUCE_SUM));
   }
-  // Algorithm 1 on groups [P:323-362] with readings R1-R13
+  // Algorithm 1 on groups [P:323-362] with readings R1-R14
   pl = Plan();
   pl.block_of.assign(n, -1);
   std::vector<int> refs(n, 0);
   for (auto& G : groups)
     for (int p : G.inputs)
       if (!is_external(p)) refs[p]++;
+  // R14 zero-copy CONCAT: inputs planned as views of the concat's block (outer
+  // concats first, so nested concats map to one root); see oracle/planner.py
+  pl.view_root.assign(n, -1);
+  pl.view_outer.assign(n, 0);
+  pl.view_inner_root.assign(n, 0);
+  pl.view_off.assign(n, 0);
+  pl.view_inner.assign(n, 0);
+  if (!incremental && !getenv("CG_NO_CONCAT_VIEWS")) {  // (the env switch is a debugging aid: dumps then differ)
+    std::vector<char> is_sink(n, 0);
+    std::vector<int> consumers(n, 0);
+    for (auto& G : groups) {
+      is_sink[G.sink] = 1;
+      for (int p : G.inputs) consumers[p]++;
+    }
+    for (auto it = groups.rbegin(); it != groups.rend(); ++it) {
+      const int c = it->sink;
+      const Node& nc = nodes[c];
+      if (nc.op != CG_CONCAT) continue;
+      const int ax = nc.attr.axis;
+      int64_t outer = 1, inner_c = 1;
+      for (int k = 0; k < (int)nc.shape.size(); ++k) (k < ax ? outer : inner_c) *= nc.shape[k];
+      int root = c;
+      int64_t inner_root = inner_c, base = 0;
+      if (pl.view_root[c] >= 0) {
+        if (pl.view_outer[c] != outer) continue;
+        root = pl.view_root[c];
+        inner_root = pl.view_inner_root[c];
+        base = pl.view_off[c];
+      }
+      int64_t off = 0;
+      for (int v : nc.preds) {
+        int64_t inner_v = 1;
+        for (int k = ax; k < (int)nodes[v].shape.size(); ++k) inner_v *= nodes[v].shape[k];
+        const int op = nodes[v].op;
+        const bool once = std::count(nc.preds.begin(), nc.preds.end(), v) == 1;
+        if (is_sink[v] && !is_external(v) && op != CG_RESHAPE && op != CG_ALLREDUCE_SUM && !keep[v] &&
+            consumers[v] == 1 && once) {
+          pl.view_root[v] = root;
+          pl.view_outer[v] = outer;
+          pl.view_inner_root[v] = inner_root;
+          pl.view_off[v] = base + off;
+          pl.view_inner[v] = inner_v;
+        }
+        off += inner_v;
+      }
+    }
+  }
   std::set<std::pair<uint64_t, int>> reusable;
   auto& size = pl.size;
   auto new_block = [&](uint64_t s) {
@@ -703,7 +751,7 @@ int HostGraph::plan(const std::vector<int>& outs_in, uint32_t fl, Error* err) {
       for (int p : G.inputs) {
         if (is_external(p)) continue;
         if (phase_filter && ((numel(nodes[p].shape) == dn) != want_full)) continue;
-        if (--refs[p] == 0 && !keep[p]) {
+        if (--refs[p] == 0 && !keep[p] && pl.view_root[p] < 0) {
           reusable.insert({size[pl.block_of[p]], pl.block_of[p]});
           released.push_back(p);
         }
@@ -712,7 +760,11 @@ int HostGraph::plan(const std::vector<int>& outs_in, uint32_t fl, Error* err) {
     if (G.safe) release(true, true);
     for (int m : G.materialised) {
       uint64_t nb = 4 * (uint64_t)numel(nodes[m].shape);
-      if (incremental && keep[m]) {
+      if (pl.view_root[m] >= 0 || pl.block_of[m] >= 0) {  // R14: the family's root block
+        const int root = pl.view_root[m] >= 0 ? pl.view_root[m] : m;
+        if (pl.block_of[root] < 0) pl.block_of[root] = find_best_block(4 * (uint64_t)numel(nodes[root].shape), {});
+        pl.block_of[m] = pl.block_of[root];
+      } else if (incremental && keep[m]) {
         pl.block_of[m] = new_block(nb);
       } else {
         std::vector<int> pref;
@@ -850,7 +902,15 @@ std::string HostGraph::plan_json() const {
       first = false;
     }
   o << "],\"plan_bytes\":" << pl.plan_bytes << ",\"pool_bytes\":" << pl.pool_bytes
-    << ",\"unshared_bytes\":" << unshared_bytes << "}";
+    << ",\"unshared_bytes\":" << unshared_bytes << ",\"views\":[";
+  first = true;
+  for (int v = 0; v < (int)pl.view_root.size(); ++v)
+    if (pl.view_root[v] >= 0) {
+      o << (first ? "" : ",") << "[" << v << "," << pl.view_root[v] << "," << pl.view_outer[v] << ","
+        << pl.view_inner_root[v] << "," << pl.view_off[v] << "," << pl.view_inner[v] << "]";
+      first = false;
+    }
+  o << "]}";
   return o.str();
 }
 

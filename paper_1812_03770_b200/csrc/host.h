@@ -63,6 +63,10 @@ struct Group {
 };
 
 struct Plan {
+  // R14 zero-copy CONCAT views: node -> root (-1: not a view); element (o, i) of a
+  // view is element o * view_inner_root + view_off + i of the root
+  std::vector<int> view_root;
+  std::vector<int64_t> view_outer, view_inner_root, view_off, view_inner;
   std::vector<int> block_of;         // node id -> block id (-1: not pooled)
   std::vector<uint64_t> size;        // block id -> bytes (exact, after growth)
   std::vector<uint64_t> offset;      // block id -> byte offset in the pool (256-aligned)

@@ -497,13 +497,16 @@ __global__ void avgpool_kernel(const float* __restrict__ x, float* __restrict__ 
 }
 
 template <typename I>
-__global__ void concat_kernel(ConcatArgs a, float* __restrict__ dst, I outer, I dst_inner) {
-  const I total = outer * dst_inner;
+__global__ void concat_kernel(ConcatArgs a, float* __restrict__ dst, I outer, I dst_inner, I src_inner) {
+  // iterate over the SOURCE elements (src_inner = sum of the sources' inner extents):
+  // columns of the destination row that no source covers are left untouched
+  const I total = outer * src_inner;
   for (I t = (I)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
-    const I row = t / dst_inner, col = t % dst_inner;
+    const I row = t / src_inner;
+    I c = t % src_inner;
     int k = 0;
-    while (k + 1 < a.n && col >= a.offset[k + 1]) ++k;
-    dst[t] = a.src[k][row * a.inner[k] + (col - a.offset[k])];
+    while (k + 1 < a.n && c >= (I)a.inner[k]) c -= (I)a.inner[k++];
+    dst[row * dst_inner + a.offset[k] + c] = a.src[k][row * a.inner[k] + c];
   }
 }
 
@@ -673,13 +676,14 @@ __global__ void pool4_kernel(const float4* __restrict__ x, float4* __restrict__ 
   }
 }
 
-__global__ void concat4_kernel(ConcatArgs a, float4* __restrict__ dst, int outer, int dst_inner4) {
-  const int total = outer * dst_inner4;
+__global__ void concat4_kernel(ConcatArgs a, float4* __restrict__ dst, int outer, int dst_inner4, int src_inner4) {
+  const int total = outer * src_inner4;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    const int row = t / dst_inner4, col = (t - row * dst_inner4) * 4;
-    int k = 0;
-    while (k + 1 < a.n && col >= a.offset[k + 1]) ++k;
-    dst[t] = __ldg(reinterpret_cast<const float4*>(a.src[k] + (size_t)row * a.inner[k] + (col - a.offset[k])));
+    const int row = t / src_inner4;
+    int c = (t - row * src_inner4) * 4, k = 0;
+    while (k + 1 < a.n && c >= (int)a.inner[k]) c -= (int)a.inner[k++];
+    dst[(size_t)row * dst_inner4 + (a.offset[k] + c) / 4] =
+        __ldg(reinterpret_cast<const float4*>(a.src[k] + (size_t)row * a.inner[k] + c));
   }
 }
 
@@ -841,16 +845,21 @@ cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStre
 }
 
 cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long long dst_inner, cudaStream_t s) {
-  bool vec = dst_inner % 4 == 0 && outer * dst_inner < INT32_MAX;
-  for (int k = 0; k < a.n; ++k) vec = vec && a.inner[k] % 4 == 0 && a.offset[k] % 4 == 0;
+  if (a.n < 1) return cudaSuccess;
+  long long src_inner = 0;
+  for (int k = 0; k < a.n; ++k) src_inner += a.inner[k];
+  bool vec = dst_inner % 4 == 0 && outer * dst_inner < INT32_MAX && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  for (int k = 0; k < a.n; ++k)
+    vec = vec && a.inner[k] % 4 == 0 && a.offset[k] % 4 == 0 && (reinterpret_cast<uintptr_t>(a.src[k]) & 15) == 0;
   if (vec) {
-    concat4_kernel<<<grid_for(outer * dst_inner / 4), 256, 0, s>>>(a, (float4*)dst, (int)outer, (int)(dst_inner / 4));
+    concat4_kernel<<<grid_for(outer * src_inner / 4), 256, 0, s>>>(a, (float4*)dst, (int)outer, (int)(dst_inner / 4),
+                                                                   (int)(src_inner / 4));
     return cudaGetLastError();
   }
   if (outer * dst_inner < INT32_MAX)
-    concat_kernel<int><<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, (int)outer, (int)dst_inner);
+    concat_kernel<int><<<grid_for(outer * src_inner), 256, 0, s>>>(a, dst, (int)outer, (int)dst_inner, (int)src_inner);
   else
-    concat_kernel<long long><<<grid_for(outer * dst_inner), 256, 0, s>>>(a, dst, outer, dst_inner);
+    concat_kernel<long long><<<grid_for(outer * src_inner), 256, 0, s>>>(a, dst, outer, dst_inner, src_inner);
   return cudaGetLastError();
 }
 

@@ -44,7 +44,7 @@ struct ConcatArgs {
   const float* src[kMaxConcat];
   long long inner[kMaxConcat];   // elements per outer index contributed by each source
   long long offset[kMaxConcat];  // element offset of each source inside a destination row
-  int n;
+  int n;                         // sources: they need not cover the row (R14 slices stay untouched)
 };
 cudaError_t launch_concat(const ConcatArgs& a, float* dst, long long outer, long long dst_inner, cudaStream_t s);
 

@@ -850,3 +850,52 @@ def test_concurrent_capture_bit_identical(which, monkeypatch):
     got = _run_training_state(spec, 4)
     for a, b in zip(got, ref):
         assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------- R14 zero-copy CONCAT
+def test_zero_copy_concat_inception_block():
+    """An Inception-style block: two tensor-core conv branches with a BN-like
+    scale/shift + ReLU epilogue, a max-pool branch and a nested concat; the conv
+    branches must store straight into their slices of the concat block (the
+    epilogue's row stride = the concat's channels), the pool branch through a
+    slice copy, and every value must match the oracle."""
+    rng = np.random.default_rng(21)
+    n, h, w, ci = 16, 35, 35, 32  # >= one wave of 128-row tiles: no split-K, the epilogue stores
+    og = OGraph()
+    g = cg.Graph(0)
+    x = rng.uniform(-1, 1, (n, h, w, ci)).astype(np.float32)
+    vx, ox = g.var(x.shape), og.add_leaf("VAR", x.shape)
+    vals = {ox: x}
+    branches_g, branches_o = [], []
+    for k, co in enumerate((64, 96)):
+        wk = (rng.uniform(-1, 1, (3, 3, ci, co)) / 9).astype(np.float32)
+        sc = rng.uniform(0.5, 1.5, (co,)).astype(np.float32)
+        sh = rng.uniform(-0.1, 0.1, (co,)).astype(np.float32)
+        vw, ow = g.var(wk.shape), og.add_leaf("VAR", wk.shape)
+        vs, os_ = g.const(sc), og.add_leaf("CONST", sc.shape, value=sc)
+        vb, ob = g.const(sh), og.add_leaf("CONST", sh.shape, value=sh)
+        vals[ow] = wk
+        cv = g.add_node("CONV2D", [vx, vw], sh=1, sw=1, pad=1)
+        cvo = og.add_node("CONV2D", [ox, ow], {"sh": 1, "sw": 1, "pad": 1})
+        r = g.add_node("RELU", [g.add_node("ADD", [g.add_node("MUL", [cv, vs]), vb])])
+        ro = og.add_node("RELU", [og.add_node("ADD", [og.add_node("MUL", [cvo, os_]), ob])])
+        branches_g.append((r, vw, wk))
+        branches_o.append(ro)
+    mp = g.add_node("MAXPOOL2D", [vx], kh=3, kw=3, sh=1, sw=1, pad=1)
+    mpo = og.add_node("MAXPOOL2D", [ox], {"kh": 3, "kw": 3, "sh": 1, "sw": 1, "pad": 1})
+    inner = g.add_node("CONCAT", [branches_g[0][0], branches_g[1][0]], axis=3)
+    inner_o = og.add_node("CONCAT", branches_o, {"axis": 3})
+    cat = g.add_node("CONCAT", [inner, mp], axis=3)
+    cat_o = og.add_node("CONCAT", [inner_o, mpo], {"axis": 3})
+    out = g.add_node("NEG", [cat])
+    out_o = og.add_node("NEG", [cat_o])
+    g.plan_memory([out])
+    g.assign(vx, x)
+    for _, vw, wk in branches_g:
+        g.assign(vw, wk)
+    g.eval([out])
+    st = g.view_stats()
+    assert st["direct"] == 2 and st["copied"] == 1, st
+    ref = evaluate(og, vals)[out_o]
+    assert normwise(g.read(out), ref) <= 5e-5
+    g.destroy()

@@ -13,6 +13,7 @@ import glob
 import os
 import re
 
+import numpy as np
 import pytest
 
 from oracle.dump import compile_graph, graph_json, plan_json
@@ -205,3 +206,75 @@ def test_row_runs_compile_random():
         g, _, _, _ = host_graph(random_spec(seed), 0)
         n += _rowrun_check(g)[0]
     assert n >= 0
+
+
+# ---- R14 zero-copy CONCAT (f2; sub-block views, offset != 0 extension of P:303-310)
+def _concat_spec(nested=False, twice=False, keep_a=False, reshape_b=False):
+    from workloads.configs import Spec
+    s = Spec("concat")
+    x = s.var("x", [2, 3, 4], {"kind": "uniform", "tag": "x", "lo": -1.0, "hi": 1.0})
+    y = s.var("y", [2, 3, 2], {"kind": "uniform", "tag": "y", "lo": -1.0, "hi": 1.0})
+    a = s.op("RELU", x)
+    b = s.op("RESHAPE", s.op("NEG", s.op("RESHAPE", y, dims=[2, 6])), dims=[2, 3, 2]) if reshape_b else s.op("NEG", y)
+    c = s.op("CONCAT", a, b, a, axis=2) if twice else s.op("CONCAT", a, b, axis=2)
+    if nested:
+        d = s.op("EXP", y)
+        c = s.op("CONCAT", c, d, axis=2)
+    s.output(s.op("SIN", c))
+    if keep_a:
+        s.output(a)
+    return s.to_dict(), (x, y, a, b, c)
+
+
+def _plan(spec, flags=0):
+    og, oo = from_spec(spec)
+    return compile_graph(og, oo, flags, compute_values=False)
+
+
+def test_concat_views_oracle_pins():
+    """The view tuples are fixed by the concat layout: element (o, i) of input v
+    is element o * inner(root) + offset + i of the root (axis 2 of [2,3,*])."""
+    from oracle.validate import validate_plan
+    spec, (x, y, a, b, c) = _concat_spec()
+    cp = _plan(spec)
+    assert cp.plan.views == {a: (c, 6, 6, 0, 4), b: (c, 6, 6, 4, 2)}
+    assert cp.plan.block[a] == cp.plan.block[b] == cp.plan.block[c]
+    assert validate_plan(cp) == []
+    # the mapping reproduces numpy concatenation exactly
+    rng = np.random.default_rng(0)
+    va, vb = rng.standard_normal((2, 3, 4)), rng.standard_normal((2, 3, 2))
+    root = np.zeros(2 * 3 * 6)
+    for v, val in ((a, va), (b, vb)):
+        _, outer, inner_root, off, inner = cp.plan.views[v]
+        flat = val.reshape(outer, inner)
+        for o in range(outer):
+            root[o * inner_root + off: o * inner_root + off + inner] = flat[o]
+    assert np.array_equal(root.reshape(2, 3, 6), np.concatenate([va, vb], axis=2))
+    check_parity(spec, 0)
+    check_parity(spec, cg.PLAN_NO_FUSION)
+
+
+def test_concat_views_nested_and_refusals():
+    from oracle.validate import validate_plan
+    spec, (x, y, a, b, c) = _concat_spec(nested=True)
+    cp = _plan(spec)
+    inner_c, outer_c = [n["id"] for n in spec["nodes"] if n["op"] == "CONCAT"]
+    assert c == outer_c
+    d = [n["id"] for n in spec["nodes"] if n["op"] == "EXP"][0]
+    # the inner concat is a view of the outer one; its inputs map to the same root
+    assert cp.plan.views[inner_c] == (outer_c, 6, 8, 0, 6)
+    assert cp.plan.views[a] == (outer_c, 6, 8, 0, 4) and cp.plan.views[b] == (outer_c, 6, 8, 4, 2)
+    assert cp.plan.views[d] == (outer_c, 6, 8, 6, 2)
+    assert validate_plan(cp) == []
+    check_parity(spec, 0)
+    # refusals: an input used twice, a kept input, a RESHAPE producer, incremental plans
+    spec2, (_, _, a2, b2, _) = _concat_spec(twice=True)
+    assert a2 not in _plan(spec2).plan.views and b2 in _plan(spec2).plan.views
+    spec3, (_, _, a3, b3, _) = _concat_spec(keep_a=True)
+    assert a3 not in _plan(spec3).plan.views and b3 in _plan(spec3).plan.views
+    spec4, (_, _, a4, b4, _) = _concat_spec(reshape_b=True)
+    assert b4 not in _plan(spec4).plan.views and a4 in _plan(spec4).plan.views
+    assert _plan(spec, cg.PLAN_INCREMENTAL).plan.views == {}
+    for sp in (spec2, spec3, spec4):
+        check_parity(sp, 0)
+    check_parity(spec, cg.PLAN_INCREMENTAL)
