@@ -680,10 +680,7 @@ def _sec_c5():
     t0 = time.perf_counter()
     g, outs = cg.build_from_spec(spec, device=local, data_fn=_leaf)
     g.optimise(outs)
-    info = g.plan_memory(outs, cg.PLAN_FUSED_COLL if fused else 0)
-    if fused and world > 1:
-        from paper_1812_03770_b200.dist import connect_fused
-        connect_fused(g)
+    info = g.plan_memory(outs, 0)
     build_s = time.perf_counter() - t0
     ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
     l0 = g.launch_count()
@@ -696,7 +693,9 @@ def _sec_c5():
     r = {"metric": "images/s", "value": world * 256 / (ms * 1e-3), "unit": "images/s", "ms_per_eval": ms,
          "batch_per_gpu": 256, "scaling": "weak", "plan_peak_bytes": peak, "unshared_bytes": unshared,
          "peak_vs_unshared": peak / unshared, "n_groups": info["n_groups"], "n_blocks": info["n_blocks"],
-         "build_s": build_s, "clocks": clk, "launches_per_eval": launches, "algorithmic_flops_per_eval": flops}
+         "build_s": build_s, "clocks": clk, "launches_per_eval": launches, "algorithmic_flops_per_eval": flops,
+         "n_fused_epilogues": info["n_fused"],
+         "zero_copy_concat_slices": g.view_stats()}  # R14: direct = stored by the conv epilogue
     if tf32:
         ach = 3 * flops / (ms * 1e-3) / 1e12
         r["roofline"] = {"bound": "tensor", "scope": "whole evaluation (convs dominate)", "achieved": ach,

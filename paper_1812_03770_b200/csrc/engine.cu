@@ -1859,6 +1859,10 @@ extern "C" int64_t cgx_codegen_check(cg_graph* g, int num_sms, char* log, size_t
   for (const Group& G : g->hg.groups) {
     if (G.kind != G_EW && G.kind != G_RED) continue;
     KernelSpec ks = gen_group(g->hg, G, num_sms);
+    if (const char* kd = getenv("CG_DUMP_KERNELS")) {  // inspection on a CPU-only box
+      FILE* f = fopen((std::string(kd) + "/" + ks.name + ".cu").c_str(), "w");
+      if (f) { fputs(ks.source.c_str(), f); fclose(f); }
+    }
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, ks.source.c_str(), "check.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return CG_E_NVRTC;
     const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-default-device", "--std=c++17"};
