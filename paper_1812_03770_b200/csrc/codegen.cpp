@@ -283,6 +283,83 @@ KernelSpec gen_ew(const HostGraph& hg, const Group& G, int num_sms) {
         }
       }
     }
+    // software-pipelined variant (1 row per iteration, CG_EW_PREFETCH=1): the next
+    // row's loads are issued before this row's arithmetic.  Measured on C2 under
+    // sw_power_cap (tools/ew_prefetch_ab.sh, 3 interleaved pairs): 5,700 GB/s vs
+    // 5,930 without -- occupancy already hides the latency and the extra live
+    // registers cost more -- so it is off by default.
+    static const bool prefetch = getenv("CG_EW_PREFETCH") && atoi(getenv("CG_EW_PREFETCH")) == 1;
+    if (prefetch && U_row == 1) {
+      auto is_rowdep = [&](size_t q) { return !(so[q] == 0 && (si[q] == 0 || hoist)); };
+      b << "  const long long step = (long long)gridDim.x * " << TY << ";\n";
+      b << "  long long rb = (long long)blockIdx.x * " << TY << " + ty;\n";
+      for (int j = 0; j < KC; ++j)
+        for (size_t q = 0; q < nin; ++q) {
+          if (!is_rowdep(q)) continue;
+          if (si[q] != 0 && V == 4) b << "  float4 p" << q << "_" << j << " = make_float4(0.f,0.f,0.f,0.f);\n";
+          else b << "  float p" << q << "_" << j << " = 0.f;\n";
+        }
+      auto emit_loads = [&](const std::string& rv, const std::string& ind) {
+        for (int j = 0; j < KC; ++j) {
+          b << ind << "{ const int c = tx + " << j * TX << "; if (c < " << WV << ") {\n";
+          for (size_t q = 0; q < nin; ++q) {
+            if (!is_rowdep(q)) continue;
+            if (si[q] == 0) b << ind << " p" << q << "_" << j << " = in" << q << "[" << rv << " * " << so[q] << "LL];\n";
+            else if (V == 4) b << ind << " p" << q << "_" << j << " = cg_ld4(in" << q << " + " << rv << " * " << so[q] << "LL + c * 4);\n";
+            else b << ind << " p" << q << "_" << j << " = in" << q << "[" << rv << " * " << so[q] << "LL + c * " << si[q] << "LL];\n";
+          }
+          b << ind << "} }\n";
+        }
+      };
+      b << "  if (rb < " << R << "LL) {\n";
+      emit_loads("rb", "   ");
+      b << "  }\n";
+      b << "  for (; rb < " << R << "LL; rb += step) {\n";
+      b << "   const long long rn = rb + step;\n";
+      for (int j = 0; j < KC; ++j) {
+        b << "   {\n    const int c = tx + " << j * TX << ";\n";
+        b << "    if (c < " << WV << ") {\n";
+        for (size_t q = 0; q < nin; ++q) {
+          if (!is_rowdep(q)) continue;
+          if (si[q] != 0 && V == 4) b << "     const float4 f" << q << "_0 = p" << q << "_" << j << ";\n";
+          else b << "     const float s" << q << "_0 = p" << q << "_" << j << ";\n";
+        }
+        b << "     if (rn < " << R << "LL) {\n";
+        for (size_t q = 0; q < nin; ++q) {
+          if (!is_rowdep(q)) continue;
+          if (si[q] == 0) b << "      p" << q << "_" << j << " = in" << q << "[rn * " << so[q] << "LL];\n";
+          else if (V == 4) b << "      p" << q << "_" << j << " = cg_ld4(in" << q << " + rn * " << so[q] << "LL + c * 4);\n";
+          else b << "      p" << q << "_" << j << " = in" << q << "[rn * " << so[q] << "LL + c * " << si[q] << "LL];\n";
+        }
+        b << "     }\n     {\n";
+        for (int l = 0; l < V; ++l)
+          for (size_t q = 0; q < nin; ++q) {
+            b << "      const float x" << q << "_" << l << " = ";
+            if (so[q] == 0 && si[q] == 0) b << "h" << q;
+            else if (so[q] == 0 && hoist) b << (V == 4 ? "cg_lane(h" : "(h") << q << "_" << j << (V == 4 ? ", " + std::to_string(l) + ")" : ".x)");
+            else if (si[q] == 0) b << "s" << q << "_0";
+            else if (V == 4) b << "cg_lane(f" << q << "_0, " << l << ")";
+            else b << "s" << q << "_0";
+            b << ";\n";
+          }
+        b << me.emit(V);
+        for (size_t jo = 0; jo < nout; ++jo) {
+          int m = G.materialised[jo];
+          if (V == 4)
+            b << "      cg_st4(out" << jo << " + rb * " << W << "LL + c * 4, v" << m << "_0, v" << m << "_1, v" << m << "_2, v" << m
+              << "_3);\n";
+          else
+            b << "      out" << jo << "[rb * " << W << "LL + c] = v" << m << "_0;\n";
+        }
+        b << "     }\n    }\n   }\n";
+      }
+      b << "  }\n}\n";
+      int64_t work = (R + TY - 1) / TY;
+      ks.work_blocks = work;
+      ks.grid[0] = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(work, (int64_t)num_sms * 8));
+      ks.source = finish("ew", b.str(), &ks.name);
+      return ks;
+    }
     b << "  const long long step = (long long)gridDim.x * " << TY * U_row << ";\n";
     b << "  for (long long rb = (long long)blockIdx.x * " << TY * U_row << " + ty; rb < " << R << "LL; rb += step) {\n";
     for (int j = 0; j < KC; ++j) {
