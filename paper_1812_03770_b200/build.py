@@ -33,7 +33,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(CSRC, "build", src + ".o")
         os.makedirs(os.path.dirname(obj), exist_ok=True)
-        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", "-diag-suppress=177", "-Xcompiler", "-fPIC,-O3", *ARCH,
+        extra = os.environ.get("CG_EXTRA_NVCC_FLAGS", "").split()  # measurement builds (e.g. -DCG_SB_TIMING)
+        cmd = [NVCC, "-std=c++17", "-O3", "-lineinfo", "-diag-suppress=177", *extra, "-Xcompiler", "-fPIC,-O3", *ARCH,
                "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)

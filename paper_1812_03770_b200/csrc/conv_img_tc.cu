@@ -34,6 +34,7 @@
 #include <cstdlib>
 
 #include "conv_img_tc.h"
+#include "dot_tc.h"
 
 namespace cg {
 
@@ -1122,7 +1123,330 @@ CiKind kind_of(const ConvGeom& g, bool flip) {
   return CI_NONE;
 }
 
+// ---------------------------------------------------------------- stem: few-channel, strided, wide images
+// The InceptionV3 stem conv (299x299x3 -> 149x149x32, 3x3, stride 2, VALID; C5) as
+// an implicit GEMM over bands of RB output rows of one image: the band's input rows
+// are ONE contiguous span of x (VALID: no padding), staged by a single 16-byte-
+// aligned TMA bulk copy (the span's start is shifted into the buffer; the copy may
+// read up to 12 bytes past the tensor, inside its 256-byte-aligned allocation).
+// Builders form each 128-pixel x 32-k slab (K = KS*KS*CIN <= 32 per k-block,
+// k = (kh, kw, c)) from shared memory into TMEM (hi / lo), one warp issues 12
+// tf32 MMAs (M = 128, N = COUT) per slab, the epilogue applies the fused
+// elementwise chain (the BN scale / shift + ReLU of the DOT/CONV epilogue fusion,
+// per-column or scalar operands) and stores 32 channels per pixel with row stride
+// ldc.  Replaces the element-gather path of the generic conv (Ci = 3 is not a TMA
+// im2col box): 1.43 ms at batch 256 in round 1.
+constexpr int SB_THREADS = 576;  // 0-7 builders (2 groups), 8-15 epilogue (2 per lane quadrant), 16 producer, 17 MMA
+constexpr int SB_L = 6;
+constexpr int SB_NBUF = 4;  // band buffers: a band's copy latency exceeds its compute (measured with 2: 733 us)
+
+template <int CIN, int KS, int S, int IH, int IW, int OH, int OW, int COUT, int RB>
+struct SbGeo {
+  static constexpr int K = CIN * KS * KS;
+  static constexpr int NKB = (K + 31) / 32;
+  static constexpr int NR = (RB - 1) * S + KS;                 // input rows of a full band
+  static constexpr int ROWF = IW * CIN;
+  static constexpr int BUF = (NR * ROWF + 8 + 31) / 32 * 32;   // + shift slack + 16-byte tail
+  static constexpr int NB = (OH + RB - 1) / RB;                // bands per image
+  static constexpr int TMAX = (RB * OW + 127) / 128;           // tiles of a full band
+  static constexpr int B_TILE = COUT * 128;                    // bytes of one hi (or lo) K-major tile
+  static constexpr int B_BYTES = NKB * 2 * B_TILE;
+  static constexpr int ACC = COUT;                             // TMEM columns per accumulator
+  static constexpr int ACOL = 2 * COUT;
+  static_assert(COUT % 16 == 0 && COUT <= 64 && ACOL + SB_L * 64 <= 512, "TMEM");
+};
+
+template <int CIN, int KS, int S, int IH, int IW, int OH, int OW, int COUT, int RB>
+__global__ void __launch_bounds__(SB_THREADS, 1)
+    conv_band_tc_kernel(const float* __restrict__ x, const float* __restrict__ w, float* __restrict__ out, int ldc,
+                        int nimgs, const __grid_constant__ EpiProg epi, int dbg) {
+  // dbg (measurement only, CG_SB_DEBUG): 1 = skip the output stores, 2 = skip the chain
+  using Geo = SbGeo<CIN, KS, S, IH, IW, OH, OW, COUT, RB>;
+  constexpr int K = Geo::K, NKB = Geo::NKB, ROWF = Geo::ROWF, BUF = Geo::BUF, NB = Geo::NB;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  float* bufs = reinterpret_cast<float*>(smem + Geo::B_BYTES);
+  float* eops = bufs + SB_NBUF * BUF;                           // per-column chain operands [kEpiMax][COUT]
+  float* ostage = eops + kEpiMax * COUT;                        // [4 quadrants][32 px][COUT + 4]: coalesced stores
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + 4 * 32 * (COUT + 4));
+  const uint32_t bar0 = smem_u32(bars);
+  constexpr int NBF = SB_NBUF;
+  auto full = [&](int b) { return bar0 + 8u * b; };
+  auto freeb = [&](int b) { return bar0 + 8u * (NBF + b); };
+  auto conv = [&](int l) { return bar0 + 8u * (2 * NBF + l); };
+  auto lofree = [&](int l) { return bar0 + 8u * (2 * NBF + SB_L + l); };
+  auto tfull = [&](int b) { return bar0 + 8u * (2 * NBF + 2 * SB_L + b); };
+  auto tempty = [&](int b) { return bar0 + 8u * (2 * NBF + 2 * SB_L + 2 + b); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NBF + 2 * SB_L + 4);
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
+  const int units = nimgs * NB;
+#ifdef CG_SB_TIMING  // per-role cycle accounting of CTA 0 (measurement builds only)
+  long long tw = 0, tx1 = 0, tx2 = 0, t0r = 0;
+#define SB_T(acc, call)                 \
+  do {                                  \
+    const long long t_ = clock64();     \
+    call;                               \
+    acc += clock64() - t_;              \
+  } while (0)
+#else
+#define SB_T(acc, call) \
+  do {                  \
+    call;               \
+  } while (0)
+#endif
+  auto band_rows = [](int b) { return min(RB, OH - b * RB); };
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NBF; ++b) {
+      mbar_init(full(b), 1);
+      mbar_init(freeb(b), 8);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 8);
+    }
+    for (int l = 0; l < SB_L; ++l) {
+      mbar_init(conv(l), 4);
+      mbar_init(lofree(l), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // B = weights [KS][KS][CIN][COUT] as K-major SWIZZLE_128B tiles (hi, lo) per k-block
+  for (int e = threadIdx.x; e < NKB * COUT * 32; e += blockDim.x) {
+    const int kb = e / (COUT * 32), rem = e % (COUT * 32), n = rem / 32, kl = rem % 32, k = kb * 32 + kl;
+    const float v = k < K ? __ldg(w + (size_t)k * COUT + n) : 0.f;  // row k = (kh, kw, c) of HWIO
+    const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    const int off = n * 128 + (((kl >> 2) ^ (n & 7)) << 4) + (kl & 3) * 4;
+    *reinterpret_cast<float*>(smem + kb * 2 * Geo::B_TILE + off) = hi;
+    *reinterpret_cast<float*>(smem + kb * 2 * Geo::B_TILE + Geo::B_TILE + off) = __fsub_rn(v, hi);
+  }
+  for (int e = threadIdx.x; e < epi.n * COUT; e += blockDim.x) {
+    const int i = e / COUT, c = e % COUT;
+    eops[e] = epi.op[i] == EPI_RELU ? 0.f : (epi.scalar[i] ? __ldg(epi.x[i]) : __ldg(epi.x[i] + c));
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 17) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+#ifdef CG_SB_TIMING
+  t0r = clock64();
+#endif
+  // the band's input span and its shift inside the staging buffer (16-byte-aligned copy)
+  auto span = [&](int u, long long* a0, int* shift, int* bytes) {
+    const int n = u / NB, b = u % NB, rows = band_rows(b);
+    const long long start = ((long long)n * IH + (long long)b * RB * S) * ROWF;
+    const int cnt = ((rows - 1) * S + KS) * ROWF;
+    *a0 = start & ~3LL;
+    *shift = (int)(start - *a0);
+    *bytes = ((cnt + *shift) * 4 + 15) / 16 * 16;
+  };
+
+  if (warp < 8) {
+    // ---------------- builders
+    const int grp = warp / 4, wq = warp % 4, rr = wq * 32 + lane;
+    int it = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int bsel = j % NBF;
+      long long a0;
+      int shift, bytes;
+      span(u, &a0, &shift, &bytes);
+      const int npx = band_rows(u % NB) * OW, T = (npx + 127) / 128;
+      SB_T(tw, mbar_wait(full(bsel), (j / NBF) & 1));
+      const float* img = bufs + bsel * BUF + shift;
+      for (int t = 0; t < T; ++t, it += NKB) {
+        const int q = t * 128 + rr;
+        const int qq = q < npx ? q : 0;
+        const int ol = qq / OW, ow = qq - ol * OW;
+        const float* base = img + (ol * S) * ROWF + (ow * S) * CIN;
+#pragma unroll
+        for (int kb = 0; kb < NKB; ++kb) {
+          const int step = it + kb;
+          if ((step & 1) != grp) continue;
+          const int l = step % SB_L;
+          float v[32];
+#pragma unroll
+          for (int kl = 0; kl < 32; ++kl) {
+            const int k = kb * 32 + kl;
+            if (k < K) {
+              const int c = k % CIN, tap = k / CIN, kh = tap / KS, kw = tap % KS;
+              v[kl] = base[kh * ROWF + kw * CIN + c];
+            } else {
+              v[kl] = 0.f;
+            }
+          }
+          SB_T(tx1, mbar_wait(lofree(l), ((step / SB_L) & 1) ^ 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ta = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(Geo::ACOL + l * 64);
+          uint32_t hv[32], lv[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const uint32_t h = __float_as_uint(v[i]) & 0xFFFFE000u;
+            hv[i] = h;
+            lv[i] = __float_as_uint(__fsub_rn(v[i], __uint_as_float(h)));
+          }
+          tmem_st32(ta, hv);
+          tmem_st32(ta + 32, lv);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(conv(l));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(freeb(bsel));
+    }
+  } else if (warp < 16) {
+    // ---------------- epilogue: per tile, sum of the k-blocks' fresh accumulators
+    // (round to nearest), the fused chain, 16-byte stores.  Two warps per TMEM lane
+    // quadrant, each owning half of the output channels.
+    constexpr int CH = COUT / 2;
+    const int wq = warp % 4, half = (warp - 8) / 4, rr = wq * 32 + lane, c0 = half * CH;
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int n = u / NB, b = u % NB, npx = band_rows(b) * OW, T = (npx + 127) / 128;
+      for (int t = 0; t < T; ++t) {
+        float sum[CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) sum[i] = 0.f;
+        for (int kb = 0; kb < NKB; ++kb, ++it) {
+          const int bb = it & 1;
+          SB_T(tw, mbar_wait(tfull(bb), (it >> 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int cc = 0; cc < CH; cc += 16) {
+            float vv[16];
+            SB_T(tx1, tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(bb * Geo::ACC + c0 + cc), vv));
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sum[cc + i] = NKB == 1 ? vv[i] : __fadd_rn(sum[cc + i], vv[i]);
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty(bb));
+        }
+        // the chain, op by op: the op and operand order are uniform, so each op is one
+        // branch and a straight unrolled loop (a per-value switch compiled to a BRX jump
+        // table per element and made the chain the kernel's bottleneck: 1.16 ms vs 0.17)
+        for (int e = 0; e < ((dbg & 2) ? 0 : epi.n); ++e) epi_apply<CH>(sum, epi.op[e], epi.swap[e], eops + e * COUT + c0);
+        // the quadrant's 32 pixels x COUT channels are one contiguous 4 KB run of the
+        // output (row pitch ldc == COUT): the warp pair assembles it in shared memory and
+        // writes it with 512-byte coalesced stores (per-lane 64-byte halves of lines
+        // written by two warps at different times measured 1.5x slower)
+        const long long pix0 = ((long long)n * OH + (long long)b * RB) * OW + t * 128 + wq * 32;
+        const int nval = min(32, npx - (t * 128 + wq * 32));
+        if (dbg & 1) {
+        } else if (ldc == COUT && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+          float* st = ostage + wq * 32 * (COUT + 4);
+#pragma unroll
+          for (int i = 0; i < CH; i += 4)
+            *reinterpret_cast<float4*>(st + lane * (COUT + 4) + c0 + i) = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
+          SB_T(tx2, asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory"));
+          constexpr int Q4 = COUT / 4;  // float4 per pixel
+#pragma unroll
+          for (int k = 0; k < 32 * Q4 / 64; ++k) {
+            const int c = half * (32 * Q4 / 2) + k * 32 + lane, px = c / Q4, part = c % Q4;
+            if (px < nval)
+              *reinterpret_cast<float4*>(out + (pix0 + px) * COUT + part * 4) =
+                  *reinterpret_cast<const float4*>(st + px * (COUT + 4) + part * 4);
+          }
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+        } else if (lane < nval) {
+          float* o = out + (pix0 + lane) * ldc + c0;
+#pragma unroll
+          for (int i = 0; i < CH; ++i) o[i] = sum[i];
+        }
+      }
+    }
+  } else if (warp == 16) {
+    // ---------------- producer: one bulk copy per band (double-buffered)
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int bsel = j % NBF;
+      long long a0;
+      int shift, bytes;
+      span(u, &a0, &shift, &bytes);
+      SB_T(tw, mbar_wait(freeb(bsel), ((j / NBF) & 1) ^ 1));
+      if (lane == 0) {
+        mbar_expect_tx(full(bsel), (uint32_t)bytes);
+        bulk_g2s(smem_u32(bufs + bsel * BUF), x + a0, (uint32_t)bytes, full(bsel));
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- warp 17: MMA issuer (N = COUT, M = 128)
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(COUT >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int npx = band_rows(u % NB) * OW, T = (npx + 127) / 128;
+      for (int t = 0; t < T; ++t)
+        for (int kb = 0; kb < NKB; ++kb, ++it) {
+          const int l = it % SB_L, bb = it & 1;
+          SB_T(tw, mbar_wait_warp(tempty(bb), ((it >> 1) & 1) ^ 1));
+          SB_T(tx1, mbar_wait_warp(conv(l), (it / SB_L) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t d = tm + (uint32_t)(bb * Geo::ACC);
+          const uint32_t ahi = tm + (uint32_t)(Geo::ACOL + l * 64), alo = ahi + 32;
+          const uint32_t bt = sbase + (uint32_t)(kb * 2 * Geo::B_TILE);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t dhi = sdesc(bt + kk * 32, 16, 1024, 2), dlo = sdesc(bt + Geo::B_TILE + kk * 32, 16, 1024, 2);
+            mma_tf32_e<1>(d, alo + kk * 8, dhi, idesc, kk > 0 ? 1u : 0u);
+            mma_tf32_e<1>(d, ahi + kk * 8, dlo, idesc, 1u);
+            mma_tf32_e<1>(d, ahi + kk * 8, dhi, idesc, 1u);
+          }
+          mma_commit_e<1>(lofree(l));
+          mma_commit_e<1>(tfull(bb));
+        }
+    }
+  }
+#ifdef CG_SB_TIMING
+  if (blockIdx.x == 0 && lane == 0)
+    printf("band warp %2d: busy %8lld wait %8lld x1 %8lld x2 %8lld\n", warp, clock64() - t0r, tw, tx1, tx2);
+#endif
+#undef SB_T
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 17) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <int CIN, int KS, int S, int IH, int IW, int OH, int OW, int COUT, int RB>
+cudaError_t launch_band(const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi, int num_sms,
+                        cudaStream_t s) {
+  using Geo = SbGeo<CIN, KS, S, IH, IW, OH, OW, COUT, RB>;
+  if (reinterpret_cast<uintptr_t>(x) & 15) return cudaErrorMisalignedAddress;
+  const size_t smem = 1024 + Geo::B_BYTES + SB_NBUF * (size_t)Geo::BUF * 4 + kEpiMax * COUT * 4 + 4 * 32 * (COUT + 4) * 4 + 512;
+  auto kern = conv_band_tc_kernel<CIN, KS, S, IH, IW, OH, OW, COUT, RB>;
+  cudaError_t e = smem_attr((const void*)kern, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int units = n * Geo::NB;
+  static const int dbg = getenv("CG_SB_DEBUG") ? atoi(getenv("CG_SB_DEBUG")) : 0;
+  kern<<<std::min(units, num_sms), SB_THREADS, smem, s>>>(x, w, out, ldc, n, epi, dbg);
+  return cudaGetLastError();
+}
+
 }  // namespace
+
+bool conv_band_supported(int n, int h, int w, int ci, int kh, int kw, int co, int ho, int wo, int sh, int sw, int pt,
+                         int pl) {
+  (void)n;
+  return !getenv("CG_NO_CONV_BAND") && h == 299 && w == 299 && ci == 3 && kh == 3 && kw == 3 && co == 32 && ho == 149 &&
+         wo == 149 && sh == 2 && sw == 2 && pt == 0 && pl == 0;
+}
+
+cudaError_t launch_conv_band(const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi, int num_sms,
+                             cudaStream_t s) {
+  // the InceptionV3 stem: 299x299x3 -> 149x149x32, 3x3 stride 2 VALID; bands of 6 output rows (894 px = 7 tiles)
+  return launch_band<3, 3, 2, 299, 299, 149, 149, 32, 6>(x, w, out, ldc, n, epi, num_sms, s);
+}
 
 bool conv_img_tc_bwdk_supported(const ConvGeom& g) {
   return kind_of(g, false) != CI_NONE && !getenv("CG_NO_CONV_IMG_TC");

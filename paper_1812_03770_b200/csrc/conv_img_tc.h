@@ -24,4 +24,13 @@ size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms);
 cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g, int num_sms,
                                     cudaStream_t s);
 
+// The InceptionV3 stem conv (Ci = 3, stride 2) over bands of output rows, with the
+// DOT/CONV epilogue's fused elementwise chain (conv_band_tc_kernel); x must be
+// 16-byte aligned and may be over-read by up to 12 bytes inside its allocation.
+struct EpiProg;
+bool conv_band_supported(int n, int h, int w, int ci, int kh, int kw, int co, int ho, int wo, int sh, int sw, int pt,
+                         int pl);
+cudaError_t launch_conv_band(const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi, int num_sms,
+                             cudaStream_t s);
+
 }  // namespace cg

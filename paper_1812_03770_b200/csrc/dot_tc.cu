@@ -34,6 +34,7 @@
 #include <mutex>
 
 #include "dot_tc.h"
+#include "conv_img_tc.h"
 #include "kernels.h"
 
 #include <algorithm>
@@ -462,25 +463,12 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (epi.n) {  // fused elementwise epilogue, IEEE-rounded per op like the unfused kernel
           const float* es = reinterpret_cast<const float*>(smem + T::EPI_BASE) + c0;
-          for (int e = 0; e < epi.n; ++e) {
-            const int op = epi.op[e], sw = epi.swap[e];
+          float vv[16];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              float v = __uint_as_float(r[q]);
-              const float xv = es[e * BN + q];
-              const float a = sw ? xv : v, bb = sw ? v : xv;
-              switch (op) {
-                case EPI_ADD: v = __fadd_rn(a, bb); break;
-                case EPI_SUB: v = __fsub_rn(a, bb); break;
-                case EPI_MUL: v = __fmul_rn(a, bb); break;
-                case EPI_DIV: v = __fdiv_rn(a, bb); break;
-                case EPI_RELU: v = v > 0.f ? v : 0.f; break;
-                case EPI_MAX: asm("max.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(bb)); break;
-                case EPI_MIN: asm("min.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(bb)); break;
-              }
-              r[q] = __float_as_uint(v);
-            }
-          }
+          for (int q = 0; q < 16; ++q) vv[q] = __uint_as_float(r[q]);
+          for (int e = 0; e < epi.n; ++e) epi_apply<16>(vv, epi.op[e], epi.swap[e], es + e * BN);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) r[q] = __float_as_uint(vv[q]);
         }
         if (row < M && n0 + c0 < N) {
           float* crow = Cz + (size_t)row * ldc;
@@ -781,6 +769,7 @@ cudaError_t launch_tc_cg(const DotTcPlan& p, float* out, cudaStream_t s) {
 }
 
 cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
+  if (p.band) return launch_conv_band(p.conv.x, p.band_w, p.C, p.ldc > 0 ? p.ldc : p.N, p.band_n, p.epi, p.num_sms, s);
   float* out = p.splits > 1 ? p.ws : p.C;
   cudaError_t e0;
   switch (p.bn) {
@@ -820,6 +809,12 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   }
   p->bn = pick_bn(p->M, co, num_sms);
   p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms, true);
+  if (conv_band_supported(n, h, wd, ci, kh, kw, co, ho, wo, sh, sw, pt, pl)) {  // the stem: row bands, no split-K
+    p->band = 1;
+    p->splits = 1;
+    p->band_w = w;
+    p->band_n = n;
+  }
   // B = weights as a [K, Co] row-major matrix (N-major), like DOT with tb = 0
   return make_map(reinterpret_cast<CUtensorMap*>(p->mapB), w, p->K, co, 32, true) ? 0 : -2;
 }

@@ -300,6 +300,9 @@ TC_CONV_CASES = [((2, 35, 35, 64), (3, 3, 64, 96), 1, 1), ((2, 35, 35, 32), (3, 
                  ((2, 17, 17, 32), (1, 7, 32, 64), 1, 1), ((2, 17, 17, 32), (7, 1, 32, 64), 1, 1),
                  ((2, 12, 13, 96), (5, 5, 96, 48), 1, 1), ((9, 35, 35, 64), (3, 3, 64, 96), 1, 1),
                  ((4, 37, 33, 32), (3, 3, 32, 32), 2, 0),
+                 # the InceptionV3 stem (Ci = 3, stride 2, VALID): the row-band kernel; 5 images
+                 # cover full bands, the 5-row last band and a unit split across CTAs
+                 ((5, 299, 299, 3), (3, 3, 3, 32), 2, 0),
                  # Ci % 16 == 0: pairs of 16-channel im2col boxes; K % 32 == 16 exercises the zero half-slab
                  ((2, 12, 12, 16), (3, 3, 16, 32), 1, 1), ((2, 17, 17, 48), (5, 5, 48, 64), 1, 1),
                  ((2, 15, 15, 80), (3, 3, 80, 192), 1, 0), ((3, 16, 15, 48), (3, 3, 48, 64), 2, 1)]
