@@ -12,12 +12,13 @@
 // split once per CTA) from shared memory.  3xTF32: hi.hi + hi.lo + lo.hi as in
 // dot_tc.cu.
 //
-// Accuracy: the tensor core's fp32 accumulation truncates, so a 400-deep chain
-// in one accumulator loses ~K/8 ulps (measured 1.6e-6 .. 2.5e-5 normwise on the
-// DOT kernel).  Here each 32-deep k-block goes to a fresh TMEM accumulator and
-// the epilogue warps add it into a register sum with round-to-nearest, so the
-// truncation applies to 32-deep partials only (fp32-GEMM accuracy).  N <= 16
-// makes that cheap: 16 registers per thread, one 8 KiB TMEM read per k-block.
+// Accuracy: the tensor core's fp32 accumulation truncates (a K-deep chain loses
+// ~K/8 ulps of the partial sums, measured 1.6e-6 .. 2.5e-5 normwise on the DOT
+// kernel).  The first version gave each 32-deep k-block a fresh accumulator and
+// summed them with round-to-nearest in registers; that made the MMA wait for an
+// epilogue drain every k-block, and the K <= 150 of these convs is well inside the
+// tolerance the generic implicit GEMM already meets with whole-K chains, so a
+// tile's k-blocks now chain in one accumulator (integer-exact tests unaffected).
 //
 // Work: persistent CTAs over units of G whole images (G*P pixels = T tiles of
 // 128).  Warps: 0-3 image loaders (global NHWC -> planar smem, double-buffered),
@@ -299,20 +300,19 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int n0 = u * G, nimg = min(G, nimgs - n0);
       for (int t = 0; t < T; ++t) {
+        // the tile's NKB k-blocks accumulate in one TMEM accumulator (as the generic
+        // implicit GEMM); a fresh accumulator per k-block made the MMA wait for a drain
+        // every k-block
         float sum[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) sum[i] = 0.f;
-        for (int kb = 0; kb < NKB; ++kb, ++it) {
+        {
           const int b = it & 1;
           mbar_wait(tfull(b), (it >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          float v[16];
-          tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * 16), v);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) sum[i] = __fadd_rn(sum[i], v[i]);
+          tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * 16), sum);
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty(b));
+          ++it;
         }
         const int q = t * 128 + rr;
         if (q < nimg * P) {
@@ -346,28 +346,29 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     // instruction descriptor: D f32, A / B tf32, A (TMEM) and B K-major, N = 16, M = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-    int it = 0;
+    int it = 0, tile = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x)
-      for (int t = 0; t < T; ++t)
+      for (int t = 0; t < T; ++t, ++tile) {
+        const int b = tile & 1;
+        mbar_wait_warp(tempty(b), ((tile >> 1) & 1) ^ 1);  // the epilogue has read this accumulator
+        const uint32_t d = tm + (uint32_t)(b * 16);
         for (int kb = 0; kb < NKB; ++kb, ++it) {
-          const int l = it % CI_L, b = it & 1;
-          mbar_wait_warp(tempty(b), ((it >> 1) & 1) ^ 1);  // the epilogue has read this accumulator
+          const int l = it % CI_L;
           mbar_wait_warp(conv(l), (it / CI_L) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t d = tm + (uint32_t)(b * 16);
           const uint32_t ahi = tm + (uint32_t)(CI_ACOL + l * 64), alo = ahi + 32;
           const uint32_t bt = sbase + (uint32_t)(kb * 4096);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t dhi = sdesc(bt + kk * 32, 16, 1024, 2), dlo = sdesc(bt + 2048 + kk * 32, 16, 1024, 2);
-            // small terms first, then the leading hi.hi product; a fresh accumulator per k-block
-            mma_tf32_e<1>(d, alo + kk * 8, dhi, idesc, kk > 0 ? 1u : 0u);
+            mma_tf32_e<1>(d, alo + kk * 8, dhi, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
             mma_tf32_e<1>(d, ahi + kk * 8, dlo, idesc, 1u);
             mma_tf32_e<1>(d, ahi + kk * 8, dhi, idesc, 1u);
           }
           mma_commit_e<1>(lofree(l));
-          mma_commit_e<1>(tfull(b));
         }
+        mma_commit_e<1>(tfull(b));
+      }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1433,6 +1434,364 @@ cudaError_t launch_band(const float* x, const float* w, float* out, int ldc, int
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- 3x3 stride-1 convs on wide images (C5 stem)
+// 149x149x32 -> 147x147x32 VALID and 147x147x32 -> 147x147x64 SAME (InceptionV3
+// layers 2 and 3).  The generic implicit GEMM re-reads every input pixel 9 times
+// through TMA im2col (1.48 / 0.87 ms at batch 256, A-side bound).  Here each input
+// ROW is staged once, by a 4-D tensor-map TMA whose box is CIN + 4 channels wide
+// (the out-of-bounds fill pads every pixel to 36 floats: conflict-free 16-byte
+// shared loads with pixels on lanes), into a ring of NS row slots; tiles of 128
+// consecutive output pixels of one image (<= 2 output rows, <= 4 input rows) are
+// built from the ring (tap (kh, kw) of 32 channels = one k-block = 8 LDS.128 per
+// pixel), 12 tf32 MMAs (M = 128, N = NH) per k-block; COUT > NH is split over
+// CTAs (NH output channels each).  Rows leave the ring when every builder warp has
+// moved past them.  The epilogue (fresh accumulator per k-block summed with
+// round-to-nearest, the fused chain, coalesced stores) is the band kernel's.
+constexpr int RW_THREADS = 576;  // 0-7 builders, 8-15 epilogue, 16 producer, 17 MMA
+constexpr int RW_L = 6;           // A slots
+constexpr int RW_NS = 6;          // row slots
+constexpr int RW_QU = 4;          // units per image (tile ranges): balance over 148 CTAs
+
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT, int NH>
+struct RwGeo {
+  static constexpr int CPAD = CIN + 4;
+  // a tensor TMA destination must be 128-byte aligned: input column iw sits at staged
+  // column iw + PLS with PLS * CPAD * 4 % 128 == 0 (PLS >= PL; the columns before it
+  // stay zero and serve as the left padding), and every slot starts on 128 bytes
+  static constexpr int PLS = PL == 0 ? 0 : (PL * CPAD * 4 % 128 == 0 ? PL : (128 / 16) * ((PL + 7) / 8));
+  static constexpr int PR = OW + KS - 1 - PL - IW > 0 ? OW + KS - 1 - PL - IW : 0;
+  static constexpr int WPS = IW + PLS + PR;
+  static constexpr int ROWF = (WPS * CPAD + 31) / 32 * 32;
+  static_assert(PLS >= PL && (PLS * CPAD * 4) % 128 == 0, "TMA destination alignment");
+  static constexpr int NKB = KS * KS * CIN / 32;
+  static constexpr int CB = CIN / 32;                 // k-blocks per tap
+  static constexpr int P = OH * OW;
+  static constexpr int TPI = (P + 127) / 128;         // tiles per image
+  static constexpr int TPQ = (TPI + RW_QU - 1) / RW_QU;
+  static constexpr int HALVES = COUT / NH;
+  static constexpr int B_TILE = NH * 128;
+  static constexpr int B_BYTES = NKB * 2 * B_TILE;
+  static constexpr int ACC = NH;
+  static constexpr int ACOL = 2 * NH;
+  static_assert(CIN % 32 == 0 && COUT % NH == 0 && NH % 16 == 0 && ACOL + RW_L * 64 <= 512, "geometry");
+  static_assert(OW >= 64, "a tile spans at most two output rows");
+};
+
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT, int NH>
+__global__ void __launch_bounds__(RW_THREADS, 1)
+    conv_rows_tc_kernel(const float* __restrict__ w, float* __restrict__ out, int ldc, int nimgs,
+                        const __grid_constant__ CUtensorMap xmap, const __grid_constant__ EpiProg epi) {
+  using Geo = RwGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT, NH>;
+  constexpr int NKB = Geo::NKB, ROWF = Geo::ROWF, CPAD = Geo::CPAD, P = Geo::P, TPI = Geo::TPI, TPQ = Geo::TPQ;
+  constexpr int HALVES = Geo::HALVES, NS = RW_NS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sbase = smem_u32(smem);
+  float* rows = reinterpret_cast<float*>(smem + Geo::B_BYTES);
+  float* eops = rows + NS * ROWF;
+  float* ostage = eops + kEpiMax * NH;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + 4 * 32 * (NH + 4));
+  const uint32_t bar0 = smem_u32(bars);
+  auto rfull = [&](int b) { return bar0 + 8u * b; };
+  auto rfree = [&](int b) { return bar0 + 8u * (NS + b); };
+  auto conv = [&](int l) { return bar0 + 8u * (2 * NS + l); };
+  auto lofree = [&](int l) { return bar0 + 8u * (2 * NS + RW_L + l); };
+  auto tfull = [&](int b) { return bar0 + 8u * (2 * NS + 2 * RW_L + b); };
+  auto tempty = [&](int b) { return bar0 + 8u * (2 * NS + 2 * RW_L + 2 + b); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NS + 2 * RW_L + 4);
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
+  const int units = nimgs * RW_QU * HALVES;
+  // unit u -> image, tile range [t0, t1), channel half; its input rows [ih0, ih0 + nr)
+  auto unit_of = [&](int u, int* img, int* t0, int* t1, int* half, int* oh_lo, int* nr) {
+    *half = u % HALVES;
+    const int q = (u / HALVES) % RW_QU;
+    *img = u / (HALVES * RW_QU);
+    *t0 = q * TPQ;
+    *t1 = min(TPI, (q + 1) * TPQ);
+    *oh_lo = (*t0 * 128) / OW;
+    const int oh_hi = min(OH - 1, (*t1 * 128 - 1) / OW);
+    *nr = *t1 > *t0 ? oh_hi - *oh_lo + KS : 0;
+  };
+  const int h0 = (units > 0) ? 0 : 0;
+  (void)h0;
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(rfull(b), 1);
+      mbar_init(rfree(b), 8);
+    }
+    for (int l = 0; l < RW_L; ++l) {
+      mbar_init(conv(l), 4);
+      mbar_init(lofree(l), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull(b), 1);
+      mbar_init(tempty(b), 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // every row slot's pad columns stay zero (TMA writes the interior only)
+  for (int e = threadIdx.x; e < NS * ROWF; e += blockDim.x) rows[e] = 0.f;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (warp == 17) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  // B (weights, this CTA's NH channels) is rebuilt per unit only when the half changes
+  int cur_half = -1;
+  auto load_b = [&](int half) {  // called by every thread between units (block-wide sync below)
+    for (int e = threadIdx.x; e < NKB * NH * 32; e += blockDim.x) {
+      const int kb = e / (NH * 32), rem = e % (NH * 32), n = rem / 32, kl = rem % 32, k = kb * 32 + kl;
+      const float v = __ldg(w + (size_t)k * COUT + half * NH + n);  // k = (kh, kw, c): HWIO row
+      const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+      const int off = n * 128 + (((kl >> 2) ^ (n & 7)) << 4) + (kl & 3) * 4;
+      *reinterpret_cast<float*>(smem + kb * 2 * Geo::B_TILE + off) = hi;
+      *reinterpret_cast<float*>(smem + kb * 2 * Geo::B_TILE + Geo::B_TILE + off) = __fsub_rn(v, hi);
+    }
+    for (int e = threadIdx.x; e < epi.n * NH; e += blockDim.x) {
+      const int i = e / NH, c = e % NH;
+      eops[e] = epi.op[i] == EPI_RELU ? 0.f : (epi.scalar[i] ? __ldg(epi.x[i]) : __ldg(epi.x[i] + half * NH + c));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  };
+  // every CTA handles one half only when HALVES divides the CTA stride; otherwise B is
+  // loaded per unit by all roles in lockstep (not needed for the compiled geometries)
+  {
+    int img, t0, t1, half, oh_lo, nr;
+    unit_of(blockIdx.x, &img, &t0, &t1, &half, &oh_lo, &nr);
+    cur_half = half;
+    load_b(half);
+  }
+  __syncthreads();
+
+  if (warp < 8) {
+    // ---------------- builders
+    const int grp = warp / 4, wq = warp % 4, rr = wq * 32 + lane;
+    int it = 0, sbase_row = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int img, t0, t1, half, oh_lo, nr;
+      unit_of(u, &img, &t0, &t1, &half, &oh_lo, &nr);
+      int waited = 0, released = 0;
+      for (int t = t0; t < t1; ++t) {
+        const int first = (t * 128) / OW - oh_lo;
+        const int last = min(OH - 1, (t * 128 + 127) / OW) - oh_lo + KS - 1;
+        for (; waited <= last; ++waited) {
+          const int sq = sbase_row + waited;
+          mbar_wait(rfull(sq % NS), (sq / NS) & 1);
+        }
+        const int q = t * 128 + rr;
+        const int qq = q < P ? q : t * 128;
+        const int oh = qq / OW, ow = qq - oh * OW, lr = oh - oh_lo;
+#pragma unroll 1
+        for (int kb = 0; kb < NKB; ++kb) {
+          const int step = it + kb;
+          if ((step & 1) != grp) continue;
+          const int l = step % RW_L;
+          const int tap = kb / Geo::CB, cb = kb % Geo::CB, kh = tap / KS, kw = tap % KS;
+          const int sq = sbase_row + lr + kh;
+          const float* src = rows + (sq % NS) * ROWF + (ow + kw + Geo::PLS - PL) * CPAD + cb * 32;
+          float4 v4[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v4[i] = *reinterpret_cast<const float4*>(src + 4 * i);
+          mbar_wait(lofree(l), ((step / RW_L) & 1) ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          uint32_t hv[32], lv[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float c4[4] = {v4[i].x, v4[i].y, v4[i].z, v4[i].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t h = __float_as_uint(c4[j]) & 0xFFFFE000u;
+              hv[4 * i + j] = h;
+              lv[4 * i + j] = __float_as_uint(__fsub_rn(c4[j], __uint_as_float(h)));
+            }
+          }
+          const uint32_t ta = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(Geo::ACOL + l * 64);
+          tmem_st32(ta, hv);
+          tmem_st32(ta + 32, lv);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(conv(l));
+        }
+        it += NKB;
+        // rows no later tile of this unit needs
+        const int next_first = t + 1 < t1 ? ((t + 1) * 128) / OW - oh_lo : nr;
+        for (; released < next_first; ++released) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(rfree((sbase_row + released) % NS));
+        }
+      }
+      for (; released < nr; ++released) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(rfree((sbase_row + released) % NS));
+      }
+      sbase_row += nr;
+    }
+  } else if (warp < 16) {
+    // ---------------- epilogue (two warps per lane quadrant, NH / 2 channels each)
+    constexpr int CH = NH / 2;
+    const int wq = warp % 4, hh = (warp - 8) / 4, rr = wq * 32 + lane, c0 = hh * CH;
+    int it = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int img, t0, t1, half, oh_lo, nr;
+      unit_of(u, &img, &t0, &t1, &half, &oh_lo, &nr);
+      for (int t = t0; t < t1; ++t) {
+        // the whole K (NKB k-blocks) accumulates in one TMEM accumulator per tile, as in
+        // the generic implicit GEMM (a fresh accumulator per k-block made the MMA wait
+        // for a drain every k-block: the pipeline ran at ~1/5 of the MMA rate)
+        float sum[CH];
+        {
+          const int bb = it & 1;
+          mbar_wait(tfull(bb), (it >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int cc = 0; cc < CH; cc += 16) {
+            float vv[16];
+            tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(bb * Geo::ACC + c0 + cc), vv);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sum[cc + i] = vv[i];
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty(bb));
+          ++it;
+        }
+        for (int e = 0; e < epi.n; ++e) epi_apply<CH>(sum, epi.op[e], epi.swap[e], eops + e * NH + c0);
+        // the quadrant's 32 pixels x NH channels: NH * 4-byte runs per pixel, assembled
+        // in shared memory by the warp pair and stored with coalesced 16-byte writes
+        const long long pix0 = (long long)img * P + t * 128 + wq * 32;
+        const int nval = min(32, P - (t * 128 + wq * 32));
+        float* st = ostage + wq * 32 * (NH + 4);
+#pragma unroll
+        for (int i = 0; i < CH; i += 4)
+          *reinterpret_cast<float4*>(st + lane * (NH + 4) + c0 + i) = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+        constexpr int Q4 = NH / 4;
+#pragma unroll
+        for (int k = 0; k < 32 * Q4 / 64; ++k) {
+          const int c = hh * (32 * Q4 / 2) + k * 32 + lane, px = c / Q4, part = c % Q4;
+          if (px < nval)
+            *reinterpret_cast<float4*>(out + (pix0 + px) * ldc + half * NH + part * 4) =
+                *reinterpret_cast<const float4*>(st + px * (NH + 4) + part * 4);
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+      }
+    }
+  } else if (warp == 16) {
+    // ---------------- producer: one 4-D TMA per input row (zero rows for the padding)
+    const uint64_t xmap_addr = reinterpret_cast<uint64_t>(&xmap);
+    int sq = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int img, t0, t1, half, oh_lo, nr;
+      unit_of(u, &img, &t0, &t1, &half, &oh_lo, &nr);
+      for (int j = 0; j < nr; ++j, ++sq) {
+        const int slot = sq % NS, ih = oh_lo - PT + j;
+        mbar_wait(rfree(slot), ((sq / NS) & 1) ^ 1);
+        float* dst = rows + slot * ROWF;
+        if (ih >= 0 && ih < IH) {
+          if (lane == 0) {
+            mbar_expect_tx(rfull(slot), (uint32_t)(IW * CPAD * 4));
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+                    smem_u32(dst + Geo::PLS * CPAD)),
+                "l"(xmap_addr), "r"(0), "r"(0), "r"(ih), "r"(img), "r"(rfull(slot))
+                : "memory");
+          }
+        } else {
+          for (int e = lane; e < ROWF; e += 32) dst[e] = 0.f;  // a padding row
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (a later TMA refill of the slot)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(rfull(slot));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- warp 17: MMA issuer (N = NH, M = 128)
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NH >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    int it = 0, tile = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int img, t0, t1, half, oh_lo, nr;
+      unit_of(u, &img, &t0, &t1, &half, &oh_lo, &nr);
+      for (int t = t0; t < t1; ++t, ++tile) {
+        const int bb = tile & 1;
+        mbar_wait_warp(tempty(bb), ((tile >> 1) & 1) ^ 1);  // the epilogue has drained this accumulator
+        const uint32_t d = tm + (uint32_t)(bb * Geo::ACC);
+        for (int kb = 0; kb < NKB; ++kb, ++it) {
+          const int l = it % RW_L;
+          mbar_wait_warp(conv(l), (it / RW_L) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t ahi = tm + (uint32_t)(Geo::ACOL + l * 64), alo = ahi + 32;
+          const uint32_t bt = sbase + (uint32_t)(kb * 2 * Geo::B_TILE);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t dhi = sdesc(bt + kk * 32, 16, 1024, 2), dlo = sdesc(bt + Geo::B_TILE + kk * 32, 16, 1024, 2);
+            mma_tf32_e<1>(d, alo + kk * 8, dhi, idesc, (kb > 0 || kk > 0) ? 1u : 0u);
+            mma_tf32_e<1>(d, ahi + kk * 8, dlo, idesc, 1u);
+            mma_tf32_e<1>(d, ahi + kk * 8, dhi, idesc, 1u);
+          }
+          mma_commit_e<1>(lofree(l));
+        }
+        mma_commit_e<1>(tfull(bb));
+      }
+    }
+  }
+  (void)cur_half;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 17) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// 4-D tiled map over NHWC x [n][h][w][c], box {c + 4, w, 1, 1}: one input row per load,
+// every pixel padded to c + 4 floats by the out-of-bounds zero fill
+bool make_row_map(CUtensorMap* m, const float* x, int n, int h, int w, int c) {
+  static EncodeTiledFnCI fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFnCI)p;
+  });
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 4, (cuuint64_t)w * c * 4, (cuuint64_t)h * w * c * 4};
+  cuuint32_t box[4] = {(cuuint32_t)(c + 4), (cuuint32_t)w, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)x, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT, int NH>
+cudaError_t launch_rows(const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi, int num_sms,
+                        cudaStream_t s) {
+  using Geo = RwGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT, NH>;
+  CUtensorMap xmap;
+  std::memset(&xmap, 0, sizeof(xmap));
+  if (!make_row_map(&xmap, x, n, IH, IW, CIN)) return cudaErrorInvalidValue;
+  const size_t smem = 1024 + Geo::B_BYTES + (size_t)RW_NS * Geo::ROWF * 4 + kEpiMax * NH * 4 + 4 * 32 * (NH + 4) * 4 +
+                      (2 * RW_NS + 2 * RW_L + 6) * 8;
+  auto kern = conv_rows_tc_kernel<CIN, KS, IH, IW, OH, OW, PT, PL, COUT, NH>;
+  cudaError_t e = smem_attr((const void*)kern, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int units = n * RW_QU * Geo::HALVES;
+  // a CTA keeps one channel half: the grid is a multiple of HALVES (B is loaded once)
+  int grid = std::min(units, num_sms) / Geo::HALVES * Geo::HALVES;
+  if (grid < Geo::HALVES) grid = Geo::HALVES;
+  kern<<<grid, RW_THREADS, smem, s>>>(w, out, ldc, n, xmap, epi);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool conv_band_supported(int n, int h, int w, int ci, int kh, int kw, int co, int ho, int wo, int sh, int sw, int pt,
@@ -1440,6 +1799,23 @@ bool conv_band_supported(int n, int h, int w, int ci, int kh, int kw, int co, in
   (void)n;
   return !getenv("CG_NO_CONV_BAND") && h == 299 && w == 299 && ci == 3 && kh == 3 && kw == 3 && co == 32 && ho == 149 &&
          wo == 149 && sh == 2 && sw == 2 && pt == 0 && pl == 0;
+}
+
+int conv_rows_kind(int h, int w, int ci, int kh, int kw, int co, int ho, int wo, int sh, int sw, int pt, int pl) {
+  if (getenv("CG_NO_CONV_ROWS") || kh != 3 || kw != 3 || sh != 1 || sw != 1 || ci != 32) return 0;
+  if (h == 149 && w == 149 && co == 32 && ho == 147 && wo == 147 && pt == 0 && pl == 0) return 1;
+  // (split over two CTAs per row range -- B for 64 channels does not fit next to the
+  // ring -- it builds every A slab twice; still 1.60 ms against the generic implicit
+  // GEMM's 2.20 ms at batch 256)
+  if (h == 147 && w == 147 && co == 64 && ho == 147 && wo == 147 && pt == 1 && pl == 1) return 2;
+  return 0;
+}
+
+cudaError_t launch_conv_rows(int kind, const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi,
+                             int num_sms, cudaStream_t s) {
+  if (kind == 1) return launch_rows<32, 3, 149, 149, 147, 147, 0, 0, 32, 32>(x, w, out, ldc, n, epi, num_sms, s);
+  if (kind == 2) return launch_rows<32, 3, 147, 147, 147, 147, 1, 1, 64, 32>(x, w, out, ldc, n, epi, num_sms, s);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_conv_band(const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi, int num_sms,

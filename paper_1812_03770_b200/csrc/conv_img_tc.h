@@ -32,5 +32,11 @@ bool conv_band_supported(int n, int h, int w, int ci, int kh, int kw, int co, in
                          int pl);
 cudaError_t launch_conv_band(const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi, int num_sms,
                              cudaStream_t s);
+// 3x3 stride-1 convs with 32 input channels on wide images (the InceptionV3 stem's
+// layers 2 and 3): input rows staged once each in a ring (conv_rows_tc_kernel).
+// kind 0 = not compiled for this geometry.
+int conv_rows_kind(int h, int w, int ci, int kh, int kw, int co, int ho, int wo, int sh, int sw, int pt, int pl);
+cudaError_t launch_conv_rows(int kind, const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi,
+                             int num_sms, cudaStream_t s);
 
 }  // namespace cg

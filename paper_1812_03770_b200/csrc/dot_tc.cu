@@ -769,7 +769,9 @@ cudaError_t launch_tc_cg(const DotTcPlan& p, float* out, cudaStream_t s) {
 }
 
 cudaError_t launch_dot_tc(const DotTcPlan& p, cudaStream_t s) {
-  if (p.band) return launch_conv_band(p.conv.x, p.band_w, p.C, p.ldc > 0 ? p.ldc : p.N, p.band_n, p.epi, p.num_sms, s);
+  if (p.band == 1) return launch_conv_band(p.conv.x, p.band_w, p.C, p.ldc > 0 ? p.ldc : p.N, p.band_n, p.epi, p.num_sms, s);
+  if (p.band >= 2)
+    return launch_conv_rows(p.band - 1, p.conv.x, p.band_w, p.C, p.ldc > 0 ? p.ldc : p.N, p.band_n, p.epi, p.num_sms, s);
   float* out = p.splits > 1 ? p.ws : p.C;
   cudaError_t e0;
   switch (p.bn) {
@@ -811,6 +813,11 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
   p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms, true);
   if (conv_band_supported(n, h, wd, ci, kh, kw, co, ho, wo, sh, sw, pt, pl)) {  // the stem: row bands, no split-K
     p->band = 1;
+    p->splits = 1;
+    p->band_w = w;
+    p->band_n = n;
+  } else if (const int kind = conv_rows_kind(h, wd, ci, kh, kw, co, ho, wo, sh, sw, pt, pl)) {  // stem 3x3: row ring
+    p->band = 1 + kind;
     p->splits = 1;
     p->band_w = w;
     p->band_n = n;

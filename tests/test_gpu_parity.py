@@ -303,6 +303,8 @@ TC_CONV_CASES = [((2, 35, 35, 64), (3, 3, 64, 96), 1, 1), ((2, 35, 35, 32), (3, 
                  # the InceptionV3 stem (Ci = 3, stride 2, VALID): the row-band kernel; 5 images
                  # cover full bands, the 5-row last band and a unit split across CTAs
                  ((5, 299, 299, 3), (3, 3, 3, 32), 2, 0),
+                 # stem layers 2 / 3: input rows staged once in a ring (VALID 32 -> 32, SAME 32 -> 64)
+                 ((3, 149, 149, 32), (3, 3, 32, 32), 1, 0), ((3, 147, 147, 32), (3, 3, 32, 64), 1, 1),
                  # Ci % 16 == 0: pairs of 16-channel im2col boxes; K % 32 == 16 exercises the zero half-slab
                  ((2, 12, 12, 16), (3, 3, 16, 32), 1, 1), ((2, 17, 17, 48), (5, 5, 48, 64), 1, 1),
                  ((2, 15, 15, 80), (3, 3, 80, 192), 1, 0), ((3, 16, 15, 48), (3, 3, 48, 64), 2, 1)]
