@@ -45,7 +45,8 @@ namespace {
 
 constexpr int CI_THREADS = 448;   // 14 warps
 constexpr int CI_L = 6;           // A stages in TMEM (64 columns each: 32 hi + 32 lo)
-constexpr int CI_ACOL = 32;       // TMEM columns 0..31: two 16-column accumulators
+constexpr int CI_NACC = 4;        // 16-column accumulators (more tiles between the MMA and the epilogue)
+constexpr int CI_ACOL = 16 * CI_NACC;
 
 // Staged images for the small-image kernels: [HP][WPS][CIN] at XBASE + g * IMGF,
 // zero where a window leaves the image.  Staging modes (one TMA-engine operation per
@@ -190,8 +191,8 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   auto conv = [&](int l) { return bar0 + 8u * (4 + l); };
   auto lofree = [&](int l) { return bar0 + 8u * (4 + CI_L + l); };
   auto tfull = [&](int b) { return bar0 + 8u * (4 + 2 * CI_L + b); };
-  auto tempty = [&](int b) { return bar0 + 8u * (6 + 2 * CI_L + b); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * CI_L);
+  auto tempty = [&](int b) { return bar0 + 8u * (4 + 2 * CI_L + CI_NACC + b); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * CI_L + 2 * CI_NACC);
 
   // role index through a shuffle: provably warp-uniform (convergent role branches)
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
@@ -201,6 +202,8 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(imgfull(b), 1);    // the producer's arrive.expect_tx
       mbar_init(imgfree(b), 8);    // every builder warp
+    }
+    for (int b = 0; b < CI_NACC; ++b) {
       mbar_init(tfull(b), 1);
       mbar_init(tempty(b), 4);     // the epilogue warps
     }
@@ -305,8 +308,8 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
         // every k-block
         float sum[16];
         {
-          const int b = it & 1;
-          mbar_wait(tfull(b), (it >> 1) & 1);
+          const int b = it % CI_NACC;
+          mbar_wait(tfull(b), (it / CI_NACC) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * 16), sum);
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -349,8 +352,8 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     int it = 0, tile = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x)
       for (int t = 0; t < T; ++t, ++tile) {
-        const int b = tile & 1;
-        mbar_wait_warp(tempty(b), ((tile >> 1) & 1) ^ 1);  // the epilogue has read this accumulator
+        const int b = tile % CI_NACC;
+        mbar_wait_warp(tempty(b), ((tile / CI_NACC) & 1) ^ 1);  // the epilogue has read this accumulator
         const uint32_t d = tm + (uint32_t)(b * 16);
         for (int kb = 0; kb < NKB; ++kb, ++it) {
           const int l = it % CI_L;
