@@ -136,7 +136,7 @@ typedef struct cg_plan_info {
   int32_t n_groups;          /* kernel groups in evaluation order Gamma */
   int32_t n_blocks;          /* shared pool blocks */
   int32_t n_kernels;         /* distinct generated kernels compiled */
-  int32_t n_fused;           /* elementwise groups computed in a tensor-core epilogue (f2) */
+  int32_t n_fused;           /* elementwise groups computed inside another group's kernel (f2: DOT / CONV / pool epilogues, pool prologues) */
   uint64_t pool_bytes;       /* sum of align256(block bytes) */
   uint64_t plan_bytes;       /* sum of exact block bytes */
   uint64_t external_bytes;   /* Var + Const buffers */

@@ -46,6 +46,7 @@ __device__ __forceinline__ float apply_chain(const EpiProg& epi, float v, long l
       case EPI_DIV: v = __fdiv_rn(a, b); break;
       case EPI_MAX: asm("max.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(b)); break;
       case EPI_MIN: asm("min.NaN.f32 %0, %1, %2;" : "=f"(v) : "f"(a), "f"(b)); break;
+      case EPI_RGRAD: v = a > 0.f ? b : 0.f; break;
     }
   }
   return v;

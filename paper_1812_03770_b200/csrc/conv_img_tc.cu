@@ -21,9 +21,11 @@
 // tile's k-blocks now chain in one accumulator (integer-exact tests unaffected).
 //
 // Work: persistent CTAs over units of G whole images (G*P pixels = T tiles of
-// 128).  Warps: 0-3 image loaders (global NHWC -> planar smem, double-buffered),
-// 4-7 and 8-11 two builder groups taking alternate k-blocks, 12-15 epilogue,
-// 16 TMEM allocator + MMA issuer.  Deterministic: fixed summation order.
+// 128).  Warps: 0-3 and 4-7 two builder groups taking alternate k-blocks, 8-11 and
+// 12-15 two epilogue groups taking alternate tiles (the epilogue's per-tile latency
+// -- TMEM load, fused chain, stores -- was the bound once a chain was fused), 16
+// the TMA producer (images, double-buffered), 17 TMEM allocator + MMA issuer.
+// Deterministic: fixed summation order.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -43,7 +45,7 @@ namespace {
 
 #include "tc_prims.cuh"
 
-constexpr int CI_THREADS = 448;   // 14 warps
+constexpr int CI_THREADS = 576;   // 18 warps
 constexpr int CI_L = 6;           // A stages in TMEM (64 columns each: 32 hi + 32 lo)
 constexpr int CI_NACC = 4;        // 16-column accumulators (more tiles between the MMA and the epilogue)
 constexpr int CI_ACOL = 16 * CI_NACC;
@@ -173,7 +175,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
 __global__ void __launch_bounds__(CI_THREADS, 1)
     conv_img_tc_kernel(const float* __restrict__ in, const float* __restrict__ w, float* __restrict__ out, int nimgs,
-                       int G, int T, const __grid_constant__ CUtensorMap xmap) {
+                       int G, int T, const __grid_constant__ CUtensorMap xmap, const __grid_constant__ EpiProg epi) {
   using Geo = CiGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
   using SG = typename Geo::SG;
   constexpr int K = Geo::K, NKB = Geo::NKB, P = Geo::P;
@@ -193,6 +195,9 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   auto tfull = [&](int b) { return bar0 + 8u * (4 + 2 * CI_L + b); };
   auto tempty = [&](int b) { return bar0 + 8u * (4 + 2 * CI_L + CI_NACC + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * CI_L + 2 * CI_NACC);
+  // the fused chain's scalar / column operands, staged once: epx[e][co]
+  float* epx = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
+  static_assert((4 + 2 * CI_L + 2 * CI_NACC) * 8 + 4 <= 256, "barrier area");
 
   // role index through a shuffle: provably warp-uniform (convergent role branches)
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
@@ -230,8 +235,12 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   }
   // the padding / guard of both image buffers stays zero (TMA writes only the frames)
   for (int e = threadIdx.x; e < 2 * buf_floats; e += blockDim.x) imgs[e] = 0.f;
+  for (int e = threadIdx.x; e < epi.n * COUT; e += blockDim.x) {
+    const int op = e / COUT, c = e % COUT;
+    epx[e] = epi.op[op] == EPI_RELU || epi.scalar[op] == 2 ? 0.f : __ldg(epi.x[op] + (epi.scalar[op] == 1 ? 0 : c));
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core / TMA
-  if (warp == 13) {
+  if (warp == 17) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -296,13 +305,15 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(imgfree(b));  // this warp has read the images of unit j
     }
-  } else if (warp < 12) {
-    // ---------------- epilogue: each k-block's accumulator -> round-to-nearest register sum
-    const int wq = warp % 4, rr = wq * 32 + lane;
+  } else if (warp < 16) {
+    // ---------------- epilogue: two groups of four warps (one per TMEM lane quadrant)
+    // take alternate tiles; accumulator b = tile % CI_NACC always goes to group b % 2
+    const int wq = warp % 4, rr = wq * 32 + lane, eg = (warp - 8) / 4;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int n0 = u * G, nimg = min(G, nimgs - n0);
-      for (int t = 0; t < T; ++t) {
+      for (int t = 0; t < T; ++t, ++it) {
+        if ((it & 1) != eg) continue;
         // the tile's NKB k-blocks accumulate in one TMEM accumulator (as the generic
         // implicit GEMM); a fresh accumulator per k-block made the MMA wait for a drain
         // every k-block
@@ -315,11 +326,30 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty(b));
-          ++it;
         }
         const int q = t * 128 + rr;
         if (q < nimg * P) {
           float* o = out + ((size_t)n0 * P + q) * COUT;
+          if (epi.n) {  // fused elementwise chain (f2), op by op as the separate kernel
+            float v[COUT];
+#pragma unroll
+            for (int i = 0; i < COUT; ++i) v[i] = sum[i];
+#pragma unroll 1
+            for (int e = 0; e < epi.n; ++e) {
+              float xe[COUT];
+              if (epi.scalar[e] == 2) {  // full tensor: this pixel's COUT values
+                const float* src = epi.x[e] + ((size_t)n0 * P + q) * COUT;
+#pragma unroll
+                for (int i = 0; i < COUT; ++i) xe[i] = __ldg(src + i);
+              } else {
+#pragma unroll
+                for (int i = 0; i < COUT; ++i) xe[i] = epx[e * COUT + i];
+              }
+              epi_apply<COUT>(v, epi.op[e], epi.swap[e], xe);
+            }
+#pragma unroll
+            for (int i = 0; i < COUT; ++i) sum[i] = v[i];
+          }
           if (COUT % 4 == 0) {
 #pragma unroll
             for (int i = 0; i < COUT; i += 4)
@@ -334,7 +364,7 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
         }
       }
     }
-  } else if (warp == 12) {
+  } else if (warp == 16) {
     // ---------------- producer: one TMA-engine copy per unit of G images (double-buffered)
     const uint64_t xmap_addr = reinterpret_cast<uint64_t>(&xmap);  // (address of the parameter itself)
     int j = 0;
@@ -345,7 +375,7 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
       stage_images<SG>(smem_u32(imgs + b * buf_floats), in, xmap_addr, n0, nimg, G, imgfull(b), lane);
     }
   } else {
-    // ---------------- warp 13: MMA issuer (whole warp walks the loop; one elected lane issues)
+    // ---------------- warp 17: MMA issuer (whole warp walks the loop; one elected lane issues)
     // instruction descriptor: D f32, A / B tf32, A (TMEM) and B K-major, N = 16, M = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
@@ -375,7 +405,7 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 13) {
+  if (warp == 17) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
@@ -1082,7 +1112,8 @@ cudaError_t launch_bwdin(const float* dy, const float* w, float* dx, int n, int 
 }
 
 template <int CIN, int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
-cudaError_t launch_geo(const float* in, const float* w, float* out, int n, int num_sms, cudaStream_t s) {
+cudaError_t launch_geo(const float* in, const float* w, float* out, int n, const EpiProg* epi, int num_sms,
+                       cudaStream_t s) {
   using Geo = CiGeo<CIN, KS, IH, IW, OH, OW, PT, PL, COUT>;
   using SG = typename Geo::SG;
   if (reinterpret_cast<uintptr_t>(in) & 15) return cudaErrorMisalignedAddress;
@@ -1101,7 +1132,7 @@ cudaError_t launch_geo(const float* in, const float* w, float* out, int n, int n
     if (cost < best_cost) { best_cost = cost; best_g = G; }
   }
   const int G = best_g, T = (G * Geo::P + 127) / 128;
-  const size_t smem = 1024 + Geo::B_BYTES + 2 * buf_bytes(G) + 256;
+  const size_t smem = 1024 + Geo::B_BYTES + 2 * buf_bytes(G) + 256 + kEpiMax * COUT * 4;
   CUtensorMap xmap;
   std::memset(&xmap, 0, sizeof(xmap));
   if (SG::TMAP && !make_img_map(&xmap, in, n, IH, IW, SG::WPS, SG::HP, G)) return cudaErrorInvalidValue;
@@ -1109,7 +1140,9 @@ cudaError_t launch_geo(const float* in, const float* w, float* out, int n, int n
   cudaError_t e = smem_attr((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
   const int units = (n + G - 1) / G;
-  kern<<<std::min(units, num_sms), CI_THREADS, smem, s>>>(in, w, out, n, G, T, xmap);
+  EpiProg ep{};
+  if (epi) ep = *epi;
+  kern<<<std::min(units, num_sms), CI_THREADS, smem, s>>>(in, w, out, n, G, T, xmap, ep);
   return cudaGetLastError();
 }
 
@@ -1852,12 +1885,13 @@ bool conv_img_tc_supported(const ConvGeom& g, bool flip) {
 }
 
 cudaError_t launch_conv_img_tc(const float* in, const float* w, float* out, const ConvGeom& g, bool flip, int num_sms,
-                               cudaStream_t s) {
+                               cudaStream_t s, const EpiProg* epi) {
+  if (flip && epi && epi->n) return cudaErrorInvalidValue;  // (no epilogue on the col2im kernel)
   switch (kind_of(g, flip)) {
     case CI_C4_CONV1:  // x [n,28,28,1] (*) w [5,5,1,6], SAME
-      return launch_geo<1, 5, 28, 28, 28, 28, 2, 2, 6>(in, w, out, g.n, num_sms, s);
+      return launch_geo<1, 5, 28, 28, 28, 28, 2, 2, 6>(in, w, out, g.n, epi, num_sms, s);
     case CI_C4_CONV2:  // p1 [n,14,14,6] (*) w [5,5,6,16], VALID
-      return launch_geo<6, 5, 14, 14, 10, 10, 0, 0, 16>(in, w, out, g.n, num_sms, s);
+      return launch_geo<6, 5, 14, 14, 10, 10, 0, 0, 16>(in, w, out, g.n, epi, num_sms, s);
     case CI_C4_CONV2_BWDIN:  // dy [n,10,10,16], w [5,5,6,16] -> dx [n,14,14,6] (VALID forward)
       return launch_bwdin<16, 5, 10, 10, 14, 14, 0, 0, 6>(in, w, out, g.n, num_sms, s);
     default:

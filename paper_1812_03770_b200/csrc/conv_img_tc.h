@@ -9,12 +9,16 @@
 
 namespace cg {
 
+struct EpiProg;
+
 // true when (geometry, pass) has a compiled instantiation; flip = backward-input
 bool conv_img_tc_supported(const ConvGeom& g, bool flip);
 // fwd:  y[n,oh,ow,co] = sum_{kh,kw,ci} x[n,oh+kh-pt,ow+kw-pl,ci] w[kh,kw,ci,co]
 // flip: dx[n,h,w,ci]  = sum_{kh,kw,co} dy[n,h-kh+pt,w-kw+pl,co] w[kh,kw,ci,co]   (stride 1)
+// epi (forward only; NULL or n == 0: plain store): the fused elementwise chain of
+// the f2 epilogue fusion, applied to each output pixel's COUT values before the store
 cudaError_t launch_conv_img_tc(const float* in, const float* w, float* out, const ConvGeom& g, bool flip, int num_sms,
-                               cudaStream_t s);
+                               cudaStream_t s, const EpiProg* epi = nullptr);
 
 // backward-kernel (C4 geometries; g = the forward conv): dw[kh,kw,ci,co] =
 // sum_{n,oh,ow} x[n,oh+kh-pt,ow+kw-pl,ci] dy[n,oh,ow,co]; per-CTA partials in ws
@@ -27,7 +31,6 @@ cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, 
 // The InceptionV3 stem conv (Ci = 3, stride 2) over bands of output rows, with the
 // DOT/CONV epilogue's fused elementwise chain (conv_band_tc_kernel); x must be
 // 16-byte aligned and may be over-read by up to 12 bytes inside its allocation.
-struct EpiProg;
 bool conv_band_supported(int n, int h, int w, int ci, int kh, int kw, int co, int ho, int wo, int sh, int sw, int pt,
                          int pl);
 cudaError_t launch_conv_band(const float* x, const float* w, float* out, int ldc, int n, const EpiProg& epi, int num_sms,

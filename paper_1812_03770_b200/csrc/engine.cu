@@ -307,6 +307,16 @@ struct cg_graph {
   // group of a DOT/CONV group and vice versa (-1: none); fused_away[d] = the DOT/CONV
   // value is never materialised (its consumer group is computed in the epilogue)
   std::vector<std::shared_ptr<DotTcPlan>> tcplan;
+  // f2 fusion into non-GEMM producers / consumers: per group, the chain a kernel
+  // applies (conv_img_tc forward and maxpool backward: epilogue on `out`; maxpool
+  // forward: prologue from `in`, its result stored to `xo`)
+  struct EpiSlot {
+    EpiProg epi{};
+    float* out = nullptr;
+    const float* in = nullptr;
+    float* xo = nullptr;
+  };
+  std::vector<std::shared_ptr<EpiSlot>> eslot;
   // f3 fused AllReduce + update over peer memory (CG_PLAN_FUSED_COLL): per
   // ALLREDUCE group its segment (n == 0: none); device table = one entry per group
   // followed by the batched steps of a full evaluation (contiguous per step)
@@ -334,6 +344,7 @@ struct cg_graph {
   int n_views_direct = 0, n_views_copied = 0;
   std::vector<char> fused_away;
   int n_fused = 0;
+  int n_pool_fused = 0;  // f2 pooling prologues (elementwise group computed inside a max pool)
   cg_plan_info info{};
 
   int fail(int code, const std::string& m) {
@@ -406,6 +417,7 @@ static void fuse_epilogues(cg_graph* g) {
   g->partner.assign(NG, -1);
   g->fused_away.assign(hg.nodes.size(), 0);
   g->n_fused = 0;
+  g->n_pool_fused = 0;
   if (getenv("CG_NO_EPILOGUE_FUSION")) return;
   std::vector<int> consumers(hg.nodes.size(), 0), consumer_group(hg.nodes.size(), -1);
   for (size_t gi = 0; gi < NG; ++gi)
@@ -413,19 +425,20 @@ static void fuse_epilogues(cg_graph* g) {
       consumers[p]++;
       consumer_group[p] = (int)gi;
     }
-  for (size_t gd = 0; gd < NG; ++gd) {
-    auto plan = g->tcplan[gd];
-    if (!plan || plan->splits != 1) continue;
-    const int d = hg.groups[gd].sink;
-    if (hg.keep[d] || consumers[d] != 1) continue;
-    const int ge = consumer_group[d];
-    const Group& E = hg.groups[ge];
-    if (E.kind != G_EW || E.materialised.size() != 1 || E.domain != hg.nodes[d].shape) continue;
-    const Shape& D = hg.nodes[d].shape;
-    const int64_t ncol = D.back();
-    EpiProg prog{};
-    int prev = d;
-    bool ok = true;
+  auto is_view = [&](int v) { return !hg.pl.view_root.empty() && hg.pl.view_root[v] >= 0; };
+  // the group whose kernel writes v (a chain absorbed into another group's kernel is
+  // written at that group's position)
+  auto writer = [&](int v) {
+    const int gv = hg.group_of[v];
+    return gv >= 0 && g->partner[gv] >= 0 && g->glaunch[gv].empty() ? g->partner[gv] : gv;
+  };
+  // E's members as one chain starting from value `start` over domain D; the other
+  // operand of each op: a scalar, a per-column vector (external), or -- when `full`
+  // -- a full tensor of shape D (external, or internal and written before `host`)
+  auto build_chain = [&](const Group& E, int start, const Shape& D, bool full, int host, EpiProg& prog) {
+    const int64_t ncol = D.back(), nall = numel(D);
+    prog = EpiProg{};
+    int prev = start;
     for (int m : E.members) {
       const Node& nd = hg.nodes[m];
       int op = 0;
@@ -437,33 +450,90 @@ static void fuse_epilogues(cg_graph* g) {
         case CG_RELU: op = EPI_RELU; break;
         case CG_MAX2: op = EPI_MAX; break;
         case CG_MIN2: op = EPI_MIN; break;
-        default: ok = false;
+        case CG_RELU_GRAD: op = EPI_RGRAD; break;
+        default: return false;
       }
-      if (!ok || prog.n == kEpiMax) { ok = false; break; }
+      if (prog.n == kEpiMax) return false;
       const int e = prog.n++;
       prog.op[e] = op;
       if (op == EPI_RELU) {
-        ok = nd.preds.size() == 1 && nd.preds[0] == prev;
+        if (nd.preds.size() != 1 || nd.preds[0] != prev) return false;
       } else {
         const int a = nd.preds[0], b = nd.preds[1];
-        if ((a == prev) == (b == prev)) { ok = false; break; }  // exactly one chain operand
+        if ((a == prev) == (b == prev)) return false;  // exactly one chain operand
         const int x = a == prev ? b : a;
         prog.swap[e] = a == prev ? 0 : 1;
         const Shape& xs = hg.nodes[x].shape;
         const int64_t nx = numel(xs);
-        bool col = nx == ncol && !xs.empty() && xs.back() == ncol;
-        if (!hg.is_external(x) || !(nx == 1 || col)) { ok = false; break; }
-        prog.scalar[e] = nx == 1 ? 1 : 0;
+        const bool col = nx == ncol && !xs.empty() && xs.back() == ncol;
+        const bool whole = full && nx == nall && xs == D;
+        if (hg.is_external(x)) {
+          if (!(nx == 1 || col || whole)) return false;
+        } else {  // an internal value: full tensor, final before the host kernel runs
+          if (!whole || is_view(x) || g->fused_away[x] || writer(x) >= host) return false;
+        }
+        prog.scalar[e] = nx == 1 ? 1 : (whole && !col) ? 2 : 0;
         prog.x[e] = g->ptr[x];
       }
-      if (!ok) break;
       prev = m;
     }
-    if (!ok || prev != E.sink) continue;
+    return prev == E.sink;
+  };
+  // f2 pooling prologue: an elementwise group E feeding a 2x2 max pool P at the next
+  // Gamma position runs inside P's kernel (P reads E's input, writes E's value and
+  // pools it): E's value makes one HBM round trip fewer.  E's inputs must still be
+  // intact at P (P's outputs do not take their blocks).
+  const bool no_slot = getenv("CG_NO_POOL_FUSION") != nullptr;  // A/B switch: GEMM epilogues only
+  for (size_t gp = 1; gp < NG && !no_slot; ++gp) {
+    auto sl = g->eslot[gp];
+    const Node& pn = hg.nodes[hg.groups[gp].sink];
+    if (!sl || pn.op != CG_MAXPOOL2D) continue;
+    const int x = pn.preds[0];
+    if (hg.is_external(x) || hg.keep[x] || is_view(x)) continue;
+    const int ge = hg.group_of[x];
+    if (ge != (int)gp - 1) continue;
+    const Group& E = hg.groups[ge];
+    if (E.kind != G_EW || E.materialised.size() != 1 || E.sink != x || E.domain != hg.nodes[x].shape) continue;
+    const Node& first = hg.nodes[E.members[0]];
+    int start = -1;  // the chain's input: a full-shaped internal value
+    for (int q : first.preds)
+      if (!hg.is_external(q) && hg.nodes[q].shape == E.domain && !is_view(q) && !g->fused_away[q]) { start = q; break; }
+    if (start < 0) continue;
+    EpiProg prog;
+    if (!build_chain(E, start, E.domain, true, ge, prog)) continue;
+    bool clash = false;
+    for (int q : E.inputs)
+      for (int m : hg.groups[gp].materialised)
+        if (!hg.is_external(q) && hg.pl.block_of[q] == hg.pl.block_of[m]) clash = true;
+    if (clash) continue;
+    sl->epi = prog;
+    sl->in = g->ptr[start];
+    sl->xo = g->ptr[x];
+    g->glaunch[ge].clear();
+    g->partner[gp] = ge;
+    g->partner[ge] = (int)gp;
+    g->n_pool_fused++;
+  }
+  for (size_t gd = 0; gd < NG; ++gd) {
+    auto plan = g->tcplan[gd];
+    auto sl = g->eslot[gd];
+    const int sop = hg.nodes[hg.groups[gd].sink].op;
+    const bool tc = plan && plan->splits == 1;
+    const bool slot = sl && !no_slot && (sop == CG_CONV2D || sop == CG_MAXPOOL2D_BWD);
+    if ((!tc && !slot) || g->partner[gd] >= 0) continue;
+    const int d = hg.groups[gd].sink;
+    if (hg.keep[d] || consumers[d] != 1) continue;
+    const int ge = consumer_group[d];
+    const Group& E = hg.groups[ge];
+    if (E.kind != G_EW || E.materialised.size() != 1 || E.domain != hg.nodes[d].shape || g->partner[ge] >= 0) continue;
+    EpiProg prog;
+    if (!build_chain(E, d, hg.nodes[d].shape, slot, (int)gd, prog)) continue;
+    if (slot && is_view(E.sink)) continue;  // (only the GEMM epilogue stores strided slices)
     // The fused kernel writes the sink's block at gd's position in Gamma, while the
     // plan gives that block to the sink only at ge's: unless the sink slid into d's
     // block, no group strictly between the two may touch the block (its previous
-    // occupant may still be read there).
+    // occupant may still be read there).  (A full-tensor chain operand sharing the
+    // block is read at the same element, by the same thread, before the store.)
     {
       const int B = hg.pl.block_of[E.sink];
       bool clash = false;
@@ -482,8 +552,13 @@ static void fuse_epilogues(cg_graph* g) {
       }
       if (clash) continue;
     }
-    plan->epi = prog;
-    plan->C = g->ptr[E.sink];
+    if (tc) {
+      plan->epi = prog;
+      plan->C = g->ptr[E.sink];
+    } else {
+      sl->epi = prog;
+      sl->out = g->ptr[E.sink];
+    }
     g->glaunch[ge].clear();
     g->partner[gd] = ge;
     g->partner[ge] = (int)gd;
@@ -618,6 +693,7 @@ static int build_launches(cg_graph* g) {
   }
   // 2) closures
   g->tcplan.assign(hg.groups.size(), nullptr);
+  g->eslot.assign(hg.groups.size(), nullptr);
   std::vector<std::shared_ptr<EwLaunch>> ew(hg.groups.size());
   // R14: a writer that cannot store a strided slice computes into scratch, then a
   // strided copy (the concat kernel with one source) places it
@@ -749,7 +825,13 @@ static int build_launches(cg_graph* g) {
         int sms = g->num_sms;
         static const bool prefer_tc = getenv("CG_CONV_PREFER_TC") != nullptr;  // A/B measurement switch
         if (conv_img_tc_supported(cgm, false)) {  // small images, few channels: tcgen05 with smem-staged images
-          L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_img_tc(x, w, out, cgm, false, sms, s); }, 1});
+          auto sl = std::make_shared<cg_graph::EpiSlot>();
+          sl->out = out;
+          g->eslot[gi] = sl;
+          L.push_back({[x, w, sl, cgm, sms](cudaStream_t s) {
+                         return launch_conv_img_tc(x, w, sl->out, cgm, false, sms, s, &sl->epi);
+                       },
+                       1});
         } else if (conv_small_fwd_ok(cgm) && cgm.co <= 16 && !prefer_tc) {  // few channels: whole images in shared memory
           L.push_back({[x, w, out, cgm, sms](cudaStream_t s) { return launch_conv_small_fwd(x, w, out, cgm, sms, s); }, 1});
         } else if (cgm.kh == 1 && cgm.kw == 1 && cgm.sh == 1 && cgm.sw == 1 && cgm.pt == 0 && cgm.pl == 0 &&
@@ -813,6 +895,13 @@ static int build_launches(cg_graph* g) {
         ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, ys, nd.attr.kh, nd.attr.kw);
         const float* x = in[0];
         bool mx = nd.op == CG_MAXPOOL2D;
+        if (mx && maxpool_fusable(cgm)) {  // may compute its input's elementwise group (f2 pooling prologue)
+          auto sl = std::make_shared<cg_graph::EpiSlot>();
+          sl->in = x;
+          g->eslot[gi] = sl;
+          L.push_back({[sl, out, cgm](cudaStream_t s) { return launch_maxpool(sl->in, out, cgm, s, &sl->epi, sl->xo); }, 1});
+          break;
+        }
         L.push_back({[x, out, cgm, mx](cudaStream_t s) { return mx ? launch_maxpool(x, out, cgm, s) : launch_avgpool(x, out, cgm, s); },
                      1});
         break;
@@ -820,6 +909,13 @@ static int build_launches(cg_graph* g) {
       case CG_MAXPOOL2D_BWD: {
         ConvGeom cgm = geom(nd, hg.nodes[nd.preds[0]].shape, hg.nodes[nd.preds[1]].shape, nd.attr.kh, nd.attr.kw);
         const float *x = in[0], *dy = in[1];
+        if (maxpool_fusable(cgm)) {  // may apply its consumer's elementwise chain (f2 epilogue)
+          auto sl = std::make_shared<cg_graph::EpiSlot>();
+          sl->out = out;
+          g->eslot[gi] = sl;
+          L.push_back({[x, dy, sl, cgm](cudaStream_t s) { return launch_maxpool_bwd(x, dy, sl->out, cgm, s, &sl->epi); }, 1});
+          break;
+        }
         L.push_back({[x, dy, out, cgm](cudaStream_t s) { return launch_maxpool_bwd(x, dy, out, cgm, s); }, 1});
         break;
       }
@@ -1537,7 +1633,7 @@ int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint3
   g->info.n_groups = (int)hg.groups.size();
   g->info.n_blocks = (int)hg.pl.size.size();
   g->info.n_kernels = g->n_kernels;
-  g->info.n_fused = g->n_fused;
+  g->info.n_fused = g->n_fused + g->n_pool_fused;
   g->info.pool_bytes = hg.pl.pool_bytes;
   g->info.plan_bytes = hg.pl.plan_bytes;
   g->info.workspace_bytes = g->ws_floats * sizeof(float);

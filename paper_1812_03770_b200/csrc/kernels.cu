@@ -11,6 +11,8 @@
 // results are run-to-run bit-stable.
 #include "kernels.h"
 
+#include "dot_tc.h"  // EpiProg / epi_run (f2 pooling fusion)
+
 #include <algorithm>
 #include <climits>
 #include <type_traits>
@@ -389,8 +391,13 @@ __global__ void maxpool_bwd_tiled_kernel(const float* __restrict__ x, const floa
 // 2 x 2 stride-2 VALID max pool with few channels (C4: C = 6, 16).  Thread =
 // (output pixel, V channels) so neighbouring lanes read neighbouring 8- / 16-byte
 // pieces of the same window rows.  Same combine order as maxpool_kernel (bit-identical).
+// With pro.n > 0 (f2 pooling fusion, even H and W) the window values are first
+// computed from x by the producer's elementwise chain and stored to xo (every
+// element of xo lies in exactly one window), then pooled.  xo may alias x (an
+// in-place chain): each element is read and written by the same thread, in order.
 template <int C, int V>
-__global__ void maxpool2_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, ConvGeom g, int total) {
+__global__ void maxpool2_fwd_kernel(const float* x, float* __restrict__ y, ConvGeom g, int total, float* xo,
+                                    const __grid_constant__ EpiProg pro) {
   using VT = typename std::conditional<V == 4, float4, float2>::type;
   constexpr int Q = C / V;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
@@ -398,10 +405,23 @@ __global__ void maxpool2_fwd_kernel(const float* __restrict__ x, float* __restri
     const int wo = p % g.wo, q = p / g.wo, ho = q % g.ho, n = q / g.ho;
     const size_t o0 = (((size_t)n * g.h + 2 * ho) * g.w + 2 * wo) * C + c, o1 = o0 + (size_t)g.w * C;
     VT w4[4];
-    w4[0] = __ldg(reinterpret_cast<const VT*>(x + o0));
-    w4[1] = __ldg(reinterpret_cast<const VT*>(x + o0 + C));
-    w4[2] = __ldg(reinterpret_cast<const VT*>(x + o1));
-    w4[3] = __ldg(reinterpret_cast<const VT*>(x + o1 + C));
+    w4[0] = *reinterpret_cast<const VT*>(x + o0);
+    w4[1] = *reinterpret_cast<const VT*>(x + o0 + C);
+    w4[2] = *reinterpret_cast<const VT*>(x + o1);
+    w4[3] = *reinterpret_cast<const VT*>(x + o1 + C);
+    if (pro.n) {
+      const size_t off[4] = {o0, o0 + C, o1, o1 + C};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float v[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[e] = reinterpret_cast<const float*>(&w4[k])[e];
+        epi_run<V>(pro, v, (long long)off[k], c);
+#pragma unroll
+        for (int e = 0; e < V; ++e) reinterpret_cast<float*>(&w4[k])[e] = v[e];
+        *reinterpret_cast<VT*>(xo + off[k]) = w4[k];
+      }
+    }
     const float* wf = reinterpret_cast<const float*>(w4);
     VT o;
     float* of = reinterpret_cast<float*>(&o);
@@ -420,9 +440,13 @@ __global__ void maxpool2_fwd_kernel(const float* __restrict__ x, float* __restri
 // (row-major, as maxpool_bwd_tiled_kernel); rows / columns a VALID pool never
 // reads (odd H or W) get zero gradient.  Thread = (output pixel, V channels):
 // neighbouring lanes touch neighbouring 8- / 16-byte pieces of the same window rows.
+// With epi.n > 0 (f2 pooling fusion, even H and W: no skipped rows / columns) the
+// consumer's elementwise chain is applied to every gradient value before the store;
+// its full-tensor operands are read at the same flat index (dx may alias one of
+// them: same thread, read before write).
 template <int C, int V>
-__global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ dx,
-                                    ConvGeom g, int total) {
+__global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* dx, ConvGeom g,
+                                    int total, const __grid_constant__ EpiProg epi) {
   using VT = typename std::conditional<V == 4, float4, float2>::type;
   constexpr int Q = C / V;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
@@ -450,6 +474,18 @@ __global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) rf[k * V + e] = best == k ? df[e] : 0.f;
+    }
+    if (epi.n) {
+      const size_t off[4] = {o0, o0 + C, o1, o1 + C};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float v[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[e] = rf[k * V + e];
+        epi_run<V>(epi, v, (long long)off[k], c);
+#pragma unroll
+        for (int e = 0; e < V; ++e) rf[k * V + e] = v[e];
+      }
     }
     *reinterpret_cast<VT*>(dx + o0) = r4[0];
     *reinterpret_cast<VT*>(dx + o0 + C) = r4[1];
@@ -790,12 +826,19 @@ static bool maxpool2_ok(const ConvGeom& g) {
          g.w <= 2 * g.wo + 1 && !getenv("CG_POOL_GENERIC");
 }
 
-cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s) {
+bool maxpool_fusable(const ConvGeom& g) { return maxpool2_ok(g) && g.h == 2 * g.ho && g.w == 2 * g.wo; }
+
+cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s, const EpiProg* pro, float* xo) {
   long long total = (long long)g.n * g.ho * g.wo * g.co;
+  EpiProg ep{};
+  if (pro && pro->n) {
+    if (!maxpool_fusable(g) || !xo) return cudaErrorInvalidValue;
+    ep = *pro;
+  }
   if (maxpool2_ok(g)) {
     const int pix = g.n * g.ho * g.wo;
-    if (g.co == 6) maxpool2_fwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, y, g, pix * 3);
-    else maxpool2_fwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, y, g, pix * 4);
+    if (g.co == 6) maxpool2_fwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, y, g, pix * 3, xo, ep);
+    else maxpool2_fwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, y, g, pix * 4, xo, ep);
     return cudaGetLastError();
   }
   if (g.co % 4 == 0 && total < INT32_MAX) {
@@ -809,11 +852,17 @@ cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s) {
+cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s,
+                               const EpiProg* epi) {
+  EpiProg ep{};
+  if (epi && epi->n) {
+    if (!maxpool_fusable(g)) return cudaErrorInvalidValue;
+    ep = *epi;
+  }
   if (maxpool2_ok(g)) {
     const int pix = g.n * g.ho * g.wo;
-    if (g.co == 6) maxpool2_bwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, dy, dx, g, pix * 3);
-    else maxpool2_bwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, dy, dx, g, pix * 4);
+    if (g.co == 6) maxpool2_bwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, dy, dx, g, pix * 3, ep);
+    else maxpool2_bwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, dy, dx, g, pix * 4, ep);
     return cudaGetLastError();
   }
   if (g.kh == g.sh && g.kw == g.sw && g.pt == 0 && g.pl == 0 && g.h == g.ho * g.sh && g.w == g.wo * g.sw) {

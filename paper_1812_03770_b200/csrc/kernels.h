@@ -35,8 +35,17 @@ cudaError_t launch_conv2d_bwd_input(const float* dy, const float* w, float* dx, 
 size_t conv2d_bwd_kernel_ws(const ConvGeom& g, int num_sms);
 cudaError_t launch_conv2d_bwd_kernel(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g,
                                      int num_sms, cudaStream_t s);
-cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s);
-cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s);
+struct EpiProg;
+// f2 pooling fusion (2 x 2 stride-2 pools over few channels, even H and W):
+// launch_maxpool with `pro` first computes its input from `x` by the fused
+// elementwise chain of the producing group (xo = pro(x), written in full) and pools
+// that; launch_maxpool_bwd with `epi` applies the consuming group's chain to every
+// gradient value before the store.  NULL / n == 0: the plain kernels.
+bool maxpool_fusable(const ConvGeom& g);
+cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s, const EpiProg* pro = nullptr,
+                           float* xo = nullptr);
+cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s,
+                               const EpiProg* epi = nullptr);
 cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s);
 
 constexpr int kMaxConcat = 16;

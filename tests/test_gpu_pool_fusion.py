@@ -1,0 +1,106 @@
+"""f2 fusion around C4's few-channel convolutions and 2x2 max pools (
+P:273 "reduce memory access").
+
+The executor computes an elementwise group inside a neighbouring kernel that is not
+a GEMM: the bias ADD in the tcgen05 conv epilogue (conv_img_tc), the RELU in the
+max pool that consumes it (a prologue: the pool reads the ADD's value, writes the
+RELU's and pools it), and RELU_GRAD in the max-pool backward kernel (an epilogue
+with a full-tensor operand, the forward pre-activation).  Each op keeps the
+generated kernels' IEEE per-op rounding, so the training trajectory must be
+BIT-IDENTICAL to the plan without these fusions, with six groups fewer launched.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from paper_1812_03770_b200 import cg
+from tests.test_gpu_fused_coll import _build, _run
+from workloads import configs
+
+pytestmark = pytest.mark.gpu
+
+
+def _build_env(spec, env, flags=0):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: v for k, v in env.items() if v is not None})
+    try:
+        return _build(spec, flags)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("batch,flags", [(128, 0), (96, cg.PLAN_FUSED_COLL), (8192, 0)])
+def test_c4_pool_and_conv_fusion_bit_identical(batch, flags):
+    spec = configs.c4(batch=batch)
+    iters = 2 if batch > 1000 else 4
+    g0, outs, info0 = _build_env(spec, {"CG_NO_POOL_FUSION": "1"}, flags)
+    h0, w0 = _run(spec, g0, outs, iters)
+    l0 = g0.launch_count()
+    g1, outs1, info1 = _build(spec, flags)
+    h1, w1 = _run(spec, g1, outs1, iters)
+    l1 = g1.launch_count()
+    for a, b in zip(h0, h1):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    for k in w0:
+        assert np.array_equal(w0[k], w1[k]), f"parameter {k}"
+    # conv1 / conv2 bias ADD, the two RELUs before the pools, the two RELU_GRADs after
+    # the pool backward passes
+    assert info1["n_fused"] - info0["n_fused"] == 6, (info0["n_fused"], info1["n_fused"])
+    assert info1["n_groups"] == info0["n_groups"]
+    assert l0 - l1 == 6 * iters, (l0, l1)
+    g0.destroy()
+    g1.destroy()
+
+
+def test_pool_prologue_with_operands_and_odd_sizes():
+    """A longer prologue chain (SUB scalar, MUL column, MAX2 full tensor, RELU) into a
+    2x2 pool and its backward with a RELU_GRAD epilogue, bit-equal to the unfused
+    plan; an odd-sized pool (skipped last row / column) is not fused."""
+    rng = np.random.default_rng(5)
+    for hw, fused in ((12, 2), (13, 0)):
+        x = rng.standard_normal((6, hw, hw, 16)).astype(np.float32)
+        m = rng.standard_normal((6, hw, hw, 16)).astype(np.float32)
+        colv = rng.standard_normal((16,)).astype(np.float32)
+        dyv = rng.standard_normal((6, hw // 2, hw // 2, 16)).astype(np.float32)
+        res = []
+        for env in ({"CG_NO_POOL_FUSION": "1"}, {}):
+            old = os.environ.pop("CG_NO_POOL_FUSION", None)
+            os.environ.update(env)
+            try:
+                g = cg.Graph(0)
+                vx, vm, vdy = g.var(x.shape), g.var(m.shape), g.var(dyv.shape)
+                vc = g.const(colv)
+                a = g.add_node("ADD", [vx, vm])  # the pre-activation (materialised: two consumers)
+                t = g.add_node("MUL", [g.add_node("SUB", [a, g.const(np.float32(0.25))]), vc])
+                h = g.add_node("RELU", [g.add_node("MAX2", [t, vm])])
+                p = g.add_node("MAXPOOL2D", [h], kh=2, kw=2, sh=2, sw=2, pad=0)
+                dh = g.add_node("MAXPOOL2D_BWD", [h, vdy], kh=2, kw=2, sh=2, sw=2, pad=0)
+                da = g.add_node("RELU_GRAD", [a, dh])
+                outs = [p, da]
+                info = g.plan_memory(outs)
+                for v, d in ((vx, x), (vm, m), (vdy, dyv)):
+                    g.assign(v, d)
+                g.eval(outs)
+                res.append(([g.read(o) for o in outs], info["n_fused"]))
+                g.destroy()
+            finally:
+                os.environ.pop("CG_NO_POOL_FUSION", None)
+                if old is not None:
+                    os.environ["CG_NO_POOL_FUSION"] = old
+        (r0, n0), (r1, n1) = res
+        for u, v in zip(r0, r1):
+            assert np.array_equal(u, v), hw
+        assert n1 - n0 == fused, (hw, n0, n1)
+        # and the values themselves (numpy, same per-op fp32 rounding)
+        a_ = x + m
+        h_ = np.maximum(np.maximum((a_ - np.float32(0.25)) * colv, m), 0)
+        n, H, W, C = h_.shape
+        ho, wo = H // 2, W // 2
+        win = h_[:, :2 * ho, :2 * wo].reshape(n, ho, 2, wo, 2, C)
+        assert np.array_equal(r1[0], win.max(axis=(2, 4)))
