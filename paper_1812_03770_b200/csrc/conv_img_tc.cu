@@ -45,9 +45,12 @@ namespace {
 
 #include "tc_prims.cuh"
 
+#ifndef CG_CI_NACC
+#define CG_CI_NACC 4
+#endif
 constexpr int CI_THREADS = 576;   // 18 warps
 constexpr int CI_L = 6;           // A stages in TMEM (64 columns each: 32 hi + 32 lo)
-constexpr int CI_NACC = 4;        // 16-column accumulators (more tiles between the MMA and the epilogue)
+constexpr int CI_NACC = CG_CI_NACC;  // 16-column accumulators (more tiles between the MMA and the epilogue)
 constexpr int CI_ACOL = 16 * CI_NACC;
 
 // Staged images for the small-image kernels: [HP][WPS][CIN] at XBASE + g * IMGF,
@@ -196,8 +199,9 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   auto tempty = [&](int b) { return bar0 + 8u * (4 + 2 * CI_L + CI_NACC + b); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 + 2 * CI_L + 2 * CI_NACC);
   // the fused chain's scalar / column operands, staged once: epx[e][co]
-  float* epx = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
-  static_assert((4 + 2 * CI_L + 2 * CI_NACC) * 8 + 4 <= 256, "barrier area");
+  float* epx = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
+  static_assert((4 + 2 * CI_L + 2 * CI_NACC) * 8 + 4 <= 512, "barrier area");
+  static_assert(CI_ACOL + CI_L * 64 <= 512, "TMEM columns");
 
   // role index through a shuffle: provably warp-uniform (convergent role branches)
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
@@ -248,6 +252,20 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // per-role cycle accounting of CTA 0 (diagnostics only: compiled in with
+  // -DCG_CI_TIMING -- the timers cost registers the roles need)
+  long long w_a = 0, w_b = 0, w_c = 0, w_d = 0, t_role = 0;
+#ifdef CG_CI_TIMING
+#define CI_TIMED(acc, call)          \
+  do {                               \
+    const long long t_ = clock64();  \
+    call;                            \
+    acc += clock64() - t_;           \
+  } while (0)
+  t_role = clock64();
+#else
+#define CI_TIMED(acc, call) call
+#endif
 
   if (warp < 8) {
     // ---------------- builders: A slab (128 pixels x 32 k) -> TMEM hi / lo columns
@@ -257,7 +275,7 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int b = j & 1;
       const int n0 = u * G, nimg = min(G, nimgs - n0);
-      mbar_wait(imgfull(b), (j >> 1) & 1);
+      CI_TIMED(w_a, mbar_wait(imgfull(b), (j >> 1) & 1));
       const float* img = imgs + b * buf_floats;
       for (int t = 0; t < T; ++t, it += NKB) {
         // this row's output pixel: image g, (oh, ow) (rows past the unit read image 0:
@@ -280,7 +298,14 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
               v[kl] = base[SG::tap(kh, kw, c)];
             }
           }
-          mbar_wait(lofree(l), ((step / CI_L) & 1) ^ 1);
+#ifdef CG_CI_EAGER
+          CI_TIMED(w_b, mbar_wait(lofree(l), ((step / CI_L) & 1) ^ 1));
+#else
+          CI_TIMED(w_b, mbar_wait_lazy(lofree(l), ((step / CI_L) & 1) ^ 1));  // (CI_L stages of slack)
+#endif
+#ifdef CG_CI_TIMING
+          const long long t_st = clock64();
+#endif
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ta = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(CI_ACOL + l * 64);
 #pragma unroll
@@ -298,6 +323,9 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+#ifdef CG_CI_TIMING
+          w_c += clock64() - t_st;
+#endif
           __syncwarp();
           if (lane == 0) mbar_arrive(conv(l));
         }
@@ -309,6 +337,15 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     // ---------------- epilogue: two groups of four warps (one per TMEM lane quadrant)
     // take alternate tiles; accumulator b = tile % CI_NACC always goes to group b % 2
     const int wq = warp % 4, rr = wq * 32 + lane, eg = (warp - 8) / 4;
+    // the chain's first op, hoisted out of the tile loop when its operand is a scalar
+    // or per-column vector (the usual bias ADD): code and values in registers, no
+    // per-tile parameter / shared-memory loads on the epilogue's critical path
+    const int n_epi = epi.n;
+    const bool hoist = n_epi >= 1 && epi.scalar[0] != 2;
+    const int code0 = hoist ? epi.op[0] : 0, sw0 = hoist ? epi.swap[0] : 0;
+    float x0[COUT];
+#pragma unroll
+    for (int i = 0; i < COUT; ++i) x0[i] = hoist ? epx[i] : 0.f;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int n0 = u * G, nimg = min(G, nimgs - n0);
@@ -320,22 +357,42 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
         float sum[16];
         {
           const int b = it % CI_NACC;
-          mbar_wait(tfull(b), (it / CI_NACC) & 1);
+          CI_TIMED(w_a, mbar_wait(tfull(b), (it / CI_NACC) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef CG_CI_TIMING
+          {
+            const long long t_ = clock64();
+            tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * 16), sum);
+            // (a branch on the result: the clock read waits for the load's data)
+            if (__float_as_uint(sum[0]) == 0x7fc01234u && __float_as_uint(sum[15]) == 0x7fc01234u) __trap();
+            w_b += clock64() - t_;
+          }
+#else
           tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * 16), sum);
+#endif
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty(b));
         }
         const int q = t * 128 + rr;
+#ifdef CG_CI_TIMING
+        const long long t_c = clock64();
+#endif
         if (q < nimg * P) {
-          float* o = out + ((size_t)n0 * P + q) * COUT;
-          if (epi.n) {  // fused elementwise chain (f2), op by op as the separate kernel
+          if (n_epi) {  // fused elementwise chain (f2), op by op as the separate kernel
             float v[COUT];
 #pragma unroll
             for (int i = 0; i < COUT; ++i) v[i] = sum[i];
+            if (hoist) {
+              if (code0 == EPI_ADD) {  // (the bias: no jump table)
+#pragma unroll
+                for (int i = 0; i < COUT; ++i) v[i] = __fadd_rn(v[i], x0[i]);
+              } else {
+                epi_apply<COUT>(v, code0, sw0, x0);
+              }
+            }
 #pragma unroll 1
-            for (int e = 0; e < epi.n; ++e) {
+            for (int e = hoist ? 1 : 0; e < n_epi; ++e) {
               float xe[COUT];
               if (epi.scalar[e] == 2) {  // full tensor: this pixel's COUT values
                 const float* src = epi.x[e] + ((size_t)n0 * P + q) * COUT;
@@ -350,18 +407,31 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < COUT; ++i) sum[i] = v[i];
           }
+        }
+#ifdef CG_CI_TIMING
+        const long long t_d = clock64();
+        w_c += t_d - t_c;
+#endif
+#if defined(CG_CI_NOSTORE)  // diagnostics only: wrong results
+        if (__float_as_uint(sum[0]) == 0x7fc01234u) out[0] = sum[1];
+#else
+        // (a shared-memory-staged, 16-byte coalesced variant of this store measured
+        // 111 -> 134 us on conv1: the direct per-row stores stay)
+        if (q < nimg * P) {
+          float* o = out + ((size_t)n0 * P + q) * COUT;
           if (COUT % 4 == 0) {
 #pragma unroll
             for (int i = 0; i < COUT; i += 4)
               *reinterpret_cast<float4*>(o + i) = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
-          } else if (COUT % 2 == 0) {
-#pragma unroll
-            for (int i = 0; i < COUT; i += 2) *reinterpret_cast<float2*>(o + i) = make_float2(sum[i], sum[i + 1]);
           } else {
 #pragma unroll
-            for (int i = 0; i < COUT; ++i) o[i] = sum[i];
+            for (int i = 0; i < COUT; i += 2) *reinterpret_cast<float2*>(o + i) = make_float2(sum[i], sum[i + 1]);
           }
         }
+#endif
+#ifdef CG_CI_TIMING
+        w_d += clock64() - t_d;
+#endif
       }
     }
   } else if (warp == 16) {
@@ -371,8 +441,8 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const int b = j & 1;
       const int n0 = u * G, nimg = min(G, nimgs - n0);
-      mbar_wait(imgfree(b), ((j >> 1) & 1) ^ 1);
-      stage_images<SG>(smem_u32(imgs + b * buf_floats), in, xmap_addr, n0, nimg, G, imgfull(b), lane);
+      CI_TIMED(w_a, mbar_wait_lazy(imgfree(b), ((j >> 1) & 1) ^ 1));
+      CI_TIMED(w_b, stage_images<SG>(smem_u32(imgs + b * buf_floats), in, xmap_addr, n0, nimg, G, imgfull(b), lane));
     }
   } else {
     // ---------------- warp 17: MMA issuer (whole warp walks the loop; one elected lane issues)
@@ -383,11 +453,11 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x)
       for (int t = 0; t < T; ++t, ++tile) {
         const int b = tile % CI_NACC;
-        mbar_wait_warp(tempty(b), ((tile / CI_NACC) & 1) ^ 1);  // the epilogue has read this accumulator
+        CI_TIMED(w_a, mbar_wait_warp(tempty(b), ((tile / CI_NACC) & 1) ^ 1));  // the epilogue has read this accumulator
         const uint32_t d = tm + (uint32_t)(b * 16);
         for (int kb = 0; kb < NKB; ++kb, ++it) {
           const int l = it % CI_L;
-          mbar_wait_warp(conv(l), (it / CI_L) & 1);
+          CI_TIMED(w_b, mbar_wait_warp(conv(l), (it / CI_L) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t ahi = tm + (uint32_t)(CI_ACOL + l * 64), alo = ahi + 32;
           const uint32_t bt = sbase + (uint32_t)(kb * 4096);
@@ -401,8 +471,19 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
           mma_commit_e<1>(lofree(l));
         }
         mma_commit_e<1>(tfull(b));
+#ifdef CG_CI_MMALAT  // diagnostics: serialise and time each tile's MMA execution
+        CI_TIMED(w_c, mbar_wait_warp(tfull(b), (tile / CI_NACC) & 1));
+#endif
       }
   }
+#ifdef CG_CI_TIMING
+  if (blockIdx.x == 0 && lane == 0)
+    printf("ci<%d,%d> warp %2d: busy %8lld  wait_a %8lld  wait_b %8lld  c %8lld  d %8lld (cycles)\n", CIN, COUT, warp,
+           clock64() - t_role, w_a, w_b, w_c, w_d);
+#else
+  (void)w_a; (void)w_b; (void)w_c; (void)w_d; (void)t_role;
+#endif
+#undef CI_TIMED
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 17) {
@@ -1132,7 +1213,7 @@ cudaError_t launch_geo(const float* in, const float* w, float* out, int n, const
     if (cost < best_cost) { best_cost = cost; best_g = G; }
   }
   const int G = best_g, T = (G * Geo::P + 127) / 128;
-  const size_t smem = 1024 + Geo::B_BYTES + 2 * buf_bytes(G) + 256 + kEpiMax * COUT * 4;
+  const size_t smem = 1024 + Geo::B_BYTES + 2 * buf_bytes(G) + 512 + kEpiMax * COUT * 4;
   CUtensorMap xmap;
   std::memset(&xmap, 0, sizeof(xmap));
   if (SG::TMAP && !make_img_map(&xmap, in, n, IH, IW, SG::WPS, SG::HP, G)) return cudaErrorInvalidValue;

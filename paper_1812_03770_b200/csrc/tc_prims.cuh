@@ -23,6 +23,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+#ifndef CG_LAZY_NS
+#define CG_LAZY_NS 128
+#endif
+// optional suspend-time hint (ns) for try_wait (A/B measurement only, see below)
+#ifdef CG_MBAR_HINT
+#define CG_MBAR_HINT_ARG ", %3"
+#define CG_MBAR_HINT_OP , "n"(CG_MBAR_HINT)
+#else
+#define CG_MBAR_HINT_ARG ""
+#define CG_MBAR_HINT_OP
+#endif
+
 // Blocking wait on an mbarrier phase (try_wait suspends briefly in hardware; an
 // explicit suspend-time hint compiled to NANOSLEEP.SYNCS and made waiters
 // oversleep the phase flip: measured 45 -> 63 ms on C5 with fused epilogues).
@@ -36,12 +48,31 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint64_t t0 = 0;
   while (true) {
     asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2" CG_MBAR_HINT_ARG ";\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity) CG_MBAR_HINT_OP
+        : "memory");
+    if (done) return;
+    // watchdog: a lost arrival must fail the launch (10 s), not hang the GPU
+    if (t0 == 0) t0 = globaltimer();
+    else if (globaltimer() - t0 > 10000000000ull) __trap();
+  }
+}
+
+// Wait for a role that is known to run ahead (its slack hides a late wake-up):
+// back off with nanosleep between polls, so a spinning warp does not take
+// shared-memory-pipe slots from the roles on the critical path.
+__device__ __forceinline__ void mbar_wait_lazy(uint32_t bar, uint32_t parity) {
+  uint64_t t0 = 0;
+  while (true) {
+    uint32_t done;
+    asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) return;
-    // watchdog: a lost arrival must fail the launch (10 s), not hang the GPU
+    __nanosleep(CG_LAZY_NS);
     if (t0 == 0) t0 = globaltimer();
     else if (globaltimer() - t0 > 10000000000ull) __trap();
   }
@@ -54,9 +85,9 @@ __device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
   while (true) {
     uint32_t done;
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2" CG_MBAR_HINT_ARG ";\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity) CG_MBAR_HINT_OP
         : "memory");
     if (__all_sync(0xffffffffu, done)) return;
     if (t0 == 0) t0 = globaltimer();
