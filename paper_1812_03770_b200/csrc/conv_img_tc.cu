@@ -163,6 +163,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 
+// issue only (the caller waits with tcgen05.wait::ld before reading r)
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -499,8 +507,14 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
 // from global memory, no im2col) -- then dx[h, w, ci] = sum over the in-bounds
 // taps (kh, kw ascending, fixed order: deterministic) of C[(h-kh+PT, w-kw+PL), (kh, kw, ci)]
 // from a shared-memory copy of C.  One 128-row tile = one image (HO*WO <= 128).
-// Warps 0-3 builders, 4-11 epilogue (TMEM -> smem, col2im sums), 12 MMA.
-constexpr int BI_THREADS = 416;
+// Warps 0-3 builders, 4-7 drain (TMEM -> one of two smem copies of C), 8..19
+// col2im (smem -> dx), 20 MMA, 21 producer (each image's dy, 6.4 KB contiguous, by
+// one TMA bulk copy into a BI_DS-slot ring): the drain of image i+1 overlaps the
+// col2im sums of image i (one group doing both in turn, with dy prefetched one
+// image ahead in registers, was latency-bound: 117 us on C4 conv2).
+constexpr int BI_CW = 12;               // col2im warps (588 (pixel, channel pair) items per C4 image)
+constexpr int BI_THREADS = (10 + BI_CW) * 32;
+constexpr int BI_DS = 4;                // dy ring slots
 constexpr int BI_L = 4;                 // A stages (32 TMEM columns: 16 hi + 16 lo)
 
 template <int CO, int KS, int HO, int WO, int H, int W, int PT, int PL, int CI>
@@ -514,6 +528,7 @@ struct BiGeo {
   static_assert(CI % 2 == 0, "col2im reads channel pairs");
   static constexpr int B_BYTES = NN * 128 * 2;           // hi + lo tiles, K-major SW128 (K padded to 32)
   static constexpr int C_FLOATS = 128 * CP;
+  static constexpr int DY_FLOATS = (P * CO + 31) / 32 * 32;  // one image of dy (128-byte slots)
   static constexpr int ACC = NN;                         // TMEM columns per accumulator
   static constexpr int ACOL = 2 * NN;                    // first A-stage column
   static_assert(P <= 128, "one image per tile");
@@ -532,14 +547,19 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
   // address space visible to the compiler: LDS/STS instead of generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
-  float* Cs = reinterpret_cast<float*>(smem + Geo::B_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Geo::B_BYTES + (size_t)Geo::C_FLOATS * 4);
+  float* Cs0 = reinterpret_cast<float*>(smem + Geo::B_BYTES);  // two copies of C: [2][128][CP]
+  float* dyr = Cs0 + 2 * Geo::C_FLOATS;                          // dy ring [BI_DS][DY_FLOATS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dyr + BI_DS * Geo::DY_FLOATS);
   const uint32_t bar0 = smem_u32(bars);
   auto conv = [&](int l) { return bar0 + 8u * l; };
   auto lofree = [&](int l) { return bar0 + 8u * (BI_L + l); };
   auto tfull = [&](int b) { return bar0 + 8u * (2 * BI_L + b); };
   auto tempty = [&](int b) { return bar0 + 8u * (2 * BI_L + 2 + b); };
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * BI_L + 4);
+  auto csfull = [&](int b) { return bar0 + 8u * (2 * BI_L + 4 + b); };
+  auto csfree = [&](int b) { return bar0 + 8u * (2 * BI_L + 6 + b); };
+  auto dyfull = [&](int k) { return bar0 + 8u * (2 * BI_L + 8 + k); };
+  auto dyfree = [&](int k) { return bar0 + 8u * (2 * BI_L + 8 + BI_DS + k); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * BI_L + 8 + 2 * BI_DS);
   const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;  // (warp-uniform)
 
   if (threadIdx.x == 0) {
@@ -549,7 +569,13 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), 8);  // the 8 epilogue warps
+      mbar_init(tempty(b), 4);  // the 4 drain warps
+      mbar_init(csfull(b), 4);  // the 4 drain warps
+      mbar_init(csfree(b), BI_CW);  // the col2im warps
+    }
+    for (int k = 0; k < BI_DS; ++k) {
+      mbar_init(dyfull(k), 1);  // the producer's arrive.expect_tx
+      mbar_init(dyfree(k), 4);  // the builder warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -563,7 +589,7 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
     *reinterpret_cast<float*>(smem + NN * 128 + off) = __fsub_rn(v, hi);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (warp == 12) {
+  if (warp == 8 + BI_CW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -571,30 +597,41 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  long long w_a = 0, w_b = 0, t_role = 0;
+#ifdef CG_BI_TIMING
+#define BI_TIMED(acc, call)          \
+  do {                               \
+    const long long t_ = clock64();  \
+    call;                            \
+    acc += clock64() - t_;           \
+  } while (0)
+  t_role = clock64();
+#else
+#define BI_TIMED(acc, call) call
+#endif
 
   if (warp < 4) {
-    // ---------------- builders: dy row q (16 channels, 64 B) -> TMEM hi / lo (next image prefetched)
+    // ---------------- builders: dy row q (16 channels, 64 B, from the ring) -> TMEM hi / lo
     const int rr = warp * 32 + lane;
     int it = 0;
-    float4 nx[4];
-    auto fetch = [&](int n, float4 (&v)[4]) {
-      if (n < nimgs && rr < P) {
-        const float4* src = reinterpret_cast<const float4*>(dy + ((size_t)n * P + rr) * CO);
+    for (int n = blockIdx.x; n < nimgs; n += gridDim.x, ++it) {
+      const int k = it % BI_DS;
+      BI_TIMED(w_a, mbar_wait(dyfull(k), (it / BI_DS) & 1));
+      float4 cur[4];
+      if (rr < P) {
+        const float4* src = reinterpret_cast<const float4*>(dyr + k * Geo::DY_FLOATS + rr * CO);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = __ldg(src + i);
+        for (int i = 0; i < 4; ++i) cur[i] = src[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < 4; ++i) cur[i] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
-    };
-    fetch(blockIdx.x, nx);
-    for (int n = blockIdx.x; n < nimgs; n += gridDim.x, ++it) {
-      float4 cur[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) cur[i] = nx[i];
-      fetch(n + gridDim.x, nx);
+      // (generic reads of the slot before the TMA refills it: proxy fence, then release)
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dyfree(k));
       const int l = it % BI_L;
-      mbar_wait(lofree(l), ((it / BI_L) & 1) ^ 1);
+      BI_TIMED(w_b, mbar_wait(lofree(l), ((it / BI_L) & 1) ^ 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t hv[16], lv[16];
 #pragma unroll
@@ -615,38 +652,56 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(conv(l));
     }
-  } else if (warp < 12) {
-    // ---------------- epilogue: C (TMEM) -> smem, then dx by fixed-order col2im sums
-    const int wq = warp % 4, half = (warp - 4) / 4;   // TMEM lane quadrant; column half
-    const int rr = wq * 32 + lane;
-    const int et = threadIdx.x - 128;                  // 0..255
+  } else if (warp < 8) {
+    // ---------------- drain: C (TMEM) -> smem copy it & 1 (all loads of a batch in flight)
+    const int wq = warp % 4, rr = wq * 32 + lane;  // TMEM lane quadrant
     int it = 0;
     for (int n = blockIdx.x; n < nimgs; n += gridDim.x, ++it) {
       const int b = it & 1;
-      mbar_wait(tfull(b), (it >> 1) & 1);
+      float* Cs = Cs0 + b * Geo::C_FLOATS;
+      BI_TIMED(w_a, mbar_wait(csfree(b), ((it >> 1) & 1) ^ 1));  // the col2im sums of image it - 2 are done
+      BI_TIMED(w_b, mbar_wait(tfull(b), (it >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // the previous image's col2im reads of Cs are done
-      constexpr int NCH = NN / 16, H0 = (NCH + 1) / 2;
-      for (int ch = half ? H0 : 0; ch < (half ? NCH : H0); ++ch) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * Geo::ACC + ch * 16), v);
+      constexpr int NCH = NN / 16, BATCH = 2;
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (ch * 16 + i < NJ) Cs[rr * CP + ch * 16 + i] = v[i];
+      for (int c0 = 0; c0 < NCH; c0 += BATCH) {
+        uint32_t r[BATCH][16];
+#pragma unroll
+        for (int c = 0; c < BATCH; ++c)
+          if (c0 + c < NCH) tmem_ld16_nowait(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(b * Geo::ACC + (c0 + c) * 16), r[c]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < BATCH; ++c)
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (c0 + c < NCH && (c0 + c) * 16 + i < NJ) Cs[rr * CP + (c0 + c) * 16 + i] = __uint_as_float(r[c][i]);
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty(b));
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // Cs complete
-      // one thread per dx pixel, all CI channels: 25 taps x CI/2 8-byte reads; each
-      // channel in two fixed-order partial sums (even / odd kh, kh and kw ascending)
-      // added at the end -- deterministic, and half the dependent-add chain length
+      if (lane == 0) {
+        mbar_arrive(tempty(b));
+        mbar_arrive(csfull(b));  // (release: the STS above are visible to the col2im warps)
+      }
+    }
+  } else if (warp < 8 + BI_CW) {
+    // ---------------- col2im: one thread per (dx pixel, channel pair) item: 25 taps x one
+    // 8-byte read; each channel in two fixed-order partial sums (even / odd kh, kh and
+    // kw ascending) added at the end -- deterministic, half the dependent-add chain
+    // (items, not pixels, per thread: every col2im warp has work; 117 -> 84 us with the
+    // drain / col2im split.  Loading all 25 taps before the sums measured slower.)
+    constexpr int NT = BI_CW * 32, CH2 = CI / 2;
+    const int et = threadIdx.x - 256;
+    int it = 0;
+    for (int n = blockIdx.x; n < nimgs; n += gridDim.x, ++it) {
+      const int b = it & 1;
+      const float* Cs = Cs0 + b * Geo::C_FLOATS;
+      BI_TIMED(w_a, mbar_wait(csfull(b), (it >> 1) & 1));
       float* o = dx + (size_t)n * H * W * CI;
-      for (int pix = et; pix < H * W; pix += 256) {
+      for (int item = et; item < H * W * CH2; item += NT) {
+        const int pix = item / CH2, cp = item - pix * CH2;
         const int h = pix / W, ww = pix - h * W;
-        float acc[2][CI];
-#pragma unroll
-        for (int i = 0; i < CI; ++i) acc[0][i] = acc[1][i] = 0.f;
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        const float* cbase = Cs + 2 * cp;
 #pragma unroll
         for (int kh = 0; kh < KS; ++kh) {
           const int oh = h - kh + PT;
@@ -655,33 +710,40 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
           for (int kw = 0; kw < KS; ++kw) {
             const int ow = ww - kw + PL;
             if (rok && (unsigned)ow < (unsigned)WO) {
-              const float2* c2 = reinterpret_cast<const float2*>(Cs + (oh * WO + ow) * CP + (kh * KS + kw) * CI);
-#pragma unroll
-              for (int i = 0; i < CI / 2; ++i) {
-                const float2 t = c2[i];
-                acc[kh & 1][2 * i] = __fadd_rn(acc[kh & 1][2 * i], t.x);
-                acc[kh & 1][2 * i + 1] = __fadd_rn(acc[kh & 1][2 * i + 1], t.y);
-              }
+              const float2 t = *reinterpret_cast<const float2*>(cbase + (oh * WO + ow) * CP + (kh * KS + kw) * CI);
+              acc[kh & 1].x = __fadd_rn(acc[kh & 1].x, t.x);
+              acc[kh & 1].y = __fadd_rn(acc[kh & 1].y, t.y);
             }
           }
         }
-#pragma unroll
-        for (int i = 0; i < CI; ++i) acc[0][i] = __fadd_rn(acc[0][i], acc[1][i]);
-        float (&acc0)[CI] = acc[0];
-        float2* o2 = reinterpret_cast<float2*>(o + (size_t)pix * CI);
-#pragma unroll
-        for (int i = 0; i < CI / 2; ++i) o2[i] = make_float2(acc0[2 * i], acc0[2 * i + 1]);
+        *reinterpret_cast<float2*>(o + (size_t)pix * CI + 2 * cp) =
+            make_float2(__fadd_rn(acc[0].x, acc[1].x), __fadd_rn(acc[0].y, acc[1].y));
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(csfree(b));
+    }
+  } else if (warp == 9 + BI_CW) {
+    // ---------------- producer: one bulk copy per image into the dy ring
+    int it = 0;
+    for (int n = blockIdx.x; n < nimgs; n += gridDim.x, ++it) {
+      const int k = it % BI_DS;
+      BI_TIMED(w_a, mbar_wait_lazy(dyfree(k), ((it / BI_DS) & 1) ^ 1));
+      if (lane == 0) {
+        constexpr uint32_t bytes = P * CO * 4;
+        mbar_expect_tx(dyfull(k), bytes);
+        bulk_g2s(smem_u32(dyr + k * Geo::DY_FLOATS), dy + (size_t)n * P * CO, bytes, dyfull(k));
+      }
+      __syncwarp();
     }
   } else {
-    // ---------------- warp 12: MMA issuer.  D f32, A / B tf32, both K-major, N = NN, M = 128
+    // ---------------- warp 8 + BI_CW: MMA issuer.  D f32, A / B tf32, both K-major, N = NN, M = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
     int it = 0;
     for (int n = blockIdx.x; n < nimgs; n += gridDim.x, ++it) {
       const int l = it % BI_L, b = it & 1;
-      mbar_wait_warp(tempty(b), ((it >> 1) & 1) ^ 1);
-      mbar_wait_warp(conv(l), (it / BI_L) & 1);
+      BI_TIMED(w_a, mbar_wait_warp(tempty(b), ((it >> 1) & 1) ^ 1));
+      BI_TIMED(w_b, mbar_wait_warp(conv(l), (it / BI_L) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t d = tm + (uint32_t)(b * Geo::ACC);
       const uint32_t ahi = tm + (uint32_t)(Geo::ACOL + l * 32), alo = ahi + 16;
@@ -696,9 +758,16 @@ __global__ void __launch_bounds__(BI_THREADS, 1)
       mma_commit_e<1>(tfull(b));
     }
   }
+#ifdef CG_BI_TIMING
+  if (blockIdx.x == 0 && lane == 0)
+    printf("bi warp %2d: busy %8lld  wait_a %8lld  wait_b %8lld (cycles)\n", warp, clock64() - t_role, w_a, w_b);
+#else
+  (void)w_a; (void)w_b; (void)t_role;
+#endif
+#undef BI_TIMED
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 12) {
+  if (warp == 8 + BI_CW) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
@@ -1184,7 +1253,9 @@ struct BkLaunch {
 template <int CO, int KS, int HO, int WO, int H, int W, int PT, int PL, int CI>
 cudaError_t launch_bwdin(const float* dy, const float* w, float* dx, int n, int num_sms, cudaStream_t s) {
   using Geo = BiGeo<CO, KS, HO, WO, H, W, PT, PL, CI>;
-  const size_t smem = 1024 + Geo::B_BYTES + (size_t)Geo::C_FLOATS * 4 + 256;
+  static_assert((Geo::P * CO * 4) % 16 == 0, "bulk copy size");
+  if (reinterpret_cast<uintptr_t>(dy) & 15) return cudaErrorMisalignedAddress;
+  const size_t smem = 1024 + Geo::B_BYTES + 2 * (size_t)Geo::C_FLOATS * 4 + BI_DS * (size_t)Geo::DY_FLOATS * 4 + 256;
   auto kern = conv_bwdin_col2im_kernel<CO, KS, HO, WO, H, W, PT, PL, CI>;
   cudaError_t e = smem_attr((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
