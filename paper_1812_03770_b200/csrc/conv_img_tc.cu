@@ -2012,6 +2012,147 @@ cudaError_t launch_conv_band(const float* x, const float* w, float* out, int ldc
   return launch_band<3, 3, 2, 299, 299, 149, 149, 32, 6>(x, w, out, ldc, n, epi, num_sms, s);
 }
 
+// ---------------------------------------------------------------- backward-kernel, one input channel: SIMT
+// dw[kh, kw, 0, co] = sum_{n,oh,ow} x[n, oh+kh-PT, ow+kw-PL] dy[n, oh, ow, co]  (stride 1, Ci = 1).
+// With KS*KS = 25 rows and COUT = 6 columns the tensor-core formulation (K = pixels)
+// fills a quarter of each MMA (block-diagonal tile) and was MMA-issue bound at
+// 140 us on C4 conv1; the FFMA form needs 25 x 6 x 2 flops per pixel (27 us of
+// FP32 issue at full rate).  Thread = (kh, 2 adjacent output pixels): 5 x COUT
+// accumulators per output pixel pair fed by 2 x COUT dy values and 6 x values
+// from shared memory (TMA-staged images, zero padded as the forward kernel's).
+// Warps: SB_KH groups of 4 (one kernel row each) + 1 producer.  Each thread's
+// partial sums are reduced in a fixed order per CTA, the per-CTA partials in a
+// fixed order by reduce_finalize: deterministic.
+constexpr int BS_GW = 4;  // warps per kernel-row group
+
+template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
+struct BsGeo {
+  using SG = StageGeo<1, KS, IH, IW, OH, OW, PT, PL>;
+  static constexpr int P = OH * OW, PP = P / 2;           // pixels, pixel pairs per image
+  static constexpr int DYF = P * COUT;                    // dy floats per image
+  static constexpr int G = 4;                             // images per stage
+  static constexpr int XBUF = (SG::XBASE + G * SG::IMGF + 31) / 32 * 32;
+  static constexpr int THREADS = (KS * BS_GW + 1) * 32;
+  static_assert(OW % 2 == 0, "pixel pairs within a row");
+  static_assert((DYF * 4) % 16 == 0 && (COUT * 2) % 4 == 0, "16-byte dy copies / pair loads");
+};
+
+template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
+__global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREADS, 1)
+    conv_bwdk_simt_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ ws, int nimgs,
+                          const __grid_constant__ CUtensorMap xmap) {
+  using Geo = BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>;
+  using SG = typename Geo::SG;
+  constexpr int G = Geo::G, PP = Geo::PP, DYF = Geo::DYF, NT = BS_GW * 32;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* xs = reinterpret_cast<float*>(smem);                 // [2][XBUF]
+  float* dys = xs + 2 * Geo::XBUF;                             // [2][G * DYF]
+  float* red = dys + 2 * G * DYF;                              // [KS][NT] reduction scratch
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + KS * NT);
+  const uint32_t bar0 = smem_u32(bars);
+  auto full = [&](int b) { return bar0 + 8u * b; };
+  auto freeb = [&](int b) { return bar0 + 8u * (2 + b); };
+  const int warp = __shfl_sync(0xffffffffu, (int)threadIdx.x / 32, 0), lane = threadIdx.x % 32;
+  const int units = (nimgs + G - 1) / G;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(full(b), 1);
+      mbar_init(freeb(b), KS * BS_GW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int e = threadIdx.x; e < 2 * Geo::XBUF; e += blockDim.x) xs[e] = 0.f;  // padding / guard stays zero
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  if (warp == KS * BS_GW) {
+    // ---------------- producer: G images of x (3-D tensor map, zero padded) and of dy per stage
+    const uint64_t xmap_addr = reinterpret_cast<uint64_t>(&xmap);
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const int b = j & 1, n0 = u * G, nimg = min(G, nimgs - n0);
+      mbar_wait_lazy(freeb(b), ((j >> 1) & 1) ^ 1);
+      if (lane == 0) {
+        // (no arrive here: stage_images' arrive.expect_tx below completes the phase's count)
+        mbar_expect_tx_only(full(b), (uint32_t)(nimg * DYF * 4));
+        bulk_g2s(smem_u32(dys + b * G * DYF), dy + (size_t)n0 * DYF, (uint32_t)(nimg * DYF * 4), full(b));
+      }
+      stage_images<SG>(smem_u32(xs + b * Geo::XBUF), x, xmap_addr, n0, nimg, G, full(b), lane);
+    }
+    return;
+  }
+  // ---------------- compute: kernel row kh, pixel pairs t, t + NT, ... of each stage
+  const int kh = warp / BS_GW, t = threadIdx.x - kh * NT;
+  float acc[KS][COUT];
+#pragma unroll
+  for (int a = 0; a < KS; ++a)
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) acc[a][c] = 0.f;
+  int j = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+    const int b = j & 1, n0 = u * G, nimg = min(G, nimgs - n0);
+    mbar_wait(full(b), (j >> 1) & 1);
+    const float* xb = xs + b * Geo::XBUF;
+    const float* db = dys + b * G * DYF;
+    for (int q = t; q < nimg * PP; q += NT) {
+      const int g = q / PP, pp = q - g * PP, oh = pp / (OW / 2), ow = (pp - oh * (OW / 2)) * 2;
+      float d0[COUT], d1[COUT];
+      const float* dp = db + (g * Geo::P + oh * OW + ow) * COUT;
+#pragma unroll
+      for (int c = 0; c < COUT; c += 2) {
+        const float2 v0 = *reinterpret_cast<const float2*>(dp + c), v1 = *reinterpret_cast<const float2*>(dp + COUT + c);
+        d0[c] = v0.x; d0[c + 1] = v0.y; d1[c] = v1.x; d1[c + 1] = v1.y;
+      }
+      const float* xp = xb + SG::window(g, oh, ow) + SG::tap(kh, 0, 0);
+      float xv[KS + 1];
+#pragma unroll
+      for (int a = 0; a < KS + 1; ++a) xv[a] = xp[a];
+#pragma unroll
+      for (int a = 0; a < KS; ++a)
+#pragma unroll
+        for (int c = 0; c < COUT; ++c) acc[a][c] = fmaf(xv[a + 1], d1[c], fmaf(xv[a], d0[c], acc[a][c]));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(freeb(b));
+  }
+  // ---------------- fixed-order reduction over the NT threads of the row group
+  asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
+#pragma unroll
+  for (int a = 0; a < KS; ++a)
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) {  // (unrolled: acc stays in registers)
+      red[kh * NT + t] = acc[a][c];
+      asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
+      for (int h = NT / 2; h > 0; h >>= 1) {
+        if (t < h) red[kh * NT + t] = red[kh * NT + t] + red[kh * NT + t + h];
+        asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
+      }
+      if (t == 0) ws[(size_t)blockIdx.x * KS * KS * COUT + (kh * KS + a) * COUT + c] = red[kh * NT];
+      asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
+    }
+}
+
+template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
+cudaError_t launch_bwdk_simt(const float* x, const float* dy, float* dw, float* ws, int n, int num_sms, cudaStream_t s) {
+  using Geo = BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>;
+  using SG = typename Geo::SG;
+  static_assert(SG::TMAP, "zero padding from the tensor map's out-of-bounds fill");
+  if ((reinterpret_cast<uintptr_t>(dy) & 15) || (reinterpret_cast<uintptr_t>(x) & 15)) return cudaErrorMisalignedAddress;
+  CUtensorMap xmap;
+  std::memset(&xmap, 0, sizeof(xmap));
+  if (!make_img_map(&xmap, x, n, IH, IW, SG::WPS, SG::HP, Geo::G)) return cudaErrorInvalidValue;
+  const size_t smem = 1024 + (2 * (size_t)Geo::XBUF + 2 * (size_t)Geo::G * Geo::DYF + KS * BS_GW * 32) * 4 + 64;
+  auto kern = conv_bwdk_simt_kernel<KS, IH, IW, OH, OW, PT, PL, COUT>;
+  cudaError_t e = smem_attr((const void*)kern, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = std::max(1, std::min(n, num_sms));
+  kern<<<grid, Geo::THREADS, smem, s>>>(x, dy, ws, n, xmap);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_reduce_finalize(ws, dw, (long long)KS * KS * COUT, grid, 0, s);
+}
+
 bool conv_img_tc_bwdk_supported(const ConvGeom& g) {
   return kind_of(g, false) != CI_NONE && !getenv("CG_NO_CONV_IMG_TC");
 }
@@ -2024,7 +2165,9 @@ cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, 
                                     cudaStream_t s) {
   switch (kind_of(g, false)) {
     case CI_C4_CONV1:  // x [n,28,28,1], dy [n,28,28,6] -> dw [5,5,1,6] (SAME)
-      return BkLaunch<1, 5, 28, 28, 28, 28, 2, 2, 6>::run(x, dy, dw, ws, g.n, num_sms, s);
+      if (getenv("CG_BWDK_TC1"))  // (A/B: the tensor-core K = pixels formulation)
+        return BkLaunch<1, 5, 28, 28, 28, 28, 2, 2, 6>::run(x, dy, dw, ws, g.n, num_sms, s);
+      return launch_bwdk_simt<5, 28, 28, 28, 28, 2, 2, 6>(x, dy, dw, ws, g.n, num_sms, s);
     case CI_C4_CONV2:  // x [n,14,14,6], dy [n,10,10,16] -> dw [5,5,6,16] (VALID)
       return BkLaunch<6, 5, 14, 14, 10, 10, 0, 0, 16>::run(x, dy, dw, ws, g.n, num_sms, s);
     default:
