@@ -446,7 +446,9 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (int i = threadIdx.x - 192; i < epi.n * BN; i += 128) {
           const int e = i / BN, c = i - e * BN, col = n0 + c;
-          es[i] = epi.op[e] == EPI_RELU ? 0.f : (epi.scalar[e] ? __ldg(epi.x[e]) : (col < N ? __ldg(epi.x[e] + col) : 0.f));
+          es[i] = epi.op[e] == EPI_RELU || epi.scalar[e] == 2
+                      ? 0.f
+                      : (epi.scalar[e] ? __ldg(epi.x[e]) : (col < N ? __ldg(epi.x[e] + col) : 0.f));
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
@@ -466,7 +468,26 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           float vv[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) vv[q] = __uint_as_float(r[q]);
-          for (int e = 0; e < epi.n; ++e) epi_apply<16>(vv, epi.op[e], epi.swap[e], es + e * BN);
+          for (int e = 0; e < epi.n; ++e) {
+            if (epi.scalar[e] == 2) {  // a full [M, N] operand (row-major, ld = N): this row's 16 values
+              float xe[16];
+              const int n = n0 + c0;
+              const float* xr = epi.x[e] + (size_t)min(row, M - 1) * N + n;
+              if ((N % 4) == 0 && n + 16 <= N && (reinterpret_cast<uintptr_t>(epi.x[e]) & 15) == 0) {
+#pragma unroll
+                for (int q = 0; q < 16; q += 4) {
+                  const float4 t = __ldg(reinterpret_cast<const float4*>(xr + q));
+                  xe[q] = t.x; xe[q + 1] = t.y; xe[q + 2] = t.z; xe[q + 3] = t.w;
+                }
+              } else {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) xe[q] = n + q < N ? __ldg(xr + q) : 0.f;
+              }
+              epi_apply<16>(vv, epi.op[e], epi.swap[e], xe);
+            } else {
+              epi_apply<16>(vv, epi.op[e], epi.swap[e], es + e * BN);
+            }
+          }
 #pragma unroll
           for (int q = 0; q < 16; ++q) r[q] = __float_as_uint(vv[q]);
         }

@@ -527,7 +527,10 @@ static void fuse_epilogues(cg_graph* g) {
     const Group& E = hg.groups[ge];
     if (E.kind != G_EW || E.materialised.size() != 1 || E.domain != hg.nodes[d].shape || g->partner[ge] >= 0) continue;
     EpiProg prog;
-    if (!build_chain(E, d, hg.nodes[d].shape, slot, (int)gd, prog)) continue;
+    // full-tensor operands: the slot kernels and the GEMM epilogue (gemm_tc_kernel reads
+    // them at [row, col] with ld = N); not the band / row-ring conv kernels
+    const bool full = slot || (tc && plan->band == 0 && !no_slot);
+    if (!build_chain(E, d, hg.nodes[d].shape, full, (int)gd, prog)) continue;
     if (slot && is_view(E.sink)) continue;  // (only the GEMM epilogue stores strided slices)
     // The fused kernel writes the sink's block at gd's position in Gamma, while the
     // plan gives that block to the sink only at ge's: unless the sink slid into d's

@@ -1,4 +1,5 @@
-"""f2 fusion around C4's few-channel convolutions and 2x2 max pools (
+"""f2 fusion around C4's few-channel convolutions and 2x2 max pools, and full-tensor
+operands in the GEMM epilogue (
 P:273 "reduce memory access").
 
 The executor computes an elementwise group inside a neighbouring kernel that is not
@@ -50,10 +51,12 @@ def test_c4_pool_and_conv_fusion_bit_identical(batch, flags):
     for k in w0:
         assert np.array_equal(w0[k], w1[k]), f"parameter {k}"
     # conv1 / conv2 bias ADD, the two RELUs before the pools, the two RELU_GRADs after
-    # the pool backward passes
-    assert info1["n_fused"] - info0["n_fused"] == 6, (info0["n_fused"], info1["n_fused"])
+    # the pool backward passes, and RELU_GRAD(a3, dh3) in the dh3 GEMM's epilogue
+    # (a full-tensor operand)
+    nf = info1["n_fused"] - info0["n_fused"]
+    assert nf == 7, (info0["n_fused"], info1["n_fused"])
     assert info1["n_groups"] == info0["n_groups"]
-    assert l0 - l1 == 6 * iters, (l0, l1)
+    assert l0 - l1 == nf * iters, (l0, l1)
     g0.destroy()
     g1.destroy()
 
@@ -104,3 +107,23 @@ def test_pool_prologue_with_operands_and_odd_sizes():
         ho, wo = H // 2, W // 2
         win = h_[:, :2 * ho, :2 * wo].reshape(n, ho, 2, wo, 2, C)
         assert np.array_equal(r1[0], win.max(axis=(2, 4)))
+
+
+def test_c3_relu_grad_in_gemm_epilogue_bit_identical():
+    """C3's backward: dh_k = da_{k+1} . W^T feeds only RELU_GRAD(a_k, dh_k); a
+    tensor-core GEMM's epilogue applies it with a_k read at [row, col] (a full-tensor
+    operand), so dh_k never reaches HBM -- same values as the separate kernel."""
+    spec = configs.c3(batch=512, widths=(784, 256, 128, 10))
+    g0, outs, info0 = _build_env(spec, {"CG_NO_POOL_FUSION": "1"})
+    h0, w0 = _run(spec, g0, outs, 4)
+    g1, outs1, info1 = _build(spec)
+    h1, w1 = _run(spec, g1, outs1, 4)
+    for a, b in zip(h0, h1):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    for k in w0:
+        assert np.array_equal(w0[k], w1[k]), f"parameter {k}"
+    # dh1 (a tensor-core GEMM) takes it; dh2 = dL . W3^T (K = 10) is a SIMT small-K dot
+    assert info1["n_fused"] - info0["n_fused"] == 1, (info0["n_fused"], info1["n_fused"])
+    g0.destroy()
+    g1.destroy()
