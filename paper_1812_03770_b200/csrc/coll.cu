@@ -67,26 +67,72 @@ __global__ void __launch_bounds__(256) fused_allreduce_kernel(const __grid_const
       for (int r = 0; r < P; ++r) wait_ge(my + r, e);
     __syncthreads();
   }
-  const CollSeg& sg = a.segs[blockIdx.y];
+  // this segment's descriptor and update chain, staged once per block (read per
+  // element from the global table, the chain's fields were a chain of dependent
+  // loads per op per element: C3's update 22.6 us for 7.4 MB of gradients)
+  __shared__ CollSeg sseg;
+  if (threadIdx.x == 0) sseg = a.segs[blockIdx.y];
+  __syncthreads();
+  const CollSeg& sg = sseg;
+  const bool ncol32 = sg.ncol < (1ll << 31) && sg.n < (1ll << 31);
   const float* g[kCollMaxRanks];
 #pragma unroll
   for (int r = 0; r < kCollMaxRanks; ++r) g[r] = r < P ? a.base[r] + sg.goff : nullptr;
   const long long stride = (long long)gridDim.x * blockDim.x;
   if (sg.vec) {
+    // CU float4 vectors per thread per iteration (grid-stride, coalesced), every load
+    // of a step issued before its arithmetic: the gradient vectors, then per chain op
+    // its operand vectors (a full-tensor operand such as W in W - lr * g) -- one HBM
+    // latency per step for all of them (one vector at a time was two serialised
+    // latencies per vector: C3's update 13 -> ~4 us)
+    constexpr int CU = 4;
     const long long n4 = sg.n >> 2;
-    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += stride) {
-      float4 s = reinterpret_cast<const float4*>(g[0])[j];
+    for (long long j0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; j0 < n4; j0 += CU * stride) {
+      float v[CU][4];
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const long long j = j0 + u * stride;
+        float4 t = j < n4 ? reinterpret_cast<const float4*>(g[0])[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[u][0] = t.x; v[u][1] = t.y; v[u][2] = t.z; v[u][3] = t.w;
+      }
 #pragma unroll 1
       for (int r = 1; r < P; ++r) {  // rank order: identical on every rank
-        const float4 t = reinterpret_cast<const float4*>(g[r])[j];
-        s.x = __fadd_rn(s.x, t.x); s.y = __fadd_rn(s.y, t.y); s.z = __fadd_rn(s.z, t.z); s.w = __fadd_rn(s.w, t.w);
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const long long j = j0 + u * stride;
+          if (j >= n4) continue;
+          const float4 t = reinterpret_cast<const float4*>(g[r])[j];
+          v[u][0] = __fadd_rn(v[u][0], t.x); v[u][1] = __fadd_rn(v[u][1], t.y);
+          v[u][2] = __fadd_rn(v[u][2], t.z); v[u][3] = __fadd_rn(v[u][3], t.w);
+        }
       }
-      const long long i = j * 4;
-      s.x = apply_chain(sg.epi, s.x, i, sg.ncol);
-      s.y = apply_chain(sg.epi, s.y, i + 1, sg.ncol);
-      s.z = apply_chain(sg.epi, s.z, i + 2, sg.ncol);
-      s.w = apply_chain(sg.epi, s.w, i + 3, sg.ncol);
-      reinterpret_cast<float4*>(sg.out)[j] = s;
+#pragma unroll 1
+      for (int e = 0; e < sg.epi.n; ++e) {
+        const int op = sg.epi.op[e], sc = sg.epi.scalar[e], sw = sg.epi.swap[e];
+        const float* x = sg.epi.x[e];
+        float xe[CU][4];
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {  // (vec: a float4 never straddles a row, coll_seg_vec_ok)
+          const long long j = j0 + u * stride;
+          const long long i = j * 4;
+          if (op == EPI_RELU || j >= n4) {
+            xe[u][0] = xe[u][1] = xe[u][2] = xe[u][3] = 0.f;
+          } else if (sc == 1) {
+            xe[u][0] = xe[u][1] = xe[u][2] = xe[u][3] = __ldg(x);
+          } else {
+            const long long off = sc == 2 ? i : ncol32 ? (long long)((unsigned)i % (unsigned)sg.ncol) : i % sg.ncol;
+            const float4 t = __ldg(reinterpret_cast<const float4*>(x + off));
+            xe[u][0] = t.x; xe[u][1] = t.y; xe[u][2] = t.z; xe[u][3] = t.w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < CU; ++u) epi_apply<4>(v[u], op, sw, xe[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < CU; ++u) {
+        const long long j = j0 + u * stride;
+        if (j < n4) reinterpret_cast<float4*>(sg.out)[j] = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+      }
     }
   } else {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < sg.n; i += stride) {
@@ -124,8 +170,11 @@ __global__ void __launch_bounds__(256) fused_allreduce_kernel(const __grid_const
 bool coll_seg_vec_ok(const CollSeg& s, const float* const* base, int nranks) {
   bool vec = (s.n & 3) == 0 && (reinterpret_cast<uintptr_t>(s.out) & 15) == 0 && (s.goff & 3) == 0;
   for (int r = 0; r < nranks; ++r) vec = vec && (reinterpret_cast<uintptr_t>(base[r]) & 15) == 0;
-  for (int e = 0; e < s.epi.n; ++e)  // full-tensor operands are read per element (any alignment)
-    (void)e;
+  for (int e = 0; e < s.epi.n; ++e) {  // vector operands: 16-byte loads; a column float4 within one row
+    if (s.epi.op[e] == EPI_RELU || s.epi.scalar[e] == 1) continue;
+    vec = vec && (reinterpret_cast<uintptr_t>(s.epi.x[e]) & 15) == 0;
+    if (s.epi.scalar[e] == 0) vec = vec && (s.ncol & 3) == 0;
+  }
   return vec;
 }
 

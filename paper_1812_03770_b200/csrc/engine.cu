@@ -1102,7 +1102,8 @@ static int build_launches(cg_graph* g) {
     for (size_t gi = 0; gi < NG; ++gi) {
       CollSeg& cs = g->collseg[gi];
       if (cs.n == 0) continue;
-      cs.vec = (cs.n & 3) == 0 && (reinterpret_cast<uintptr_t>(cs.out) & 15) == 0 && (cs.goff & 3) == 0;
+      const float* pb = reinterpret_cast<const float*>(g->pool);  // (peer pools: cudaMalloc-aligned too)
+      cs.vec = coll_seg_vec_ok(cs, &pb, 1);
       g->coll_entry[gi] = (int)tab.size();
       tab.push_back(cs);
     }
