@@ -3,9 +3,9 @@
 // A correlation of a stride-1 KS x KS kernel over small images (C4's LeNet
 // layers: 28x28x1 -> 6, 14x14x6 -> 16, and the 16 -> 6 backward-input pass) is an
 // implicit GEMM   out[q, n] = sum_k A[q, k] B[k, n]   with q = output pixel,
-// k = (c, kh, kw) and n = output channel (<= 16).  The im2col operand A is never
-// materialised: whole images are staged in shared memory (channel-planar, so
-// adjacent pixels are adjacent words) and builder warps form each 128-pixel x
+// k = (kh, kw, c) and n = output channel (<= 16).  The im2col operand A is never
+// materialised: whole images are staged in shared memory (NHWC as in HBM, zero
+// padded for SAME) and builder warps form each 128-pixel x
 // 32-k slab from them with compile-time offsets (the geometry is a template),
 // split it into TF32 hi/lo and write it to TENSOR MEMORY; the MMAs
 // (tcgen05.mma.kind::tf32, M = 128, N = 16) take A from TMEM and B (the weights,
@@ -231,12 +231,12 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // B (weights) for every k-block, split once: K-major SWIZZLE_128B tiles of 16 rows
-  // (n) x 32 k; 16-byte chunk c of row n at chunk c ^ (n & 7).  k = (c, kh, kw).
+  // (n) x 32 k; 16-byte chunk c of row n at chunk c ^ (n & 7).  k = (kh, kw, c).
   for (int e = threadIdx.x; e < NKB * 16 * 32; e += blockDim.x) {
     const int kb = e / 512, rem = e % 512, n = rem / 32, kl = rem % 32, k = kb * 32 + kl;
     float v = 0.f;
     if (k < K && n < COUT) {
-      const int c = k / (KS * KS), t = k % (KS * KS), kh = t / KS, kw = t % KS;
+      const int c = k % CIN, t = k / CIN, kh = t / KS, kw = t % KS;
       v = __ldg(w + ((size_t)(kh * KS + kw) * CIN + c) * COUT + n);  // w [KS][KS][CIN][COUT]
     }
     const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
@@ -297,13 +297,32 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
           if ((step & 1) != grp) continue;
           const int l = step % CI_L;
           float v[32];
+          if constexpr (CIN % 2 == 0) {
+            static_assert(SG::XBASE % 2 == 0 && SG::IMGF % 2 == 0, "8-byte pair loads");
+            // k = (kh, kw, c): a pair (k, k + 1), k even, is channels (c, c + 1) of one
+            // tap -- one 8-byte load (a 6-word lane stride hits 16 distinct bank pairs
+            // per half warp: conflict-free; the channel-major order took 32 two-way
+            // conflicted 4-byte loads per slab)
 #pragma unroll
-          for (int kl = 0; kl < 32; ++kl) {
-            const int k = kb * 32 + kl;
-            v[kl] = 0.f;
-            if (k < K) {
-              const int c = k / (KS * KS), tt = k % (KS * KS), kh = tt / KS, kw = tt % KS;
-              v[kl] = base[SG::tap(kh, kw, c)];
+            for (int kl = 0; kl < 32; kl += 2) {
+              const int k = kb * 32 + kl;
+              v[kl] = v[kl + 1] = 0.f;
+              if (k < K) {
+                const int c = k % CIN, tt = k / CIN, kh = tt / KS, kw = tt % KS;
+                const float2 t = *reinterpret_cast<const float2*>(base + SG::tap(kh, kw, c));
+                v[kl] = t.x;
+                v[kl + 1] = t.y;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int kl = 0; kl < 32; ++kl) {
+              const int k = kb * 32 + kl;
+              v[kl] = 0.f;
+              if (k < K) {
+                const int c = k % CIN, tt = k / CIN, kh = tt / KS, kw = tt % KS;
+                v[kl] = base[SG::tap(kh, kw, c)];
+              }
             }
           }
 #ifdef CG_CI_EAGER

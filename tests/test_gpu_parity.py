@@ -620,8 +620,9 @@ def _teacher_forced(spec, iters, tol, rewrites=0):
     spec = dict(spec)
     # pinned: pre-activations (ReLU decisions) and the gradients entering the
     # optimiser (AdaGrad's lr*g/(sqrt(s)+eps) is a sign-like map of tiny g)
-    zs = [n["preds"][0] for n in spec["nodes"] if n["op"] == "RELU"]
-    zs += [n["id"] for n in spec["nodes"] if n["op"] == "ALLREDUCE_SUM"]
+    pre = [n["preds"][0] for n in spec["nodes"] if n["op"] == "RELU"]
+    grads = [n["id"] for n in spec["nodes"] if n["op"] == "ALLREDUCE_SUM"]
+    zs = pre + grads
     spec["outputs"] = list(spec["outputs"]) + zs
     g, outs, _, _ = gpu_graph(spec, 0, rewrites=rewrites)
     og, oo = from_spec(spec)
@@ -641,7 +642,14 @@ def _teacher_forced(spec, iters, tol, rewrites=0):
         free = evaluate(og, state, needed)
         gz = {z: g.read(z) for z in zs}
         pinned = evaluate_pinned(og, state, gz, needed)
-        errs = [normwise(gz[z], free[z]) for z in zs]
+        # the gradients against the oracle pinned at the pre-activations only: every
+        # ReLU mask and max-pool argmax (taken on relu(pre-activation)) is then the
+        # GPU's, as this test's reading intends (compared with the free oracle, one
+        # argmax within rounding of a tie moved a whole window's gradient: C4 batch
+        # 64, iteration 1, after the conv2 kernel's k order changed)
+        pinned_pre = evaluate_pinned(og, state, {z: gz[z] for z in pre}, needed)
+        errs = [normwise(gz[z], free[z]) for z in pre]
+        errs += [normwise(gz[z], pinned_pre[z]) for z in grads]
         errs += [normwise(g.read(o), pinned[o]) for o in oo if o not in gz]
         nxt = dict(state)
         apply_updates(og, pinned, nxt)
