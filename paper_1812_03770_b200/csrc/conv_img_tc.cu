@@ -442,8 +442,9 @@ __global__ void __launch_bounds__(CI_THREADS, 1)
 #if defined(CG_CI_NOSTORE)  // diagnostics only: wrong results
         if (__float_as_uint(sum[0]) == 0x7fc01234u) out[0] = sum[1];
 #else
-        // (a shared-memory-staged, 16-byte coalesced variant of this store measured
-        // 111 -> 134 us on conv1: the direct per-row stores stay)
+        // (measured slower on conv1: a shared-memory-staged variant with 16-byte
+        // coalesced stores, 111 -> 134 us, and one TMA bulk store per tile from
+        // double-buffered staging, 112 -> 122 us; the direct per-row stores stay)
         if (q < nimg * P) {
           float* o = out + ((size_t)n0 * P + q) * COUT;
           if (COUT % 4 == 0) {
