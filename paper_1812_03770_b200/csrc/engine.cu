@@ -315,8 +315,13 @@ struct cg_graph {
     float* out = nullptr;
     const float* in = nullptr;
     float* xo = nullptr;
+    unsigned char* codes = nullptr;  // 2x2 max pool: the forward's recorded window decisions
   };
   std::vector<std::shared_ptr<EpiSlot>> eslot;
+  // max-pool backward group -> the forward pool group whose decisions it reads (-1:
+  // none); demanding the backward demands the forward (its codes must be current)
+  std::vector<int> code_dep;
+  std::vector<void*> code_bufs;
   // f3 fused AllReduce + update over peer memory (CG_PLAN_FUSED_COLL): per
   // ALLREDUCE group its segment (n == 0: none); device table = one entry per group
   // followed by the batched steps of a full evaluation (contiguous per step)
@@ -902,7 +907,10 @@ static int build_launches(cg_graph* g) {
           auto sl = std::make_shared<cg_graph::EpiSlot>();
           sl->in = x;
           g->eslot[gi] = sl;
-          L.push_back({[sl, out, cgm](cudaStream_t s) { return launch_maxpool(sl->in, out, cgm, s, &sl->epi, sl->xo); }, 1});
+          L.push_back({[sl, out, cgm](cudaStream_t s) {
+                         return launch_maxpool(sl->in, out, cgm, s, &sl->epi, sl->xo, sl->codes);
+                       },
+                       1});
           break;
         }
         L.push_back({[x, out, cgm, mx](cudaStream_t s) { return mx ? launch_maxpool(x, out, cgm, s) : launch_avgpool(x, out, cgm, s); },
@@ -916,7 +924,10 @@ static int build_launches(cg_graph* g) {
           auto sl = std::make_shared<cg_graph::EpiSlot>();
           sl->out = out;
           g->eslot[gi] = sl;
-          L.push_back({[x, dy, sl, cgm](cudaStream_t s) { return launch_maxpool_bwd(x, dy, sl->out, cgm, s, &sl->epi); }, 1});
+          L.push_back({[x, dy, sl, cgm](cudaStream_t s) {
+                         return launch_maxpool_bwd(x, dy, sl->out, cgm, s, &sl->epi, sl->codes);
+                       },
+                       1});
           break;
         }
         L.push_back({[x, dy, out, cgm](cudaStream_t s) { return launch_maxpool_bwd(x, dy, out, cgm, s); }, 1});
@@ -957,6 +968,35 @@ static int build_launches(cg_graph* g) {
       g->glaunch[gi].push_back(slice_copy(pending_copy[gi]));
       g->n_views_copied++;
     }
+  // 2x2 max pools: the backward reads the forward's window decisions (one byte per
+  // output element) instead of the input's four window values (C4: 154 MB -> 9.6 MB
+  // per backward); single-stream capture only (the codes are not a pool block the
+  // concurrent schedule orders)
+  g->code_dep.assign(hg.groups.size(), -1);
+  {
+    const char* ns_env = getenv("CG_STREAMS");
+    const bool one_stream = !ns_env || atoi(ns_env) <= 1;
+    for (size_t gb = 0; gb < hg.groups.size() && one_stream && !getenv("CG_NO_POOL_CODES"); ++gb) {
+      const Node& bn = hg.nodes[hg.groups[gb].sink];
+      if (bn.op != CG_MAXPOOL2D_BWD || !g->eslot[gb]) continue;
+      for (size_t gp = 0; gp < gb; ++gp) {
+        const Node& fn = hg.nodes[hg.groups[gp].sink];
+        if (fn.op != CG_MAXPOOL2D || !g->eslot[gp] || fn.preds[0] != bn.preds[0] || fn.attr.kh != bn.attr.kh ||
+            fn.attr.kw != bn.attr.kw || fn.attr.sh != bn.attr.sh || fn.attr.sw != bn.attr.sw || fn.attr.pad != bn.attr.pad)
+          continue;
+        auto& fsl = *g->eslot[gp];
+        if (!fsl.codes) {
+          void* cb = nullptr;
+          CUDA_TRY(g, cudaMalloc(&cb, (size_t)numel(fn.shape)), "cudaMalloc(pool codes)");
+          g->code_bufs.push_back(cb);
+          fsl.codes = static_cast<unsigned char*>(cb);
+        }
+        g->eslot[gb]->codes = fsl.codes;
+        g->code_dep[gb] = (int)gp;
+        break;
+      }
+    }
+  }
   fuse_epilogues(g);
   // R14: an elementwise writer of a view either runs in a tensor-core epilogue that
   // stores the slice directly (row stride = the root's), or computes into scratch
@@ -1703,6 +1743,9 @@ int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float*
     // an epilogue-fused pair only runs as one kernel
     const int pg = g->partner.empty() ? -1 : g->partner[gi];
     if (pg >= 0 && !R[pg]) demand(hg.groups[pg].sink, true);
+    // a max-pool backward reading the forward's decisions: the forward runs too
+    const int cd = g->code_dep.empty() ? -1 : g->code_dep[gi];
+    if (cd >= 0 && !R[cd]) demand(hg.groups[cd].sink, true);
   };
   for (int r : roots) demand(r, false);
   for (;;) {  // clobber fix-point: a group may not read a block another launched group overwrote
@@ -1798,6 +1841,7 @@ void cg_destroy(cg_graph* g) {
     cudaFree(g->stage_buf);
     for (void* p : g->ipc_open) cudaIpcCloseMemHandle(p);
     for (void* p : g->view_scratch) cudaFree(p);
+    for (void* p : g->code_bufs) cudaFree(p);
     cudaFree(g->coll_dev);
     cudaFree(g->coll_flags);
     if (g->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(g->comm);

@@ -395,9 +395,12 @@ __global__ void maxpool_bwd_tiled_kernel(const float* __restrict__ x, const floa
 // computed from x by the producer's elementwise chain and stored to xo (every
 // element of xo lies in exactly one window), then pooled.  xo may alias x (an
 // in-place chain): each element is read and written by the same thread, in order.
+// codes != NULL: also record, per (output pixel, channel), the window position the
+// backward pass routes the gradient to (maxpool2_bwd_kernel's rule on the same
+// values), so the backward reads one byte instead of the four window values.
 template <int C, int V>
 __global__ void maxpool2_fwd_kernel(const float* x, float* __restrict__ y, ConvGeom g, int total, float* xo,
-                                    const __grid_constant__ EpiProg pro) {
+                                    const __grid_constant__ EpiProg pro, unsigned char* __restrict__ codes) {
   using VT = typename std::conditional<V == 4, float4, float2>::type;
   constexpr int Q = C / V;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
@@ -433,6 +436,22 @@ __global__ void maxpool2_fwd_kernel(const float* x, float* __restrict__ y, ConvG
       of[e] = m;
     }
     *reinterpret_cast<VT*>(y + (size_t)p * C + c) = o;
+    if (codes) {
+      unsigned packed = 0;
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        float m = -__int_as_float(0x7f800000);
+        int best = -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // (the backward kernel's first-maximum rule)
+          const float v = wf[k * V + e];
+          if (v > m || best < 0) { m = v; best = k; }
+        }
+        packed |= (unsigned)best << (8 * e);
+      }
+      if (V == 4) *reinterpret_cast<unsigned*>(codes + (size_t)p * C + c) = packed;
+      else *reinterpret_cast<unsigned short*>(codes + (size_t)p * C + c) = (unsigned short)packed;
+    }
   }
 }
 
@@ -446,7 +465,7 @@ __global__ void maxpool2_fwd_kernel(const float* x, float* __restrict__ y, ConvG
 // them: same thread, read before write).
 template <int C, int V>
 __global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* dx, ConvGeom g,
-                                    int total, const __grid_constant__ EpiProg epi) {
+                                    int total, const __grid_constant__ EpiProg epi, const unsigned char* __restrict__ codes) {
   using VT = typename std::conditional<V == 4, float4, float2>::type;
   constexpr int Q = C / V;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
@@ -454,28 +473,54 @@ __global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __
     const int wo = p % g.wo, q = p / g.wo, ho = q % g.ho, n = q / g.ho;
     const size_t o0 = (((size_t)n * g.h + 2 * ho) * g.w + 2 * wo) * C + c, o1 = o0 + (size_t)g.w * C;
     VT w4[4];
-    w4[0] = __ldg(reinterpret_cast<const VT*>(x + o0));
-    w4[1] = __ldg(reinterpret_cast<const VT*>(x + o0 + C));
-    w4[2] = __ldg(reinterpret_cast<const VT*>(x + o1));
-    w4[3] = __ldg(reinterpret_cast<const VT*>(x + o1 + C));
+    unsigned packed = 0;
+    if (codes) {  // the forward pass's recorded decisions
+      packed = V == 4 ? __ldg(reinterpret_cast<const unsigned*>(codes + (size_t)p * C + c))
+                      : __ldg(reinterpret_cast<const unsigned short*>(codes + (size_t)p * C + c));
+    } else {
+      w4[0] = __ldg(reinterpret_cast<const VT*>(x + o0));
+      w4[1] = __ldg(reinterpret_cast<const VT*>(x + o0 + C));
+      w4[2] = __ldg(reinterpret_cast<const VT*>(x + o1));
+      w4[3] = __ldg(reinterpret_cast<const VT*>(x + o1 + C));
+    }
     const VT dv = __ldg(reinterpret_cast<const VT*>(dy + (size_t)p * C + c));
+    // the usual chain, RELU_GRAD(pre-activation, this gradient): its four mask vectors
+    // are loaded here with the window's other loads (one memory round trip, not two)
+    const bool rg = epi.n == 1 && epi.op[0] == EPI_RGRAD && epi.scalar[0] == 2 && epi.swap[0] == 1 &&
+                    (reinterpret_cast<uintptr_t>(epi.x[0]) & (sizeof(VT) - 1)) == 0;
+    VT m4[4];
+    if (rg) {
+      const float* a = epi.x[0];
+      m4[0] = __ldg(reinterpret_cast<const VT*>(a + o0));
+      m4[1] = __ldg(reinterpret_cast<const VT*>(a + o0 + C));
+      m4[2] = __ldg(reinterpret_cast<const VT*>(a + o1));
+      m4[3] = __ldg(reinterpret_cast<const VT*>(a + o1 + C));
+    }
     VT r4[4];
     const float* wf = reinterpret_cast<const float*>(w4);
     const float* df = reinterpret_cast<const float*>(&dv);
     float* rf = reinterpret_cast<float*>(r4);
 #pragma unroll
     for (int e = 0; e < V; ++e) {
-      float m = -__int_as_float(0x7f800000);
       int best = -1;
+      if (codes) {
+        best = (int)(packed >> (8 * e)) & 255;
+      } else {
+        float m = -__int_as_float(0x7f800000);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float v = wf[k * V + e];
-        if (v > m || best < 0) { m = v; best = k; }
+        for (int k = 0; k < 4; ++k) {
+          const float v = wf[k * V + e];
+          if (v > m || best < 0) { m = v; best = k; }
+        }
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) rf[k * V + e] = best == k ? df[e] : 0.f;
     }
-    if (epi.n) {
+    if (rg) {  // RELU_GRAD(a, v) = a > 0 ? v : 0, as epi_apply
+      const float* mf = reinterpret_cast<const float*>(m4);
+#pragma unroll
+      for (int i = 0; i < 4 * V; ++i) rf[i] = mf[i] > 0.f ? rf[i] : 0.f;
+    } else if (epi.n) {
       const size_t off[4] = {o0, o0 + C, o1, o1 + C};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -828,7 +873,9 @@ static bool maxpool2_ok(const ConvGeom& g) {
 
 bool maxpool_fusable(const ConvGeom& g) { return maxpool2_ok(g) && g.h == 2 * g.ho && g.w == 2 * g.wo; }
 
-cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s, const EpiProg* pro, float* xo) {
+cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s, const EpiProg* pro, float* xo,
+                           unsigned char* codes) {
+  if (codes && !maxpool_fusable(g)) return cudaErrorInvalidValue;
   long long total = (long long)g.n * g.ho * g.wo * g.co;
   EpiProg ep{};
   if (pro && pro->n) {
@@ -837,8 +884,8 @@ cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStre
   }
   if (maxpool2_ok(g)) {
     const int pix = g.n * g.ho * g.wo;
-    if (g.co == 6) maxpool2_fwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, y, g, pix * 3, xo, ep);
-    else maxpool2_fwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, y, g, pix * 4, xo, ep);
+    if (g.co == 6) maxpool2_fwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, y, g, pix * 3, xo, ep, codes);
+    else maxpool2_fwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, y, g, pix * 4, xo, ep, codes);
     return cudaGetLastError();
   }
   if (g.co % 4 == 0 && total < INT32_MAX) {
@@ -853,7 +900,8 @@ cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStre
 }
 
 cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s,
-                               const EpiProg* epi) {
+                               const EpiProg* epi, const unsigned char* codes) {
+  if (codes && !maxpool_fusable(g)) return cudaErrorInvalidValue;
   EpiProg ep{};
   if (epi && epi->n) {
     if (!maxpool_fusable(g)) return cudaErrorInvalidValue;
@@ -861,8 +909,8 @@ cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const
   }
   if (maxpool2_ok(g)) {
     const int pix = g.n * g.ho * g.wo;
-    if (g.co == 6) maxpool2_bwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, dy, dx, g, pix * 3, ep);
-    else maxpool2_bwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, dy, dx, g, pix * 4, ep);
+    if (g.co == 6) maxpool2_bwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, dy, dx, g, pix * 3, ep, codes);
+    else maxpool2_bwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, dy, dx, g, pix * 4, ep, codes);
     return cudaGetLastError();
   }
   if (g.kh == g.sh && g.kw == g.sw && g.pt == 0 && g.pl == 0 && g.h == g.ho * g.sh && g.w == g.wo * g.sw) {

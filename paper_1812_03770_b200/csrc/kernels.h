@@ -42,10 +42,13 @@ struct EpiProg;
 // that; launch_maxpool_bwd with `epi` applies the consuming group's chain to every
 // gradient value before the store.  NULL / n == 0: the plain kernels.
 bool maxpool_fusable(const ConvGeom& g);
+// codes (maxpool_fusable geometries): one byte per (output pixel, channel), the window
+// position the backward pass routes the gradient to -- written by the forward
+// kernel, read by the backward kernel instead of the input's four window values.
 cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s, const EpiProg* pro = nullptr,
-                           float* xo = nullptr);
+                           float* xo = nullptr, unsigned char* codes = nullptr);
 cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s,
-                               const EpiProg* epi = nullptr);
+                               const EpiProg* epi = nullptr, const unsigned char* codes = nullptr);
 cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s);
 
 constexpr int kMaxConcat = 16;

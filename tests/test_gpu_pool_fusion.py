@@ -127,3 +127,47 @@ def test_c3_relu_grad_in_gemm_epilogue_bit_identical():
     assert info1["n_fused"] - info0["n_fused"] == 1, (info0["n_fused"], info1["n_fused"])
     g0.destroy()
     g1.destroy()
+
+
+def test_pool_codes_bit_identical_and_incremental():
+    """2x2 max-pool backward reading the forward's recorded window decisions (one
+    byte per output element) instead of the input: C4 trajectories are bit-identical
+    to the plan without codes; asking for the backward value alone after the input
+    changed still re-runs the forward (its decisions must be current)."""
+    spec = configs.c4(batch=96)
+    g0, outs, _ = _build_env(spec, {"CG_NO_POOL_CODES": "1"})
+    h0, w0 = _run(spec, g0, outs, 3)
+    g1, outs1, _ = _build(spec)
+    h1, w1 = _run(spec, g1, outs1, 3)
+    for a, b in zip(h0, h1):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    for k in w0:
+        assert np.array_equal(w0[k], w1[k]), f"parameter {k}"
+    g0.destroy()
+    g1.destroy()
+
+    rng = np.random.default_rng(9)
+    shp = (4, 12, 12, 16)
+    g = cg.Graph(0)
+    vx, vdy = g.var(shp), g.var((4, 6, 6, 16))
+    h = g.add_node("RELU", [vx])
+    p = g.add_node("MAXPOOL2D", [h], kh=2, kw=2, sh=2, sw=2, pad=0)
+    dh = g.add_node("MAXPOOL2D_BWD", [h, vdy], kh=2, kw=2, sh=2, sw=2, pad=0)
+    g.plan_memory([p, dh], cg.PLAN_INCREMENTAL)
+    dyv = rng.standard_normal((4, 6, 6, 16)).astype(np.float32)
+    g.assign(vdy, dyv)
+
+    def ref(xv):
+        hv = np.maximum(xv, 0)
+        win = hv.reshape(4, 6, 2, 6, 2, 16).transpose(0, 1, 3, 2, 4, 5).reshape(4, 6, 6, 4, 16)
+        best = np.argmax(win, axis=3)  # first maximum, as the kernels
+        out = np.zeros((4, 6, 6, 4, 16), np.float32)
+        np.put_along_axis(out, best[:, :, :, None, :], dyv[:, :, :, None, :], axis=3)
+        return out.reshape(4, 6, 6, 2, 2, 16).transpose(0, 1, 3, 2, 4, 5).reshape(shp)
+    for it in range(3):
+        xv = rng.standard_normal(shp).astype(np.float32)
+        g.assign(vx, xv)
+        g.eval([dh] if it else [p, dh])
+        assert np.array_equal(g.read(dh), ref(xv)), it
+    g.destroy()
