@@ -422,7 +422,7 @@ __global__ void maxpool2_fwd_kernel(const float* x, float* __restrict__ y, ConvG
         epi_run<V>(pro, v, (long long)off[k], c);
 #pragma unroll
         for (int e = 0; e < V; ++e) reinterpret_cast<float*>(&w4[k])[e] = v[e];
-        *reinterpret_cast<VT*>(xo + off[k]) = w4[k];
+        if (xo) *reinterpret_cast<VT*>(xo + off[k]) = w4[k];  // (NULL: no reader needs the values)
       }
     }
     const float* wf = reinterpret_cast<const float*>(w4);
@@ -879,7 +879,7 @@ cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStre
   long long total = (long long)g.n * g.ho * g.wo * g.co;
   EpiProg ep{};
   if (pro && pro->n) {
-    if (!maxpool_fusable(g) || !xo) return cudaErrorInvalidValue;
+    if (!maxpool_fusable(g) || (!xo && !codes)) return cudaErrorInvalidValue;
     ep = *pro;
   }
   if (maxpool2_ok(g)) {
