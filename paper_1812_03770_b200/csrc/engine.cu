@@ -317,6 +317,7 @@ struct cg_graph {
     float* xo = nullptr;
     unsigned char* codes = nullptr;  // 2x2 max pool: the forward's recorded window decisions
     float* aux = nullptr;            // conv bwd-kernel: a fused SUM group's output (the bias gradient)
+    int code_mask = 0;               // max-pool backward: RELU_GRAD from the codes' sign bit
   };
   std::vector<std::shared_ptr<EpiSlot>> eslot;
   // max-pool backward group -> the forward pool group whose decisions it reads (-1:
@@ -588,6 +589,17 @@ static void fuse_epilogues(cg_graph* g) {
     } else {
       sl->epi = prog;
       sl->out = g->ptr[E.sink];
+      // a max-pool backward over x = RELU(a) whose chain is exactly RELU_GRAD(a, .):
+      // a[k] > 0 <=> relu(a)[k] > 0 at the routed position k, recorded by the forward
+      if (sop == CG_MAXPOOL2D_BWD && sl->codes && prog.n == 1 && prog.op[0] == EPI_RGRAD && prog.swap[0] == 1 &&
+          prog.scalar[0] == 2) {
+        const Node& xn = hg.nodes[hg.nodes[hg.groups[gd].sink].preds[0]];
+        const int rg = E.members[0];
+        if (xn.op == CG_RELU && hg.nodes[rg].preds[0] == xn.preds[0]) {
+          sl->code_mask = 1;
+          sl->epi = EpiProg{};
+        }
+      }
     }
     g->glaunch[ge].clear();
     g->partner[gd] = ge;
@@ -988,7 +1000,7 @@ static int build_launches(cg_graph* g) {
           sl->out = out;
           g->eslot[gi] = sl;
           L.push_back({[x, dy, sl, cgm](cudaStream_t s) {
-                         return launch_maxpool_bwd(x, dy, sl->out, cgm, s, &sl->epi, sl->codes);
+                         return launch_maxpool_bwd(x, dy, sl->out, cgm, s, &sl->epi, sl->codes, sl->code_mask);
                        },
                        1});
           break;

@@ -447,7 +447,9 @@ __global__ void maxpool2_fwd_kernel(const float* x, float* __restrict__ y, ConvG
           const float v = wf[k * V + e];
           if (v > m || best < 0) { m = v; best = k; }
         }
-        packed |= (unsigned)best << (8 * e);
+        // bit 7: the window's selected value is > 0 (for the backward's RELU_GRAD
+        // when the pooled input is relu(a): a[best] > 0 <=> relu(a)[best] > 0)
+        packed |= ((unsigned)best | (m > 0.f ? 0x80u : 0u)) << (8 * e);
       }
       if (V == 4) *reinterpret_cast<unsigned*>(codes + (size_t)p * C + c) = packed;
       else *reinterpret_cast<unsigned short*>(codes + (size_t)p * C + c) = (unsigned short)packed;
@@ -464,8 +466,11 @@ __global__ void maxpool2_fwd_kernel(const float* x, float* __restrict__ y, ConvG
 // its full-tensor operands are read at the same flat index (dx may alias one of
 // them: same thread, read before write).
 template <int C, int V>
+// code_mask: the consumer chain is RELU_GRAD(a, .) with x = relu(a): applied from
+// the codes' recorded sign bit instead of reading a.
 __global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* dx, ConvGeom g,
-                                    int total, const __grid_constant__ EpiProg epi, const unsigned char* __restrict__ codes) {
+                                    int total, const __grid_constant__ EpiProg epi, const unsigned char* __restrict__ codes,
+                                    int code_mask) {
   using VT = typename std::conditional<V == 4, float4, float2>::type;
   constexpr int Q = C / V;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
@@ -504,7 +509,8 @@ __global__ void maxpool2_bwd_kernel(const float* __restrict__ x, const float* __
     for (int e = 0; e < V; ++e) {
       int best = -1;
       if (codes) {
-        best = (int)(packed >> (8 * e)) & 255;
+        const unsigned cb = (packed >> (8 * e)) & 255u;
+        best = code_mask && !(cb & 0x80u) ? -1 : (int)(cb & 3u);  // (-1: masked, nothing routed)
       } else {
         float m = -__int_as_float(0x7f800000);
 #pragma unroll
@@ -900,8 +906,8 @@ cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStre
 }
 
 cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s,
-                               const EpiProg* epi, const unsigned char* codes) {
-  if (codes && !maxpool_fusable(g)) return cudaErrorInvalidValue;
+                               const EpiProg* epi, const unsigned char* codes, int code_mask) {
+  if ((codes && !maxpool_fusable(g)) || (code_mask && !codes)) return cudaErrorInvalidValue;
   EpiProg ep{};
   if (epi && epi->n) {
     if (!maxpool_fusable(g)) return cudaErrorInvalidValue;
@@ -909,8 +915,8 @@ cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const
   }
   if (maxpool2_ok(g)) {
     const int pix = g.n * g.ho * g.wo;
-    if (g.co == 6) maxpool2_bwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, dy, dx, g, pix * 3, ep, codes);
-    else maxpool2_bwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, dy, dx, g, pix * 4, ep, codes);
+    if (g.co == 6) maxpool2_bwd_kernel<6, 2><<<grid_for(pix * 3), 256, 0, s>>>(x, dy, dx, g, pix * 3, ep, codes, code_mask);
+    else maxpool2_bwd_kernel<16, 4><<<grid_for(pix * 4), 256, 0, s>>>(x, dy, dx, g, pix * 4, ep, codes, code_mask);
     return cudaGetLastError();
   }
   if (g.kh == g.sh && g.kw == g.sw && g.pt == 0 && g.pl == 0 && g.h == g.ho * g.sh && g.w == g.wo * g.sw) {

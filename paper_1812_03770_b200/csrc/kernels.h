@@ -47,8 +47,10 @@ bool maxpool_fusable(const ConvGeom& g);
 // kernel, read by the backward kernel instead of the input's four window values.
 cudaError_t launch_maxpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s, const EpiProg* pro = nullptr,
                            float* xo = nullptr, unsigned char* codes = nullptr);
+// code_mask (with codes): the consumer RELU_GRAD(a, .) of a pool over relu(a), applied
+// from the codes' recorded sign bit (a is not read)
 cudaError_t launch_maxpool_bwd(const float* x, const float* dy, float* dx, const ConvGeom& g, cudaStream_t s,
-                               const EpiProg* epi = nullptr, const unsigned char* codes = nullptr);
+                               const EpiProg* epi = nullptr, const unsigned char* codes = nullptr, int code_mask = 0);
 cudaError_t launch_avgpool(const float* x, float* y, const ConvGeom& g, cudaStream_t s);
 
 constexpr int kMaxConcat = 16;
