@@ -2055,20 +2055,36 @@ struct BsGeo {
   static constexpr int THREADS = (KS * BS_GW + 1) * 32;
   static_assert(OW % 2 == 0, "pixel pairs within a row");
   static_assert((DYF * 4) % 16 == 0 && (COUT * 2) % 4 == 0, "16-byte dy copies / pair loads");
+  // POOLED: dy given as the 2x2 max-pool backward's inputs -- the pooled gradient
+  // [n, OH/2, OW/2, COUT] and the forward's decision codes (same shape, bytes)
+  static constexpr int DPF = (OH / 2) * (OW / 2) * COUT;
+  template <bool POOLED>
+  __host__ __device__ static constexpr int slot() { return POOLED ? G * DPF + (G * DPF + 15) / 16 * 4 : G * DYF; }  // floats per stage
+  template <bool POOLED>
+  static constexpr size_t smem_bytes() {
+    return 1024 + (2 * (size_t)XBUF + 2 * (size_t)slot<POOLED>() + (POOLED ? (size_t)G * DYF : 0) + KS * BS_GW * 32) * 4 +
+           64;
+  }
 };
 
-template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
+// POOLED: dy = RELU_GRAD(a, MAXPOOL2D_BWD(relu(a), dp)) is never materialised; each
+// pixel pair's dy is formed from dp and the pool's codes (bit 7: the routed value is
+// > 0, bits 0-1: the window position) -- the values the pool-backward kernel would
+// have stored.
+template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT, bool POOLED = false>
 __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREADS, 1)
     conv_bwdk_simt_kernel(const float* __restrict__ x, const float* __restrict__ dy, float* __restrict__ ws, int nimgs,
-                          const __grid_constant__ CUtensorMap xmap, float* __restrict__ wsb) {
+                          const __grid_constant__ CUtensorMap xmap, float* __restrict__ wsb,
+                          const unsigned char* __restrict__ pcodes) {
   using Geo = BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>;
   using SG = typename Geo::SG;
   constexpr int G = Geo::G, PP = Geo::PP, DYF = Geo::DYF, NT = BS_GW * 32;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* xs = reinterpret_cast<float*>(smem);                 // [2][XBUF]
-  float* dys = xs + 2 * Geo::XBUF;                             // [2][G * DYF]
-  float* red = dys + 2 * G * DYF;                              // [KS][NT] reduction scratch
+  float* dys = xs + 2 * Geo::XBUF;                             // [2][SLOT]: dy, or (POOLED) dp + codes
+  float* dyx = dys + 2 * Geo::template slot<POOLED>();         // (POOLED) this stage's dy, formed once: [G * DYF]
+  float* red = dyx + (POOLED ? G * DYF : 0);                   // [KS][NT] reduction scratch
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + KS * NT);
   const uint32_t bar0 = smem_u32(bars);
   auto full = [&](int b) { return bar0 + 8u * b; };
@@ -2095,8 +2111,17 @@ __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREA
       mbar_wait_lazy(freeb(b), ((j >> 1) & 1) ^ 1);
       if (lane == 0) {
         // (no arrive here: stage_images' arrive.expect_tx below completes the phase's count)
-        mbar_expect_tx_only(full(b), (uint32_t)(nimg * DYF * 4));
-        bulk_g2s(smem_u32(dys + b * G * DYF), dy + (size_t)n0 * DYF, (uint32_t)(nimg * DYF * 4), full(b));
+        if constexpr (POOLED) {
+          constexpr int DPF = Geo::DPF;
+          const uint32_t cbytes = (uint32_t)(nimg * DPF + 15) / 16 * 16;  // (the codes buffer is padded)
+          mbar_expect_tx_only(full(b), (uint32_t)(nimg * DPF * 4) + cbytes);
+          constexpr int SLOT = Geo::template slot<true>();
+          bulk_g2s(smem_u32(dys + b * SLOT), dy + (size_t)n0 * DPF, (uint32_t)(nimg * DPF * 4), full(b));
+          bulk_g2s(smem_u32(dys + b * SLOT + G * DPF), pcodes + (size_t)n0 * DPF, cbytes, full(b));
+        } else {
+          mbar_expect_tx_only(full(b), (uint32_t)(nimg * DYF * 4));
+          bulk_g2s(smem_u32(dys + b * G * DYF), dy + (size_t)n0 * DYF, (uint32_t)(nimg * DYF * 4), full(b));
+        }
       }
       stage_images<SG>(smem_u32(xs + b * Geo::XBUF), x, xmap_addr, n0, nimg, G, full(b), lane);
     }
@@ -2118,9 +2143,31 @@ __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREA
   int j = 0;
   for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
     const int b = j & 1, n0 = u * G, nimg = min(G, nimgs - n0);
+    if constexpr (POOLED) asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");  // previous stage's dy read
     mbar_wait(full(b), (j >> 1) & 1);
     const float* xb = xs + b * Geo::XBUF;
-    const float* db = dys + b * G * DYF;
+    const float* db = dys + b * Geo::template slot<POOLED>();
+    if constexpr (POOLED) {
+      // dy = RELU_GRAD(a, MAXPOOL2D_BWD(relu(a), dp)) formed once per stage from dp and
+      // the pool's codes (bit 7: the routed value > 0; bits 0-1: window position
+      // k = 2 * row + column): the values the pool-backward kernel would have stored
+      const unsigned char* cb = reinterpret_cast<const unsigned char*>(db + G * Geo::DPF);
+      constexpr int WPR = OW / 2;
+      for (int e = threadIdx.x; e < nimg * Geo::DPF; e += KS * NT) {
+        const int c = e % COUT, w = e / COUT, wc = w % WPR, wr = (w / WPR) % (OH / 2), gg = w / (WPR * (OH / 2));
+        const unsigned code = cb[e];
+        const float v = db[e];
+        const int k = (code & 0x80u) ? (int)(code & 3u) : -1;
+        float* o = dyx + ((gg * OH + 2 * wr) * OW + 2 * wc) * COUT + c;
+        o[0] = k == 0 ? v : 0.f;
+        o[COUT] = k == 1 ? v : 0.f;
+        o[OW * COUT] = k == 2 ? v : 0.f;
+        o[OW * COUT + COUT] = k == 3 ? v : 0.f;
+      }
+      // (buffer b is released after the items below: its x images are still read)
+      asm volatile("bar.sync 1, %0;" ::"r"(KS * NT) : "memory");  // the stage's dy complete
+      db = dyx;
+    }
     for (int q = t; q < nimg * PP; q += NT) {
       const int g = q / PP, pp = q - g * PP, oh = pp / (OW / 2), ow = (pp - oh * (OW / 2)) * 2;
       float d0[COUT], d1[COUT];
@@ -2178,7 +2225,7 @@ __global__ void __launch_bounds__(BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>::THREA
 
 template <int KS, int IH, int IW, int OH, int OW, int PT, int PL, int COUT>
 cudaError_t launch_bwdk_simt(const float* x, const float* dy, float* dw, float* ws, int n, int num_sms, cudaStream_t s,
-                             float* db) {
+                             float* db, const unsigned char* pcodes) {
   using Geo = BsGeo<KS, IH, IW, OH, OW, PT, PL, COUT>;
   using SG = typename Geo::SG;
   static_assert(SG::TMAP, "zero padding from the tensor map's out-of-bounds fill");
@@ -2186,13 +2233,14 @@ cudaError_t launch_bwdk_simt(const float* x, const float* dy, float* dw, float* 
   CUtensorMap xmap;
   std::memset(&xmap, 0, sizeof(xmap));
   if (!make_img_map(&xmap, x, n, IH, IW, SG::WPS, SG::HP, Geo::G)) return cudaErrorInvalidValue;
-  const size_t smem = 1024 + (2 * (size_t)Geo::XBUF + 2 * (size_t)Geo::G * Geo::DYF + KS * BS_GW * 32) * 4 + 64;
-  auto kern = conv_bwdk_simt_kernel<KS, IH, IW, OH, OW, PT, PL, COUT>;
+  const size_t smem = pcodes ? Geo::template smem_bytes<true>() : Geo::template smem_bytes<false>();
+  auto kern = pcodes ? conv_bwdk_simt_kernel<KS, IH, IW, OH, OW, PT, PL, COUT, true>
+                     : conv_bwdk_simt_kernel<KS, IH, IW, OH, OW, PT, PL, COUT, false>;
   cudaError_t e = smem_attr((const void*)kern, (int)smem);
   if (e != cudaSuccess) return e;
   const int grid = std::max(1, std::min(n, num_sms));
   float* wsb = db ? ws + (size_t)grid * KS * KS * COUT : nullptr;  // (conv_img_tc_bwdk_ws counts it)
-  kern<<<grid, Geo::THREADS, smem, s>>>(x, dy, ws, n, xmap, wsb);
+  kern<<<grid, Geo::THREADS, smem, s>>>(x, dy, ws, n, xmap, wsb, pcodes);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = launch_reduce_finalize(ws, dw, (long long)KS * KS * COUT, grid, 0, s);
@@ -2211,13 +2259,13 @@ size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms) {  // (+ the fused bi
 bool conv_img_tc_bwdk_bias_ok(const ConvGeom& g) { return kind_of(g, false) == CI_C4_CONV1 && !getenv("CG_BWDK_TC1"); }
 
 cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g, int num_sms,
-                                    cudaStream_t s, float* db) {
-  if (db && !conv_img_tc_bwdk_bias_ok(g)) return cudaErrorInvalidValue;
+                                    cudaStream_t s, float* db, const unsigned char* pcodes) {
+  if ((db || pcodes) && !conv_img_tc_bwdk_bias_ok(g)) return cudaErrorInvalidValue;
   switch (kind_of(g, false)) {
     case CI_C4_CONV1:  // x [n,28,28,1], dy [n,28,28,6] -> dw [5,5,1,6] (SAME)
       if (getenv("CG_BWDK_TC1"))  // (A/B: the tensor-core K = pixels formulation)
         return BkLaunch<1, 5, 28, 28, 28, 28, 2, 2, 6>::run(x, dy, dw, ws, g.n, num_sms, s);
-      return launch_bwdk_simt<5, 28, 28, 28, 28, 2, 2, 6>(x, dy, dw, ws, g.n, num_sms, s, db);
+      return launch_bwdk_simt<5, 28, 28, 28, 28, 2, 2, 6>(x, dy, dw, ws, g.n, num_sms, s, db, pcodes);
     case CI_C4_CONV2:  // x [n,14,14,6], dy [n,10,10,16] -> dw [5,5,6,16] (VALID)
       return BkLaunch<6, 5, 14, 14, 10, 10, 0, 0, 16>::run(x, dy, dw, ws, g.n, num_sms, s);
     default:

@@ -28,8 +28,10 @@ cudaError_t launch_conv_img_tc(const float* in, const float* w, float* out, cons
 bool conv_img_tc_bwdk_supported(const ConvGeom& g);
 bool conv_img_tc_bwdk_bias_ok(const ConvGeom& g);
 size_t conv_img_tc_bwdk_ws(const ConvGeom& g, int num_sms);
+// pcodes != NULL (same geometries): dy = RELU_GRAD(a, MAXPOOL2D_BWD(relu(a), dp)) given
+// as dp (pointer `dy`, [n, ho/2, wo/2, co]) and the pool's decision codes (launch_maxpool)
 cudaError_t launch_conv_img_tc_bwdk(const float* x, const float* dy, float* dw, float* ws, const ConvGeom& g, int num_sms,
-                                    cudaStream_t s, float* db = nullptr);
+                                    cudaStream_t s, float* db = nullptr, const unsigned char* pcodes = nullptr);
 
 // The InceptionV3 stem conv (Ci = 3, stride 2) over bands of output rows, with the
 // DOT/CONV epilogue's fused elementwise chain (conv_band_tc_kernel); x must be

@@ -318,6 +318,8 @@ struct cg_graph {
     unsigned char* codes = nullptr;  // 2x2 max pool: the forward's recorded window decisions
     float* aux = nullptr;            // conv bwd-kernel: a fused SUM group's output (the bias gradient)
     int code_mask = 0;               // max-pool backward: RELU_GRAD from the codes' sign bit
+    const float* pdp = nullptr;      // conv bwd-kernel: dy formed from a pool backward's dp + codes
+    const unsigned char* pcodes = nullptr;
   };
   std::vector<std::shared_ptr<EpiSlot>> eslot;
   // max-pool backward group -> the forward pool group whose decisions it reads (-1:
@@ -643,6 +645,51 @@ static void fuse_epilogues(cg_graph* g) {
       break;
     }
   }
+  // The one-channel conv's backward-kernel reading its dy in the pooled form: when dy
+  // = RELU_GRAD(a, MAXPOOL2D_BWD(relu(a), dp)) is computed by a pool-backward kernel
+  // that applies the mask from its codes, and nothing else reads dy, the kernel forms
+  // dy from dp and the codes itself and the pool-backward kernel does not run (C4:
+  // a 154 MB write and read of da1 gone).  dp is read later than planned: its block
+  // must not be rewritten in between.
+  for (size_t gk = 0; gk < NG && !no_slot; ++gk) {
+    auto sk = g->eslot[gk];
+    const Node& kn = hg.nodes[hg.groups[gk].sink];
+    if (!sk || kn.op != CG_CONV2D_BWD_KERNEL) continue;
+    if (!conv_img_tc_bwdk_bias_ok(geom(kn, hg.nodes[kn.preds[0]].shape, hg.nodes[kn.preds[1]].shape, kn.attr.kh,
+                                       kn.attr.kw)))
+      continue;
+    const int dyv = kn.preds[1];
+    if (hg.is_external(dyv) || hg.keep[dyv] || is_view(dyv)) continue;
+    const int ge = hg.group_of[dyv];
+    const int gp = ge >= 0 ? g->partner[ge] : -1;
+    if (gp < 0 || !g->glaunch[ge].empty() || !g->eslot[gp] || !g->eslot[gp]->code_mask ||
+        hg.nodes[hg.groups[gp].sink].op != CG_MAXPOOL2D_BWD || hg.groups[ge].sink != dyv)
+      continue;
+    bool only = true;  // dy's readers: this group and its fused bias SUM
+    for (size_t gi = 0; gi < NG && only; ++gi) {
+      if (gi == gk || (int)gi == g->partner[gk]) continue;
+      const auto& in = hg.groups[gi].inputs;
+      only = std::find(in.begin(), in.end(), dyv) == in.end();
+    }
+    for (const auto& u : hg.updates) only = only && u.first != dyv && u.second != dyv;
+    if (!only) continue;
+    const int dp = hg.nodes[hg.groups[gp].sink].preds[1];
+    if (hg.is_external(dp) || is_view(dp)) continue;
+    const int B = hg.pl.block_of[dp];
+    bool clash = false;
+    for (size_t gm = gp + 1; gm <= gk && !clash; ++gm)
+      for (int m : hg.groups[gm].materialised)
+        if (!g->fused_away[m] && hg.pl.block_of[m] == B && m != dyv) clash = true;
+    if (g->partner[gk] >= 0)
+      for (int m : hg.groups[g->partner[gk]].materialised)
+        if (hg.pl.block_of[m] == B) clash = true;
+    if (clash) continue;
+    sk->pdp = g->ptr[dp];
+    sk->pcodes = g->eslot[gp]->codes;
+    g->glaunch[gp].clear();
+    g->fused_away[dyv] = 1;
+    g->n_pool_fused++;
+  }
   // f3: the update chain of an ALLREDUCE_SUM (W - lr * g: a scalar / column / full
   // tensor operand per op, all external) runs inside the fused collective
   for (size_t gd = 0; gd < NG && g->fused_coll; ++gd) {
@@ -961,7 +1008,8 @@ static int build_launches(cg_graph* g) {
           auto sl = std::make_shared<cg_graph::EpiSlot>();
           g->eslot[gi] = sl;
           L.push_back({[x, dy, out, ws, cgm, sms, sl](cudaStream_t s) {
-                         return launch_conv_img_tc_bwdk(x, dy, out, ws, cgm, sms, s, sl->aux);
+                         return launch_conv_img_tc_bwdk(x, sl->pcodes ? sl->pdp : dy, out, ws, cgm, sms, s, sl->aux,
+                                                        sl->pcodes);
                        },
                        2});
         }
@@ -1062,7 +1110,7 @@ static int build_launches(cg_graph* g) {
         auto& fsl = *g->eslot[gp];
         if (!fsl.codes) {
           void* cb = nullptr;
-          CUDA_TRY(g, cudaMalloc(&cb, (size_t)numel(fn.shape)), "cudaMalloc(pool codes)");
+          CUDA_TRY(g, cudaMalloc(&cb, (size_t)numel(fn.shape) + 16), "cudaMalloc(pool codes)");  // (+16: 16-byte copies)
           g->code_bufs.push_back(cb);
           fsl.codes = static_cast<unsigned char*>(cb);
         }
