@@ -682,15 +682,20 @@ bool dot_tc_supported(int M, int N, int K, int ta, int tb) {
 
 // N tile: 256 columns when that wastes no more padding than 128 (halves the
 // operand traffic per FLOP: A is re-read per N tile), else 128.
-int pick_bn(int M, int N, int num_sms) {
+int pick_bn(int M, int N, int num_sms, int K) {
   // narrow outputs (convs with 32 / 64 channels): a matching MMA N instead of padding to 128
   if (N <= 32) return 32;
   if (N <= 64) return 64;
-  (void)M, (void)num_sms;
   if (const char* e = getenv("CG_TC_BN")) {  // measurement override: only the instantiated tile widths
     const int v = atoi(e);
     if (v == 32 || v == 64 || v == 128) return v;
   }
+  // fewer 128-wide tiles than half the SMs and a short K (C4's batch x 84..400 layers:
+  // 64 tiles, K <= 400): 64-wide tiles put twice as many CTAs to work on the
+  // latency-bound pipeline (-13 us per C4 iteration); with a long K split-K fills the
+  // machine instead (C3's weight gradients, K = 4096: 64-wide was 48 us slower)
+  const long long tiles128 = (long long)((M + BM - 1) / BM) * ((N + 127) / 128);
+  if (tiles128 < num_sms / 2 && K <= 1024) return 64;
   return 128;  // TMEM: 2 x BN accumulator columns + the A stages fit 512 columns for BN <= 128
 }
 
@@ -704,7 +709,7 @@ int pick_cg(int M, int N, int bn, int splits, int num_sms, bool gather) {
 }
 
 void dot_tc_split(int M, int N, int K, int num_sms, int* splits, int* kb_per_split) {
-  const int bn = pick_bn(M, N, num_sms);
+  const int bn = pick_bn(M, N, num_sms, K);
   const long long tiles = (long long)((M + BM - 1) / BM) * ((N + bn - 1) / bn);
   const int nk = (K + BK - 1) / BK;
   // split-K: minimise (waves x k-blocks per unit) + the partials' HBM round trip
@@ -748,7 +753,7 @@ int dot_tc_prepare(DotTcPlan* p, const float* A, const float* B, float* C, int M
   bool ok = ta ? make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, K, M, 32, true)
                : make_map(reinterpret_cast<CUtensorMap*>(p->mapA), A, M, K, BM, false);
   // B: tb = 0 -> [K, N] (N-major, box 32 n x 32 k); tb = 1 -> [N, K] (K-major, box 32 k x BN/CG n)
-  p->bn = pick_bn(M, N, num_sms);
+  p->bn = pick_bn(M, N, num_sms, K);
   p->cg = pick_cg(M, N, p->bn, p->splits, num_sms, false);
   ok = ok && (tb ? make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, N, K, p->bn / p->cg, false)
                  : make_map(reinterpret_cast<CUtensorMap*>(p->mapB), B, K, N, 32, true));
@@ -830,7 +835,7 @@ int conv_tc_prepare(DotTcPlan* p, const float* x, const float* w, float* y, int 
     if (ci % 32 == 0 && make_im2col_map(ma, x, n, h, wd, ci, ho, wo, sh, sw, pt, pl, 32)) p->conv.tma = 1;
     else if (ci % 16 == 0 && make_im2col_map(ma, x, n, h, wd, ci, ho, wo, sh, sw, pt, pl, 16)) p->conv.tma = 2;
   }
-  p->bn = pick_bn(p->M, co, num_sms);
+  p->bn = pick_bn(p->M, co, num_sms, p->K);
   p->cg = pick_cg(p->M, co, p->bn, p->splits, num_sms, true);
   if (conv_band_supported(n, h, wd, ci, kh, kw, co, ho, wo, sh, sw, pt, pl)) {  // the stem: row bands, no split-K
     p->band = 1;
