@@ -18,6 +18,7 @@ import pytest
 from paper_1812_03770_b200 import cg
 from tests.test_gpu_fused_coll import _build, _run
 from workloads import configs
+from workloads.gen import materialise, retag
 
 pytestmark = pytest.mark.gpu
 
@@ -174,3 +175,31 @@ def test_pool_codes_bit_identical_and_incremental():
         g.eval([dh] if it else [p, dh])
         assert np.array_equal(g.read(dh), ref(xv)), it
     g.destroy()
+
+
+def test_c4_fused_gradients_under_partial_demand():
+    """Incremental evaluation through the executor fusions: after a new X, asking
+    only for dW1 (whose dy, da1, is never materialised -- formed from dp1 and the
+    pool's codes) or only for db1 (fused into the same kernel) must recompute the
+    chain that feeds it (pool forward codes included) and match a full evaluation."""
+    spec = configs.c4(batch=64)
+    ids = {n["name"]: n["id"] for n in spec["nodes"] if n["op"] == "VAR"}
+    grads = [n["id"] for n in spec["nodes"] if n["op"] == "CONV2D_BWD_KERNEL"]
+    sums = [n["id"] for n in spec["nodes"] if n["op"] == "SUM" and n.get("attrs", {}).get("a1") == 3]
+    want_nodes = grads + sums
+    spec = dict(spec)
+    spec["outputs"] = list(spec["outputs"]) + want_nodes
+    g, outs, info = _build(spec)
+    ref, _, _ = _build(spec)
+    xrec = spec["nodes"][ids["X"]]
+    for it in range(3):
+        xv = materialise(retag(xrec["data"], f"X@pd{it}"), xrec["shape"])
+        for gr in (g, ref):
+            gr.assign(ids["X"], xv)
+        ref.eval(outs, cg.EVAL_NO_UPDATE)
+        for node in want_nodes:  # one output at a time, each after a fresh X on g
+            g.assign(ids["X"], xv)
+            g.eval([node], cg.EVAL_NO_UPDATE)
+            assert np.array_equal(g.read(node), ref.read(node)), (it, node)
+    g.destroy()
+    ref.destroy()
