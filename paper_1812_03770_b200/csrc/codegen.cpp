@@ -61,7 +61,11 @@ std::string expr(int op, const std::vector<std::string>& a) {
     case CG_NEG: return "(-" + a[0] + ")";
     case CG_ABS: return "fabsf(" + a[0] + ")";
     case CG_SQRT: return "__fsqrt_rn(" + a[0] + ")";
-    case CG_EXP: return "expf(" + a[0] + ")";
+    case CG_EXP: {
+      // CG_FAST_EXP=1 (measurement only): 2^(x log2 e) on the SFU, see cg_exp2e
+      static const bool fast = getenv("CG_FAST_EXP") && atoi(getenv("CG_FAST_EXP")) == 1;
+      return (fast ? "cg_exp2e(" : "expf(") + a[0] + ")";
+    }
     case CG_LOG: return "logf(" + a[0] + ")";
     case CG_SIN: return "sinf(" + a[0] + ")";
     case CG_COS: return "cosf(" + a[0] + ")";
@@ -75,6 +79,16 @@ std::string expr(int op, const std::vector<std::string>& a) {
 
 const char* kPrelude = R"(
 typedef unsigned long long u64;
+// CG_FAST_EXP=1 only (measurement, not the default): exp(x) = 2^RN(x log2 e) on the
+// SFU, relative error <= |x| 2^-23 + 2 ulp (libm expf: <= 2 ulp).  C2 under the power
+// cap: 90-94 % -> 96.5-97 % of HBM (its chain is issue-bound there; a compensated
+// 2.5-ulp variant with four more instructions measured no gain), so the default stays
+// the accurate expf.
+__device__ __forceinline__ float cg_exp2e(float x) {
+  float r;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(r) : "f"(__fmul_rn(x, 1.44269504088896341f)));
+  return r;
+}
 __device__ __forceinline__ float4 cg_ld4(const float* p) {
   float4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
