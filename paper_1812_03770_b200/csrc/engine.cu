@@ -420,6 +420,21 @@ static inline int family(const HostGraph& hg, int v) {
   return v >= 0 && !hg.pl.view_root.empty() && hg.pl.view_root[v] >= 0 ? hg.pl.view_root[v] : v;
 }
 
+// A fused kernel writes value v (block B) at group gd's position in Gamma while the
+// plan gives B to v only at ge's: unless v slid into the producer's block, no group
+// in [gd, ge) may read B and none in (gd, ge) may write it (its previous occupant may
+// still be live there) -- other slices of v's zero-copy CONCAT family are disjoint.
+static bool moved_write_clashes(const HostGraph& hg, int B, int v, int gd, int ge) {
+  for (int gm = gd; gm < ge; ++gm) {
+    for (int p : hg.groups[gm].inputs)
+      if (!hg.is_external(p) && hg.pl.block_of[p] == B && family(hg, p) != family(hg, v)) return true;
+    if (gm == gd) continue;
+    for (int m : hg.groups[gm].materialised)
+      if (hg.pl.block_of[m] == B && family(hg, m) != family(hg, v)) return true;
+  }
+  return false;
+}
+
 static void fuse_epilogues(cg_graph* g) {
   HostGraph& hg = g->hg;
   const size_t NG = hg.groups.size();
@@ -568,22 +583,11 @@ static void fuse_epilogues(cg_graph* g) {
     // occupant may still be read there).  (A full-tensor chain operand sharing the
     // block is read at the same element, by the same thread, before the store.)
     {
+      // (from gd itself: the producer must not read the block it now writes -- its own
+      // input may have died at gd and left its block to the sink; a zero-copy CONCAT
+      // root takes any free block, without the in-place preference)
       const int B = hg.pl.block_of[E.sink];
-      bool clash = false;
-      if (B != hg.pl.block_of[d]) {
-        // from gd itself: the producer must not read the block it now writes (its own
-        // input may have died at gd and left its block to the sink -- a zero-copy
-        // CONCAT root takes any free block, without the in-place preference)
-        for (int gm = (int)gd; gm < ge && !clash; ++gm) {
-          // (other slices of the sink's zero-copy CONCAT family are disjoint: no clash)
-          for (int p : hg.groups[gm].inputs)
-            if (!hg.is_external(p) && hg.pl.block_of[p] == B && family(hg, p) != family(hg, E.sink)) clash = true;
-          if (gm == (int)gd) continue;
-          for (int m : hg.groups[gm].materialised)
-            if (hg.pl.block_of[m] == B && family(hg, m) != family(hg, E.sink)) clash = true;
-        }
-      }
-      if (clash) continue;
+      if (B != hg.pl.block_of[d] && moved_write_clashes(hg, B, E.sink, (int)gd, ge)) continue;
     }
     if (tc) {
       plan->epi = prog;
@@ -626,16 +630,7 @@ static void fuse_epilogues(cg_graph* g) {
           sn.attr.a1 != 3 || hg.nodes[dy].shape.size() != 4 || g->partner[gs] >= 0 || is_view(S.sink))
         continue;
       // the sum is written at gd's position: its block untouched by the groups in between
-      const int B = hg.pl.block_of[S.sink];
-      bool clash = false;
-      for (size_t gm = gd; gm < gs && !clash; ++gm) {
-        for (int p : hg.groups[gm].inputs)
-          if (!hg.is_external(p) && hg.pl.block_of[p] == B) clash = true;
-        if (gm == gd) continue;
-        for (int m : hg.groups[gm].materialised)
-          if (hg.pl.block_of[m] == B) clash = true;
-      }
-      if (clash) break;
+      if (moved_write_clashes(hg, hg.pl.block_of[S.sink], S.sink, (int)gd, (int)gs)) break;
       sl->aux = g->ptr[S.sink];
       if (!g->glaunch[gd].empty()) g->glaunch[gd].back().kernels += 1;  // (+ the bias partials' finalize)
       g->glaunch[gs].clear();
@@ -741,21 +736,7 @@ static void fuse_epilogues(cg_graph* g) {
     if (!ok || prev != E.sink) continue;
     {  // same block-clash rule as the DOT / CONV epilogues
       const int B = hg.pl.block_of[E.sink];
-      bool clash = false;
-      if (B != hg.pl.block_of[d]) {
-        // from gd itself: the producer must not read the block it now writes (its own
-        // input may have died at gd and left its block to the sink -- a zero-copy
-        // CONCAT root takes any free block, without the in-place preference)
-        for (int gm = (int)gd; gm < ge && !clash; ++gm) {
-          // (other slices of the sink's zero-copy CONCAT family are disjoint: no clash)
-          for (int p : hg.groups[gm].inputs)
-            if (!hg.is_external(p) && hg.pl.block_of[p] == B && family(hg, p) != family(hg, E.sink)) clash = true;
-          if (gm == (int)gd) continue;
-          for (int m : hg.groups[gm].materialised)
-            if (hg.pl.block_of[m] == B && family(hg, m) != family(hg, E.sink)) clash = true;
-        }
-      }
-      if (clash) continue;
+      if (B != hg.pl.block_of[d] && moved_write_clashes(hg, B, E.sink, (int)gd, ge)) continue;
     }
     cs.epi = prog;
     cs.out = g->ptr[E.sink];
