@@ -203,3 +203,42 @@ def test_c4_fused_gradients_under_partial_demand():
             assert np.array_equal(g.read(node), ref.read(node)), (it, node)
     g.destroy()
     ref.destroy()
+
+
+def test_epilogue_division_bit_identical_to_separate_kernel():
+    """The fused chains' DIV (C5's batch-norm x / sd) uses a branch-free Newton
+    quotient when every operand of a 16-value group is in range and __fdiv_rn
+    otherwise: the fused DOT epilogue equals the separate elementwise kernel bit for
+    bit, also with zeros, huge / tiny magnitudes and infinities in the data."""
+    rng = np.random.default_rng(17)
+    M, N, K = 640, 192, 96
+    a = rng.standard_normal((M, K)).astype(np.float32)
+    a[::7, :] *= np.float32(1e25)   # quotients out of the fast path's range
+    a[3, :] = 0.0
+    b = rng.standard_normal((K, N)).astype(np.float32)
+    sd = rng.uniform(0.5, 2.0, (N,)).astype(np.float32)
+    sd[5] = np.float32(1e-30)
+    sd[9] = np.float32(np.inf)
+    mean = rng.standard_normal((N,)).astype(np.float32)
+    res = []
+    for env in ({"CG_NO_EPILOGUE_FUSION": "1"}, {}):
+        old = os.environ.pop("CG_NO_EPILOGUE_FUSION", None)
+        os.environ.update(env)
+        try:
+            g = cg.Graph(0)
+            va, vb = g.var(a.shape), g.var(b.shape)
+            d = g.add_node("DOT", [va, vb], ta=0, tb=0)
+            out = g.add_node("RELU", [g.add_node("DIV", [g.add_node("SUB", [d, g.const(mean)]), g.const(sd)])])
+            info = g.plan_memory([out])
+            g.assign(va, a)
+            g.assign(vb, b)
+            g.eval([out])
+            res.append((g.read(out), info["n_fused"]))
+            g.destroy()
+        finally:
+            os.environ.pop("CG_NO_EPILOGUE_FUSION", None)
+            if old is not None:
+                os.environ["CG_NO_EPILOGUE_FUSION"] = old
+    (r0, n0), (r1, n1) = res
+    assert n1 == n0 + 1
+    assert np.array_equal(r0.view(np.uint32), r1.view(np.uint32))
