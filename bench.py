@@ -454,7 +454,12 @@ def run_c2(args):
 
     secondary = None
     if not args.no_secondary:
-        secondary = run_secondary(rank, world, local, max(5, args.steps), args)
+        try:  # (the C2 line above is printed whatever happens to the secondary configs)
+            secondary = run_secondary(rank, world, local, max(5, args.steps), args)
+        except Exception as exc:  # noqa: BLE001
+            import traceback
+            traceback.print_exc(file=sys.stderr)
+            secondary = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
     if rank == 0:
         pk = peaks()
@@ -530,7 +535,12 @@ def run_secondary(rank, world, local, iters, args):
             traceback.print_exc(file=sys.stderr)
             out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
             ok = False
-        torch.cuda.synchronize()
+        try:
+            torch.cuda.synchronize()
+        except Exception as exc:  # noqa: BLE001  (a sticky device error: no further device work here)
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+            out["skipped_after"] = name
+            break
         if not _all_ok(ok, world):
             out["skipped_after"] = name
             break
