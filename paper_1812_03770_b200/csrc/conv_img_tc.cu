@@ -1345,7 +1345,20 @@ CiKind kind_of(const ConvGeom& g, bool flip) {
 // per-column or scalar operands) and stores 32 channels per pixel with row stride
 // ldc.  Replaces the element-gather path of the generic conv (Ci = 3 is not a TMA
 // im2col box): 1.43 ms at batch 256 in round 1.
-constexpr int SB_THREADS = 576;  // 0-7 builders (2 groups), 8-15 epilogue (2 per lane quadrant), 16 producer, 17 MMA
+// Warps: builders (SB_BG groups of 4), epilogue (SB_EW per TMEM lane quadrant, COUT /
+// SB_EW channels each), producer, MMA.  With the fused batch-norm chain the epilogue
+// warps are busy the whole kernel (-DCG_SB_TIMING) while the builders wait 88 % of
+// the time, yet one builder group with four epilogue warps per quadrant measured the
+// same (467 vs 453 us): the defaults stay two and two.
+#ifndef CG_SB_BG
+#define CG_SB_BG 2
+#endif
+#ifndef CG_SB_EW
+#define CG_SB_EW 2
+#endif
+constexpr int SB_BG = CG_SB_BG, SB_EW = CG_SB_EW;
+constexpr int SB_EPI0 = 4 * SB_BG, SB_PROD = SB_EPI0 + 4 * SB_EW, SB_MMA = SB_PROD + 1;
+constexpr int SB_THREADS = (SB_MMA + 1) * 32;
 constexpr int SB_L = 6;
 constexpr int SB_NBUF = 4;  // band buffers: a band's copy latency exceeds its compute (measured with 2: 733 us)
 
@@ -1378,6 +1391,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
   float* bufs = reinterpret_cast<float*>(smem + Geo::B_BYTES);
   float* eops = bufs + SB_NBUF * BUF;                           // per-column chain operands [kEpiMax][COUT]
   float* ostage = eops + kEpiMax * COUT;                        // [4 quadrants][32 px][COUT + 4]: coalesced stores
+  static_assert(COUT % (16 * SB_EW) == 0 || (COUT / SB_EW) % 8 == 0, "epilogue channel split");
   uint64_t* bars = reinterpret_cast<uint64_t*>(ostage + 4 * 32 * (COUT + 4));
   const uint32_t bar0 = smem_u32(bars);
   constexpr int NBF = SB_NBUF;
@@ -1409,11 +1423,11 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int b = 0; b < NBF; ++b) {
       mbar_init(full(b), 1);
-      mbar_init(freeb(b), 8);
+      mbar_init(freeb(b), 4 * SB_BG);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull(b), 1);
-      mbar_init(tempty(b), 8);
+      mbar_init(tempty(b), 4 * SB_EW);
     }
     for (int l = 0; l < SB_L; ++l) {
       mbar_init(conv(l), 4);
@@ -1435,7 +1449,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
     eops[e] = epi.op[i] == EPI_RELU ? 0.f : (epi.scalar[i] ? __ldg(epi.x[i]) : __ldg(epi.x[i] + c));
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  if (warp == 17) {
+  if (warp == SB_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -1456,7 +1470,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
     *bytes = ((cnt + *shift) * 4 + 15) / 16 * 16;
   };
 
-  if (warp < 8) {
+  if (warp < SB_EPI0) {
     // ---------------- builders
     const int grp = warp / 4, wq = warp % 4, rr = wq * 32 + lane;
     int it = 0, j = 0;
@@ -1476,7 +1490,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
 #pragma unroll
         for (int kb = 0; kb < NKB; ++kb) {
           const int step = it + kb;
-          if ((step & 1) != grp) continue;
+          if (SB_BG == 2 && (step & 1) != grp) continue;
           const int l = step % SB_L;
           float v[32];
 #pragma unroll
@@ -1510,12 +1524,12 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(freeb(bsel));
     }
-  } else if (warp < 16) {
+  } else if (warp < SB_PROD) {
     // ---------------- epilogue: per tile, sum of the k-blocks' fresh accumulators
-    // (round to nearest), the fused chain, 16-byte stores.  Two warps per TMEM lane
-    // quadrant, each owning half of the output channels.
-    constexpr int CH = COUT / 2;
-    const int wq = warp % 4, half = (warp - 8) / 4, rr = wq * 32 + lane, c0 = half * CH;
+    // (round to nearest), the fused chain, 16-byte stores.  SB_EW warps per TMEM lane
+    // quadrant, each owning COUT / SB_EW of the output channels.
+    constexpr int CH = COUT / SB_EW;
+    const int wq = warp % 4, half = (warp - SB_EPI0) / 4, rr = wq * 32 + lane, c0 = half * CH;
     int it = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int n = u / NB, b = u % NB, npx = band_rows(b) * OW, T = (npx + 127) / 128;
@@ -1527,12 +1541,20 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
           const int bb = it & 1;
           SB_T(tw, mbar_wait(tfull(bb), (it >> 1) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if constexpr (CH % 16 == 0) {
 #pragma unroll
-          for (int cc = 0; cc < CH; cc += 16) {
-            float vv[16];
-            SB_T(tx1, tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(bb * Geo::ACC + c0 + cc), vv));
+            for (int cc = 0; cc < CH; cc += 16) {
+              float vv[16];
+              SB_T(tx1, tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(bb * Geo::ACC + c0 + cc), vv));
 #pragma unroll
-            for (int i = 0; i < 16; ++i) sum[cc + i] = NKB == 1 ? vv[i] : __fadd_rn(sum[cc + i], vv[i]);
+              for (int i = 0; i < 16; ++i) sum[cc + i] = NKB == 1 ? vv[i] : __fadd_rn(sum[cc + i], vv[i]);
+            }
+          } else {
+            static_assert(CH == 8, "8 or a multiple of 16 channels per epilogue warp");
+            float vv[8];
+            SB_T(tx1, tmem_ld8(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(bb * Geo::ACC + c0), vv));
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sum[i] = NKB == 1 ? vv[i] : __fadd_rn(sum[i], vv[i]);
           }
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
@@ -1554,16 +1576,16 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < CH; i += 4)
             *reinterpret_cast<float4*>(st + lane * (COUT + 4) + c0 + i) = make_float4(sum[i], sum[i + 1], sum[i + 2], sum[i + 3]);
-          SB_T(tx2, asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory"));
+          SB_T(tx2, asm volatile("bar.sync %0, %1;" ::"r"(1 + wq), "r"(32 * SB_EW) : "memory"));
           constexpr int Q4 = COUT / 4;  // float4 per pixel
 #pragma unroll
-          for (int k = 0; k < 32 * Q4 / 64; ++k) {
-            const int c = half * (32 * Q4 / 2) + k * 32 + lane, px = c / Q4, part = c % Q4;
+          for (int k = 0; k < 32 * Q4 / (32 * SB_EW); ++k) {
+            const int c = half * (32 * Q4 / SB_EW) + k * 32 + lane, px = c / Q4, part = c % Q4;
             if (px < nval)
               *reinterpret_cast<float4*>(out + (pix0 + px) * COUT + part * 4) =
                   *reinterpret_cast<const float4*>(st + px * (COUT + 4) + part * 4);
           }
-          asm volatile("bar.sync %0, 64;" ::"r"(1 + wq) : "memory");
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + wq), "r"(32 * SB_EW) : "memory");
         } else if (lane < nval) {
           float* o = out + (pix0 + lane) * ldc + c0;
 #pragma unroll
@@ -1571,7 +1593,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
         }
       }
     }
-  } else if (warp == 16) {
+  } else if (warp == SB_PROD) {
     // ---------------- producer: one bulk copy per band (double-buffered)
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -1621,7 +1643,7 @@ __global__ void __launch_bounds__(SB_THREADS, 1)
 #undef SB_T
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 17) {
+  if (warp == SB_MMA) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
