@@ -19,6 +19,14 @@ from workloads.gen import materialise, retag
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _single_stream(monkeypatch):
+    """These checks count launches, batched collectives and executor fusions of the
+    default single-stream capture (CG_STREAMS > 1 issues collectives unbatched and
+    leaves out the fusions whose side buffers the concurrent schedule cannot order)."""
+    monkeypatch.delenv("CG_STREAMS", raising=False)
+
+
 def _build(spec, nccl_id=None):
     g = cg.Graph(0, nccl_id=nccl_id)
     for rec in spec["nodes"]:

@@ -23,6 +23,14 @@ from workloads.gen import materialise, retag
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _single_stream(monkeypatch):
+    """These checks count launches, batched collectives and executor fusions of the
+    default single-stream capture (CG_STREAMS > 1 issues collectives unbatched and
+    leaves out the fusions whose side buffers the concurrent schedule cannot order)."""
+    monkeypatch.delenv("CG_STREAMS", raising=False)
+
+
 def _build_env(spec, env, flags=0):
     old = {k: os.environ.get(k) for k in env}
     os.environ.update({k: v for k, v in env.items() if v is not None})
