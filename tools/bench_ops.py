@@ -24,7 +24,8 @@ C5_CONVS = [  # (N, H, W, Ci, KH, KW, Co, stride, pad) of InceptionV3 at batch 2
     (256, 35, 35, 288, 1, 1, 64, 1, 1), (256, 35, 35, 64, 3, 3, 96, 1, 1), (256, 35, 35, 48, 5, 5, 64, 1, 1),
     (256, 17, 17, 768, 1, 1, 192, 1, 1), (256, 17, 17, 128, 1, 7, 128, 1, 1), (256, 147, 147, 32, 3, 3, 64, 1, 1),
     (256, 149, 149, 32, 3, 3, 32, 1, 0), (256, 299, 299, 3, 3, 3, 32, 2, 0),
-    (256, 17, 17, 192, 7, 1, 192, 1, 1), (256, 35, 35, 64, 3, 3, 96, 1, 1)]
+    (256, 17, 17, 192, 7, 1, 192, 1, 1), (256, 35, 35, 64, 3, 3, 96, 1, 1),
+    (256, 73, 73, 80, 3, 3, 192, 1, 0), (256, 73, 73, 64, 1, 1, 80, 1, 1)]
 
 
 def conv_main(a):
