@@ -136,7 +136,7 @@ typedef struct cg_plan_info {
   int32_t n_groups;          /* kernel groups in evaluation order Gamma */
   int32_t n_blocks;          /* shared pool blocks */
   int32_t n_kernels;         /* distinct generated kernels compiled */
-  int32_t n_fused;           /* elementwise groups computed inside another group's kernel (f2: DOT / CONV / pool epilogues, pool prologues) */
+  int32_t n_fused;           /* groups computed inside another group's kernel (f2: DOT / CONV / pool epilogues, pool prologues; sibling 1x1 convs merged into one GEMM) */
   uint64_t pool_bytes;       /* sum of align256(block bytes) */
   uint64_t plan_bytes;       /* sum of exact block bytes */
   uint64_t external_bytes;   /* Var + Const buffers */

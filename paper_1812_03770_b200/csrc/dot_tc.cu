@@ -127,7 +127,8 @@ template <bool GATHER, int BNT, int CG>
 __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, float* __restrict__ C,
                    int M, int N, int K, int a_mn, int b_mn, int kb_per_split, int splits, ConvA cv, int raw_hi,
-                   const __grid_constant__ EpiProg epi, float* __restrict__ dbg, int ldc) {
+                   const __grid_constant__ EpiProg epi, float* __restrict__ dbg, int ldc,
+                   const __grid_constant__ OutSegs segs) {
   using T = TC<BNT, CG, GATHER>;
   constexpr int BN = T::BN, SA = T::SA, SB = T::SB, LSTAGES = T::LSTAGES, BNH = BNT / CG;
   constexpr int TILE_A = T::TILE_A, TILE_B = T::TILE_B, LO_BYTES = T::LO_BYTES;
@@ -446,9 +447,15 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (int i = threadIdx.x - 192; i < epi.n * BN; i += 128) {
           const int e = i / BN, c = i - e * BN, col = n0 + c;
+          const float* xv = epi.x[e];
+          if (segs.n && col < N) {  // column-routed: the segment's own operand vector
+            int sg = 0;
+            while (sg + 1 < segs.n && col >= segs.col[sg + 1]) ++sg;
+            xv = segs.ex[sg][e] - segs.col[sg];
+          }
           es[i] = epi.op[e] == EPI_RELU || epi.scalar[e] == 2
                       ? 0.f
-                      : (epi.scalar[e] ? __ldg(epi.x[e]) : (col < N ? __ldg(epi.x[e] + col) : 0.f));
+                      : (epi.scalar[e] ? __ldg(epi.x[e]) : (col < N ? __ldg(xv + col) : 0.f));
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
       }
@@ -493,8 +500,17 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
         }
         if (row < M && n0 + c0 < N) {
           float* crow = Cz + (size_t)row * ldc;
-          const int n = n0 + c0;
-          if (vec && n + 16 <= N) {
+          int n = n0 + c0;
+          bool vseg = vec;
+          int nend = N;
+          if (segs.n) {  // column-routed: this chunk's segment (uniform across the warp)
+            int sg = 0;
+            while (sg + 1 < segs.n && n >= segs.col[sg + 1]) ++sg;
+            nend = sg + 1 < segs.n ? segs.col[sg + 1] : N;
+            crow = segs.C[sg] + (size_t)row * segs.ldc[sg] - segs.col[sg];
+            vseg = (segs.ldc[sg] % 4) == 0 && (reinterpret_cast<uintptr_t>(segs.C[sg]) & 15) == 0 && (segs.col[sg] % 4) == 0;
+          }
+          if (vseg && n + 16 <= nend) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               *reinterpret_cast<float4*>(crow + n + 4 * q) =
@@ -503,7 +519,7 @@ __global__ void __launch_bounds__(GATHER ? THREADS_GATHER : THREADS, 1)
           } else {
 #pragma unroll
             for (int q = 0; q < 16; ++q)
-              if (n + q < N) crow[n + q] = __uint_as_float(r[q]);
+              if (n + q < nend) crow[n + q] = __uint_as_float(r[q]);
           }
         }
       }
@@ -783,7 +799,7 @@ cudaError_t launch_tc(const DotTcPlan& p, float* out, cudaStream_t s) {
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<G, BNT, CG>, a, b, out, p.M, p.N, p.K, G ? 0 : p.a_mn, G ? 1 : p.b_mn,
                             p.kb_per_split, p.splits, p.conv, p.raw_hi, p.epi, p.dbg,
-                            p.splits > 1 || p.ldc <= 0 ? p.N : p.ldc);
+                            p.splits > 1 || p.ldc <= 0 ? p.N : p.ldc, p.segs);
 }
 
 template <bool G, int BNT>

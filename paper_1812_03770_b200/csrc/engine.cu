@@ -325,6 +325,11 @@ struct cg_graph {
   // max-pool backward group -> the forward pool group whose decisions it reads (-1:
   // none); demanding the backward demands the forward (its codes must be current)
   std::vector<int> code_dep;
+  // sibling 1x1 convs merged into one GEMM over concatenated weights: group -> its
+  // set (index into sib_sets; -1 none); demanding one member demands all
+  std::vector<int> sib_of;
+  std::vector<std::vector<int>> sib_sets;
+  int n_sib_merged = 0;
   std::vector<void*> code_bufs;
   // f3 fused AllReduce + update over peer memory (CG_PLAN_FUSED_COLL): per
   // ALLREDUCE group its segment (n == 0: none); device table = one entry per group
@@ -424,13 +429,17 @@ static inline int family(const HostGraph& hg, int v) {
 // plan gives B to v only at ge's: unless v slid into the producer's block, no group
 // in [gd, ge) may read B and none in (gd, ge) may write it (its previous occupant may
 // still be live there) -- other slices of v's zero-copy CONCAT family are disjoint.
-static bool moved_write_clashes(const HostGraph& hg, int B, int v, int gd, int ge) {
+// Values in never_written (fused-away intermediates: no kernel writes them, so
+// their "reads" touch nothing) are skipped when given.
+static bool moved_write_clashes(const HostGraph& hg, int B, int v, int gd, int ge,
+                                const std::vector<char>* never_written = nullptr) {
+  auto skip = [&](int x) { return never_written && (*never_written)[x]; };
   for (int gm = gd; gm < ge; ++gm) {
     for (int p : hg.groups[gm].inputs)
-      if (!hg.is_external(p) && hg.pl.block_of[p] == B && family(hg, p) != family(hg, v)) return true;
+      if (!hg.is_external(p) && !skip(p) && hg.pl.block_of[p] == B && family(hg, p) != family(hg, v)) return true;
     if (gm == gd) continue;
     for (int m : hg.groups[gm].materialised)
-      if (hg.pl.block_of[m] == B && family(hg, m) != family(hg, v)) return true;
+      if (!skip(m) && hg.pl.block_of[m] == B && family(hg, m) != family(hg, v)) return true;
   }
   return false;
 }
@@ -1131,6 +1140,113 @@ static int build_launches(cg_graph* g) {
     g->glaunch[gi].push_back(slice_copy(v));
     g->n_views_copied++;
   }
+  // 2a) sibling 1x1 convs (stride 1: GEMMs of the same input x, each
+  // with a few output channels) run as ONE GEMM over their concatenated weights
+  // with a column-routed epilogue: the A operand (x) is split into TF32 hi/lo once
+  // per output tile instead of once per sibling.  Const weights are concatenated once
+  // at planning; Var weights (re-assignable, update targets) by a copy launch before
+  // it.  Each segment's chain reads its own per-column operands.  Single-stream
+  // capture only; every member must be a split-free DOT-path plan with the same
+  // chain ops (per-column operands).
+  g->sib_of.assign(hg.groups.size(), -1);
+  g->sib_sets.clear();
+  g->n_sib_merged = 0;
+  {
+    const char* ns_env = getenv("CG_STREAMS");
+    const bool one_stream = !ns_env || atoi(ns_env) <= 1;
+    auto eligible = [&](size_t gi) -> bool {
+      auto& P = g->tcplan[gi];
+      if (!P || P->splits != 1 || P->band || P->conv.x || P->segs.n || g->glaunch[gi].empty()) return false;
+      const Node& nd = hg.nodes[hg.groups[gi].sink];
+      if (nd.op != CG_CONV2D || nd.attr.sh != 1 || nd.attr.sw != 1) return false;  // (1x1: SAME pads nothing)
+      const Shape& ws = hg.nodes[nd.preds[1]].shape;
+      if (ws[0] != 1 || ws[1] != 1 || !hg.is_external(nd.preds[1]) || (P->N % 16) != 0) return false;
+      for (int e = 0; e < P->epi.n; ++e)
+        if (P->epi.op[e] != EPI_RELU && P->epi.scalar[e] != 0) return false;
+      return true;
+    };
+    auto same_chain = [&](const DotTcPlan& a, const DotTcPlan& b) {
+      if (a.epi.n != b.epi.n) return false;
+      for (int e = 0; e < a.epi.n; ++e)
+        if (a.epi.op[e] != b.epi.op[e] || a.epi.swap[e] != b.epi.swap[e]) return false;
+      return true;
+    };
+    std::vector<char> used(hg.groups.size(), 0);
+    for (size_t lead = 0; lead < hg.groups.size() && one_stream && !getenv("CG_NO_SIBLING_GEMM"); ++lead) {
+      if (used[lead] || !eligible(lead)) continue;
+      const Node& ln = hg.nodes[hg.groups[lead].sink];
+      const DotTcPlan& LP = *g->tcplan[lead];
+      std::vector<int> set{(int)lead};
+      for (size_t gi = lead + 1; gi < hg.groups.size() && (int)set.size() < kOutSegMax; ++gi) {
+        if (used[gi] || !eligible(gi)) continue;
+        const Node& nd = hg.nodes[hg.groups[gi].sink];
+        const DotTcPlan& P = *g->tcplan[gi];
+        if (nd.preds[0] != ln.preds[0] || P.M != LP.M || P.K != LP.K || !same_chain(P, LP)) continue;
+        // the member's output is written at the lead's position
+        const int pg = g->partner[gi];
+        const int v = pg >= 0 && g->glaunch[pg].empty() ? hg.groups[pg].sink : hg.groups[gi].sink;
+        const int vend = pg >= 0 && g->glaunch[pg].empty() ? pg : (int)gi;
+        if (moved_write_clashes(hg, hg.pl.block_of[v], v, (int)lead, vend, &g->fused_away)) continue;
+        set.push_back((int)gi);
+      }
+      if (set.size() < 2) continue;
+      // merged plan
+      int Ntot = 0;
+      for (int m : set) Ntot += g->tcplan[m]->N;
+      const int K = LP.K, M = LP.M;
+      float* bcat = nullptr;
+      CUDA_TRY(g, cudaMalloc(&bcat, (size_t)K * Ntot * sizeof(float)), "cudaMalloc(sibling weights)");
+      g->code_bufs.push_back(bcat);
+      auto plan = std::make_shared<DotTcPlan>();
+      if (dot_tc_prepare(plan.get(), g->ptr[ln.preds[0]], bcat, LP.C, M, Ntot, K, 0, 0, g->ws, g->num_sms) != 0 ||
+          plan->splits != 1)
+        continue;  // (the merged shape would split K: keep the members separate)
+      ConcatArgs wcat{};
+      OutSegs sg{};
+      int col = 0;
+      for (int m : set) {
+        const DotTcPlan& P = *g->tcplan[m];
+        const Node& nd = hg.nodes[hg.groups[m].sink];
+        wcat.src[wcat.n] = g->ptr[nd.preds[1]];
+        wcat.inner[wcat.n] = P.N;
+        wcat.offset[wcat.n] = col;
+        wcat.n++;
+        for (int e = 0; e < P.epi.n; ++e) sg.ex[sg.n][e] = P.epi.x[e];
+        sg.col[sg.n] = col;
+        sg.C[sg.n] = P.C;
+        sg.ldc[sg.n] = P.ldc > 0 ? P.ldc : P.N;
+        sg.n++;
+        col += P.N;
+      }
+      plan->epi = LP.epi;
+      plan->segs = sg;
+      std::vector<Launch> L;
+      bool all_const = true;
+      for (int m : set) all_const = all_const && hg.nodes[hg.nodes[hg.groups[m].sink].preds[1]].op == CG_CONST;
+      if (all_const) {  // immutable after planning (uploaded by allocate): concatenated once, here
+        CUDA_TRY(g, launch_concat(wcat, bcat, K, Ntot, g->stream), "sibling weight concat");
+        CUDA_TRY(g, cudaStreamSynchronize(g->stream), "sibling weight concat");
+      } else {
+        L.push_back({[wcat, bcat, K, Ntot](cudaStream_t s) { return launch_concat(wcat, bcat, K, Ntot, s); }, 1});
+      }
+      L.push_back({[plan](cudaStream_t s) { return launch_dot_tc(*plan, s); }, 1});
+      // the lead's GEMM launch -> the copies + the merged GEMM; the members' GEMMs go
+      auto& LL = g->glaunch[lead];
+      LL.erase(LL.begin());
+      LL.insert(LL.begin(), L.begin(), L.end());
+      for (size_t k = 1; k < set.size(); ++k) {
+        auto& ML = g->glaunch[set[k]];
+        ML.erase(ML.begin());
+      }
+      g->tcplan[lead] = plan;
+      for (int m : set) {
+        used[m] = 1;
+        g->sib_of[m] = (int)g->sib_sets.size();
+      }
+      g->sib_sets.push_back(set);
+      g->n_sib_merged += (int)set.size() - 1;
+    }
+  }
   // 2b) f2 row runs (reduce -> broadcast fusion across groups, e.g. softmax)
   std::vector<KernelSpec> run_specs;
   g->runs.clear();
@@ -1781,7 +1897,7 @@ int cg_plan_memory(cg_graph* g, const cg_node* outputs, int32_t n_outputs, uint3
   g->info.n_groups = (int)hg.groups.size();
   g->info.n_blocks = (int)hg.pl.size.size();
   g->info.n_kernels = g->n_kernels;
-  g->info.n_fused = g->n_fused + g->n_pool_fused;
+  g->info.n_fused = g->n_fused + g->n_pool_fused + g->n_sib_merged;
   g->info.pool_bytes = hg.pl.pool_bytes;
   g->info.plan_bytes = hg.pl.plan_bytes;
   g->info.workspace_bytes = g->ws_floats * sizeof(float);
@@ -1850,6 +1966,11 @@ int cg_eval(cg_graph* g, const cg_node* outputs, int32_t n_outputs, const float*
     // a max-pool backward reading the forward's decisions: the forward runs too
     const int cd = g->code_dep.empty() ? -1 : g->code_dep[gi];
     if (cd >= 0 && !R[cd]) demand(hg.groups[cd].sink, true);
+    // merged sibling GEMMs: the lead's launch writes every member's output
+    const int ss = g->sib_of.empty() ? -1 : g->sib_of[gi];
+    if (ss >= 0)
+      for (int m : g->sib_sets[ss])
+        if (!R[m]) demand(hg.groups[m].sink, true);
   };
   for (int r : roots) demand(r, false);
   for (;;) {  // clobber fix-point: a group may not read a block another launched group overwrote
