@@ -314,6 +314,14 @@ def _barrier(world):
         dist.barrier()
 
 
+def _launches_of(g, fn):
+    """Kernel launches of ONE step (counted by the engine around a single extra call,
+    so warm-up and load-phase steps do not enter the figure)."""
+    l0 = g.launch_count()
+    fn(0)
+    return g.launch_count() - l0
+
+
 def _timed(ws, fn, iters, world, local, min_s=0.6):
     """Warm-up, a load phase of >= 0.3 s (so the sampled clocks are this kernel
     mix's clocks), then `iters` steps (raised to fill >= min_s) timed with CUDA
@@ -646,9 +654,8 @@ def _sec_train(name, gb, weak):
         for i, t in staged[k % 4].items():
             g.assign(i, t)
         g.eval(outs, cg.EVAL_FULL)
-    l0 = g.launch_count()
     ms, clk, n = _timed(ws, step, _CTX["iters"], world, local)
-    launches_per_iter = (g.launch_count() - l0) / max(1, n)
+    launches_per_iter = _launches_of(g, step)
     flops = graph_flops(g, spec)
     traffic = plan_traffic_bytes(g)
     ms_s = ms * 1e-3
@@ -693,9 +700,8 @@ def _sec_c5():
     info = g.plan_memory(outs, 0)
     build_s = time.perf_counter() - t0
     ws = torch.cuda.ExternalStream(g.work_stream(), device=dev)
-    l0 = g.launch_count()
     ms, clk, n = _timed(ws, lambda k: g.eval(outs, cg.EVAL_FULL), max(2, _CTX["iters"] // 4), world, local)
-    launches = (g.launch_count() - l0) / max(1, n)
+    launches = _launches_of(g, lambda k: g.eval(outs, cg.EVAL_FULL))
     peak = info["pool_bytes"] + info["external_bytes"] + info["workspace_bytes"]
     unshared = info["unshared_bytes"] + info["external_bytes"]
     flops = graph_flops(g, spec)
