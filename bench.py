@@ -361,7 +361,7 @@ def _timed(ws, fn, iters, world, local, min_s=0.6):
 
 
 # ---------------------------------------------------------------------------- CUDA arm: C2 (primary)
-E2E_CHUNKS = 8  # row slices of the streamed end-to-end step
+E2E_CHUNKS = int(os.environ.get("CG_E2E_CHUNKS", "8"))  # row slices of the streamed end-to-end step
 
 
 def build_c2(rows_local, row0, local, stream=None):
